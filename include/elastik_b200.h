@@ -1,0 +1,107 @@
+/*
+ * elastik_b200.h -- C ABI of the B200-native elastic-distance engine
+ * (libelastik_b200.so).  Plain pointers and sizes only.
+ *
+ * It replaces the reference package's native seam and the Python loops above it:
+ *
+ *   ek_distance_batch  <- elastik._speedups.run (pkg/src/elastik/_speedups.pyx:274-317),
+ *                         called per pair by engines._dispatch (pkg/src/elastik/engines.py:29-57)
+ *                         behind engines.distance / compute_* (engines.py:60-147)
+ *   ek_nn              <- search.nn_search / classify_1nn (pkg/src/elastik/search.py:81-160)
+ *   ek_pairwise        <- the all-pairs loop of distance(spec, "pruned_only", X[i], X[j])
+ *                         (compute_pruned_only, engines.py:106-118)
+ *   ek_subseq          <- search.subsequence_search + series.znormalize
+ *                         (pkg/src/elastik/search.py:163-215, series.py:118-131)
+ *
+ * Conventions
+ *   - kind codes follow elastik.kernels.KINDS (kernels.py:22): 0 dtw, 1 cdtw, 2 wdtw,
+ *     3 erp, 4 msm, 5 twe; cost_mode 0 squared, 1 absolute (engines.py:20-21).
+ *   - variant codes follow engines.VARIANTS (engines.py:18): 0 base, 1 ea, 2 eapruned,
+ *     3 pruned_only.
+ *   - series are float64, concatenated in one buffer; offsets/lengths are int64.
+ *     Inputs are validated by the caller exactly like series.as_series
+ *     (non-empty, 1-D, finite; series.py:19-31).
+ *   - An abandoned pair or an infeasible window is +inf, never an error
+ *     (SPEC.md:552).  Functions return 0 on success, < 0 on error, with the
+ *     message in ek_last_error().
+ *   - WDTW weights are host-computed (kernels.py:80-92, libm exp): the table for
+ *     longest length m (m+1 entries) starts at wdtw_tables[wdtw_table_off[m]]
+ *     for every m a call needs (offsets -1 elsewhere), m <= wdtw_max_len.
+ *   - All calls are synchronous on the library's stream unless noted (_dev
+ *     variants take device pointers and an explicit cudaStream_t as void*).
+ */
+#ifndef ELASTIK_B200_H
+#define ELASTIK_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ek_spec {
+  int32_t kind;          /* KINDS index */
+  int32_t cost_mode;     /* 0 squared, 1 absolute */
+  int64_t window;        /* Sakoe-Chiba half-width, < 0 means None (unbounded) */
+  double erp_gap;
+  double msm_c;
+  double twe_nu;
+  double twe_lambda;
+  const double* wdtw_tables;     /* host (or device for _dev calls) */
+  const int64_t* wdtw_table_off; /* indexed by longest length m */
+  int64_t wdtw_max_len;
+} ek_spec;
+
+/* status / diagnostics */
+const char* ek_last_error(void);
+int ek_device_count(void);
+int ek_init(int device);
+const char* ek_version(void);
+
+/* One distance per pair (s_i, t_i) with its own cutoff (engines.distance).
+ * windows: per-pair explicit window (engines.compute_ea/eapruned's `window`
+ * argument) or NULL to use spec->window.  out_cells: band cells the GPU engine
+ * evaluated (schedule-specific). */
+int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, const double* series,
+                      int64_t series_len, const int64_t* s_off, const int64_t* s_len, const int64_t* t_off,
+                      const int64_t* t_len, const double* cutoffs, const int64_t* windows, double* out_cost,
+                      int64_t* out_cells);
+
+/* 1-NN of every query against the candidates (nn_search per query, lb="none").
+ * nn_idx = -1 when every candidate is +inf.  computed/abandoned/cells per query. */
+int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,
+          const int64_t* q_len, int64_t n_queries, const double* cands, int64_t c_total, const int64_t* c_off,
+          const int64_t* c_len, int64_t n_cands, int64_t* nn_idx, double* nn_dist, int64_t* cells,
+          int64_t* computed, int64_t* abandoned);
+
+/* Same with device-resident inputs/outputs (lengths as int32, offsets int64) on `stream`. */
+int ek_nn_dev(const ek_spec* spec, int32_t variant, const double* d_queries, const int64_t* d_q_off,
+              const int32_t* d_q_len, int64_t n_queries, const double* d_cands, const int64_t* d_c_off,
+              const int32_t* d_c_len, int64_t n_cands, int32_t max_len, int64_t* d_nn_idx, double* d_nn_dist,
+              int64_t* d_cells, int64_t* d_computed, int64_t* d_abandoned, void* stream);
+
+/* Full symmetric matrix D[n*n] of distance(spec, variant, X_i, X_j); diagonal 0.0.
+ * cells: total band cells evaluated. */
+int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int64_t total, const int64_t* off,
+                const int64_t* len, int64_t n, double* D, int64_t* cells);
+
+int ek_pairwise_dev(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
+                    const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells, void* stream);
+
+/* Best window of `reference` against `query` (dtw/cdtw), every stride-1 offset,
+ * z-normalising the query once and each window on the fly when normalize != 0.
+ * Ties keep the lowest offset; best_off = -1 when every window is +inf. */
+int ek_subseq(const ek_spec* spec, int32_t variant, const double* query, int64_t lq, const double* reference,
+              int64_t n_ref, int32_t normalize, int64_t* best_off, double* best_dist, int64_t* cells,
+              int64_t* computed, int64_t* abandoned);
+
+int ek_subseq_dev(const ek_spec* spec, int32_t variant, const double* d_query, int64_t lq,
+                  const double* d_reference, int64_t n_ref, int32_t normalize, int64_t* best_off,
+                  double* best_dist, int64_t* cells, int64_t* computed, int64_t* abandoned, void* stream);
+
+/* Number of kernel launches the library issued since the last reset (bench accounting). */
+int64_t ek_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELASTIK_B200_H */

@@ -1,0 +1,735 @@
+// ek_api.cu -- the C ABI (include/elastik_b200.h): argument handling, engine
+// selection, device buffers and kernel launches.  No arithmetic of the distance
+// path happens on the host except what the reference itself does there: WDTW
+// weight tables (libm exp, kernels.py:80-92) arrive precomputed from the caller.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/elastik_b200.h"
+#include "ek_launch.cuh"
+#include "ek_misc.cuh"
+#include "ek_subseq.cuh"
+
+namespace ekb {
+template <int K> PairsFn get_pairs(int, int);
+template <int K> TriFn get_triangle(int, int);
+template <int K> NNFn get_nn(int, int);
+template <int K> UBFn get_ub(int);
+extern template PairsFn get_pairs<K_DTW>(int, int);
+extern template PairsFn get_pairs<K_WDTW>(int, int);
+extern template PairsFn get_pairs<K_ERP>(int, int);
+extern template PairsFn get_pairs<K_MSM>(int, int);
+extern template PairsFn get_pairs<K_TWE>(int, int);
+extern template TriFn get_triangle<K_DTW>(int, int);
+extern template TriFn get_triangle<K_WDTW>(int, int);
+extern template TriFn get_triangle<K_ERP>(int, int);
+extern template TriFn get_triangle<K_MSM>(int, int);
+extern template TriFn get_triangle<K_TWE>(int, int);
+extern template NNFn get_nn<K_DTW>(int, int);
+extern template NNFn get_nn<K_WDTW>(int, int);
+extern template NNFn get_nn<K_ERP>(int, int);
+extern template NNFn get_nn<K_MSM>(int, int);
+extern template NNFn get_nn<K_TWE>(int, int);
+extern template UBFn get_ub<K_DTW>(int);
+extern template UBFn get_ub<K_WDTW>(int);
+extern template UBFn get_ub<K_ERP>(int);
+extern template UBFn get_ub<K_MSM>(int);
+extern template UBFn get_ub<K_TWE>(int);
+}  // namespace ekb
+
+using namespace ekb;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return -1;
+}
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) return fail("%s failed: %s", #x, cudaGetErrorString(e_));    \
+  } while (0)
+
+struct Ctx {
+  bool ready = false;
+  int dev = 0;
+  int nsm = 0;
+  cudaStream_t stream = nullptr;
+};
+Ctx g_ctx;
+std::mutex g_mu;
+
+int ensure_ctx() {
+  if (g_ctx.ready) return 0;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail("no CUDA device available");
+  CK(cudaSetDevice(g_ctx.dev));
+  cudaDeviceProp pr;
+  CK(cudaGetDeviceProperties(&pr, g_ctx.dev));
+  if (pr.major < 10) return fail("device %d is sm_%d%d; this library is built for sm_100a", g_ctx.dev, pr.major, pr.minor);
+  g_ctx.nsm = pr.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking));
+  g_ctx.ready = true;
+  return 0;
+}
+
+// RAII stream-ordered device allocation
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  ~DBuf() { if (p) cudaFreeAsync(p, s); }
+  int alloc(size_t bytes, cudaStream_t st) {
+    s = st;
+    if (bytes == 0) bytes = 8;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) return fail("cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    return 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+template <class Fn, class... Args>
+int launch_persistent(Fn fn, int block, size_t smem, cudaStream_t st, long long warp_units, Args... args) {
+  if (!fn) return fail("no kernel instantiated for this configuration");
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+  if (per_sm < 1) return fail("kernel does not fit on an SM (smem %zu bytes)", smem);
+  const int wpb = block / 32;
+  long long want = (warp_units + wpb - 1) / wpb;
+  long long grid = std::min<long long>((long long)g_ctx.nsm * per_sm, std::max<long long>(1, want));
+  fn<<<(unsigned)grid, block, smem, st>>>(args...);
+  ++g_launches;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+template <class Fn, class... Args>
+int launch_plain(Fn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fn<<<grid, block, smem, st>>>(args...);
+  ++g_launches;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// 1-D lexicographic (distance, position) reduction + stats (subsequence search)
+__global__ void k_red1_partial(const double* __restrict__ d, const int* __restrict__ tend, long long n, int lq,
+                               int w, int eng_diag, int S, double* pd, long long* pi, long long* pc,
+                               long long* pa, long long* pcl) {
+  double bd = __longlong_as_double(0x7ff0000000000000LL);
+  long long bi = 0x7fffffffffffffffLL, nc = 0, na = 0, cl = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = d[i];
+    if (tend[i] > 0) cl += cells_done(eng_diag, S, 1, lq, lq, w, tend[i]);
+    if (v < __longlong_as_double(0x7ff0000000000000LL)) {
+      ++nc;
+      if (v < bd || (v == bd && i < bi)) { bd = v; bi = i; }
+    } else {
+      ++na;
+    }
+  }
+  __shared__ double sd[256];
+  __shared__ long long si[256], s1[256], s2[256], s3[256];
+  sd[threadIdx.x] = bd; si[threadIdx.x] = bi; s1[threadIdx.x] = nc; s2[threadIdx.x] = na; s3[threadIdx.x] = cl;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double od = sd[threadIdx.x + s];
+      const long long oi = si[threadIdx.x + s];
+      if (od < sd[threadIdx.x] || (od == sd[threadIdx.x] && oi < si[threadIdx.x])) { sd[threadIdx.x] = od; si[threadIdx.x] = oi; }
+      s1[threadIdx.x] += s1[threadIdx.x + s];
+      s2[threadIdx.x] += s2[threadIdx.x + s];
+      s3[threadIdx.x] += s3[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pd[blockIdx.x] = sd[0]; pi[blockIdx.x] = si[0]; pc[blockIdx.x] = s1[0]; pa[blockIdx.x] = s2[0]; pcl[blockIdx.x] = s3[0];
+  }
+}
+
+int kind_tag(int kind) { return kind == K_CDTW ? K_DTW : kind; }
+
+PairsFn pick_pairs(int kind, int mode, int eng) {
+  switch (kind_tag(kind)) {
+    case K_DTW: return get_pairs<K_DTW>(mode, eng);
+    case K_WDTW: return get_pairs<K_WDTW>(mode, eng);
+    case K_ERP: return get_pairs<K_ERP>(mode, eng);
+    case K_MSM: return get_pairs<K_MSM>(mode, eng);
+    case K_TWE: return get_pairs<K_TWE>(mode, eng);
+  }
+  return nullptr;
+}
+TriFn pick_tri(int kind, int mode, int eng) {
+  switch (kind_tag(kind)) {
+    case K_DTW: return get_triangle<K_DTW>(mode, eng);
+    case K_WDTW: return get_triangle<K_WDTW>(mode, eng);
+    case K_ERP: return get_triangle<K_ERP>(mode, eng);
+    case K_MSM: return get_triangle<K_MSM>(mode, eng);
+    case K_TWE: return get_triangle<K_TWE>(mode, eng);
+  }
+  return nullptr;
+}
+NNFn pick_nn(int kind, int mode, int eng) {
+  switch (kind_tag(kind)) {
+    case K_DTW: return get_nn<K_DTW>(mode, eng);
+    case K_WDTW: return get_nn<K_WDTW>(mode, eng);
+    case K_ERP: return get_nn<K_ERP>(mode, eng);
+    case K_MSM: return get_nn<K_MSM>(mode, eng);
+    case K_TWE: return get_nn<K_TWE>(mode, eng);
+  }
+  return nullptr;
+}
+UBFn pick_ub(int kind, int mode) {
+  switch (kind_tag(kind)) {
+    case K_DTW: return get_ub<K_DTW>(mode);
+    case K_WDTW: return get_ub<K_WDTW>(mode);
+    case K_ERP: return get_ub<K_ERP>(mode);
+    case K_MSM: return get_ub<K_MSM>(mode);
+    case K_TWE: return get_ub<K_TWE>(mode);
+  }
+  return nullptr;
+}
+
+// Engine for a (lines, cols, window) shape; -1 if unsupported.
+int choose_engine(int nl, int nc, int w, bool ea_rows) {
+  if (ea_rows) return nc <= 512 ? E_STR16_EA : -1;
+  const int slots = diag_slots_needed(nl, nc, w);
+  if (slots <= 128) return E_DIAG4;
+  if (slots <= 256) return E_DIAG8;
+  const bool banded = w < nl - 1;
+  if (!banded) {
+    if (nc <= 128) return E_STR4;
+    if (nc <= 256) return E_STR8;
+    if (nc <= 512) return E_STR16;
+  }
+  if (slots <= 512) return E_DIAG16;
+  if (nc <= 512) return E_STRB16;
+  return -1;
+}
+int eng_S(int e) { return engine_S(e); }
+
+int check_spec(const ek_spec* sp) {
+  if (!sp) return fail("spec is NULL");
+  if (sp->kind < 0 || sp->kind > 5) return fail("unknown distance kind code %d", sp->kind);
+  if (sp->cost_mode != 0 && sp->cost_mode != 1) return fail("unknown cost mode code %d", sp->cost_mode);
+  if (sp->kind == K_WDTW && (!sp->wdtw_tables || !sp->wdtw_table_off))
+    return fail("wdtw requires weight tables");
+  return 0;
+}
+
+// Upload the WDTW tables the call needs (host -> device) and fill Params.
+struct ParamHolder {
+  DBuf tabs, offs;
+  Params prm{};
+  int init(const ek_spec* sp, cudaStream_t st) {
+    prm.gap = sp->erp_gap;
+    prm.msm_c = sp->msm_c;
+    prm.nu = sp->twe_nu;
+    prm.lam = sp->twe_lambda;
+    prm.wt_all = nullptr;
+    prm.wt_off = nullptr;
+    prm.wt = nullptr;
+    prm.wt_len = 0;
+    if (sp->kind != K_WDTW) return 0;
+    const long long m = sp->wdtw_max_len;
+    long long total = 0;
+    for (long long k = 0; k <= m; ++k)
+      if (sp->wdtw_table_off[k] >= 0) total = std::max(total, (long long)sp->wdtw_table_off[k] + k + 1);
+    if (tabs.alloc(sizeof(double) * (size_t)total, st) || offs.alloc(sizeof(long long) * (size_t)(m + 1), st)) return -1;
+    CK(cudaMemcpyAsync(tabs.p, sp->wdtw_tables, sizeof(double) * (size_t)total, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(offs.p, sp->wdtw_table_off, sizeof(long long) * (size_t)(m + 1), cudaMemcpyHostToDevice, st));
+    prm.wt_all = tabs.as<double>();
+    prm.wt_off = offs.as<long long>();
+    return 0;
+  }
+};
+
+size_t pair_smem(int lmax, int wpb) { return sizeof(double) * (size_t)wpb * (2 * (lmax + 2) + (lmax + 1)); }
+
+// numpy pairwise-sum plan (see ek_subseq.cuh)
+void np_plan_rec(int start, int n, std::vector<int2>& leaves, std::vector<int>& ops) {
+  if (n <= 128) {
+    ops.push_back((int)leaves.size());
+    leaves.push_back(make_int2(start, n));
+    return;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  np_plan_rec(start, n2, leaves, ops);
+  np_plan_rec(start + n2, n - n2, leaves, ops);
+  ops.push_back(-1);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ek_last_error(void) { return g_err.c_str(); }
+const char* ek_version(void) { return "elastik_b200 0.1 (sm_100a)"; }
+long long ek_launch_count_impl(int reset) {
+  long long v = g_launches.load();
+  if (reset) g_launches = 0;
+  return v;
+}
+int64_t ek_launch_count(int32_t reset) { return (int64_t)ek_launch_count_impl(reset); }
+
+int ek_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int ek_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ctx.ready && g_ctx.dev == device) return 0;
+  g_ctx.ready = false;
+  g_ctx.dev = device;
+  return ensure_ctx();
+}
+
+int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, const double* series,
+                      int64_t series_len, const int64_t* s_off, const int64_t* s_len, const int64_t* t_off,
+                      const int64_t* t_len, const double* cutoffs, const int64_t* windows, double* out_cost,
+                      int64_t* out_cells) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx() || check_spec(spec)) return -1;
+  if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
+  if (n_pairs <= 0) return 0;
+  cudaStream_t st = g_ctx.stream;
+  // host-side orientation / window / variant semantics (engines.py:121-147, kernels.py:168-171)
+  std::vector<std::vector<PairDesc>> groups(E_COUNT);
+  std::vector<std::vector<long long>> gidx(E_COUNT);
+  std::vector<int> glmax(E_COUNT, 0);
+  for (int64_t p = 0; p < n_pairs; ++p) {
+    const bool swap = t_len[p] > s_len[p];
+    PairDesc pd{};
+    pd.xoff = swap ? t_off[p] : s_off[p];
+    pd.yoff = swap ? s_off[p] : t_off[p];
+    pd.nl = (int)(swap ? t_len[p] : s_len[p]);
+    pd.nc = (int)(swap ? s_len[p] : t_len[p]);
+    const long long win = windows ? windows[p] : spec->window;
+    int w = win < 0 ? pd.nl : (int)std::min<long long>(win, 1LL << 30);
+    double cut = cutoffs ? cutoffs[p] : INFINITY;
+    bool ea_rows = false;
+    out_cells[p] = 0;
+    out_cost[p] = INFINITY;
+    if (variant == 0) {  // base: compute_base (no window) or compute_ea(window, inf)
+      cut = INFINITY;
+      if (spec->window < 0 && !windows) w = pd.nl;
+    } else if (variant == 1) {  // ea: row abandoning; NaN never abandons
+      if (std::isnan(cut)) cut = INFINITY;
+      if (cut == 0.0) cut = 0.0;  // canonical +0.0
+      ea_rows = cut != INFINITY;
+    } else if (variant == 2) {  // eapruned: nothing is <= NaN
+      if (std::isnan(cut)) cut = -INFINITY;
+      if (cut == 0.0) cut = 0.0;
+    } else {  // pruned_only == base on a feasible window
+      cut = INFINITY;
+    }
+    if (w < pd.nl - pd.nc) continue;  // infeasible window: (+inf, 0)
+    pd.w = w;
+    pd.cut = cut;
+    const int eng = choose_engine(pd.nl, pd.nc, w, ea_rows);
+    if (eng < 0) return fail("series of length %d x %d with window %d exceed this build's engines", pd.nl, pd.nc, w);
+    groups[eng].push_back(pd);
+    gidx[eng].push_back(p);
+    glmax[eng] = std::max(glmax[eng], pd.nl);
+  }
+  DBuf dser;
+  if (dser.alloc(sizeof(double) * (size_t)series_len, st)) return -1;
+  CK(cudaMemcpyAsync(dser.p, series, sizeof(double) * (size_t)series_len, cudaMemcpyHostToDevice, st));
+  ParamHolder ph;
+  if (ph.init(spec, st)) return -1;
+  for (int eng = 0; eng < E_COUNT; ++eng) {
+    const size_t n = groups[eng].size();
+    if (!n) continue;
+    DBuf dp, dc, dt, dcl;
+    if (dp.alloc(sizeof(PairDesc) * n, st) || dc.alloc(sizeof(double) * n, st) || dt.alloc(sizeof(int) * n, st) ||
+        dcl.alloc(sizeof(long long) * n, st))
+      return -1;
+    CK(cudaMemcpyAsync(dp.p, groups[eng].data(), sizeof(PairDesc) * n, cudaMemcpyHostToDevice, st));
+    const int wpb = 4;
+    const size_t smem = pair_smem(glmax[eng], wpb);
+    if (launch_persistent(pick_pairs(spec->kind, spec->cost_mode, eng), 32 * wpb, smem, st, (long long)n,
+                          (const double*)dser.as<double>(), (const PairDesc*)dp.as<PairDesc>(), (int)n,
+                          glmax[eng], ph.prm, dc.as<double>(), dt.as<int>()))
+      return -1;
+    if (launch_plain(k_cells_pairs, dim3((unsigned)std::min<size_t>(1024, (n + 255) / 256)), dim3(256), 0, st,
+                     (const PairDesc*)dp.as<PairDesc>(), (const int*)dt.as<int>(), (int)n,
+                     (int)engine_is_diag(eng), eng_S(eng), kind_tag(spec->kind) == K_ERP ? 0 : 1,
+                     dcl.as<long long>()))
+      return -1;
+    std::vector<double> hc(n);
+    std::vector<long long> hcl(n);
+    CK(cudaMemcpyAsync(hc.data(), dc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hcl.data(), dcl.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t k = 0; k < n; ++k) {
+      out_cost[gidx[eng][k]] = hc[k];
+      out_cells[gidx[eng][k]] = hcl[k];
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, const int64_t* dqoff,
+                       const int32_t* dqlen, int64_t nq, const double* dC, const int64_t* dcoff, const int32_t* dclen,
+                       int64_t ncand, int32_t max_len, int64_t* d_idx, double* d_dist, int64_t* d_cells,
+                       int64_t* d_comp, int64_t* d_ab, cudaStream_t st) {
+  if (check_spec(spec)) return -1;
+  if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
+  if (nq <= 0) return 0;
+  if (ncand <= 0) return fail("candidate set is empty");
+  const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
+  const int wmax = win < 0 ? max_len : win;
+  const int eng = choose_engine(max_len, max_len, wmax, false);
+  if (eng < 0) return fail("series length %d with window %d exceeds this build's engines", max_len, wmax);
+  const bool share = variant == 1 || variant == 2;  // base / pruned_only compute every candidate exactly
+  ParamHolder ph;
+  if (ph.init(spec, st)) return -1;
+  const long long npairs = (long long)nq * ncand;
+  DBuf dord, dkeys, dout, dtend, dcut, dcnt;
+  if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dout.alloc(sizeof(double) * (size_t)npairs, st) ||
+      dtend.alloc(sizeof(int) * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
+      dcnt.alloc(sizeof(int) * 4 * 2, st))
+    return -1;
+  CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 8, st));
+  // 1. candidate order: approximate Euclidean ranking (scheduling only)
+  const bool rank = share && ncand <= 16384 && ncand > 1;
+  if (rank) {
+    if (dkeys.alloc(sizeof(float) * (size_t)npairs, st)) return -1;
+    if (launch_plain(k_rank_dist, dim3((unsigned)((ncand + 31) / 32), (unsigned)((nq + 31) / 32)), dim3(256), 0, st,
+                     dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC, (const long long*)dcoff,
+                     (const int*)dclen, (int)ncand, dkeys.as<float>()))
+      return -1;
+    int np2 = 1;
+    while (np2 < ncand) np2 <<= 1;
+    if (launch_plain(k_rank_sort, dim3((unsigned)nq), dim3(1024), (size_t)np2 * 8, st, (const float*)dkeys.as<float>(),
+                     (int)ncand, np2, dord.as<int>()))
+      return -1;
+  } else {
+    if (launch_plain(k_identity_order, dim3(1024), dim3(256), 0, st, (int)nq, (int)ncand, dord.as<int>())) return -1;
+  }
+  // 2. cutoff seed: exact diagonal upper bound of each query's top-ranked candidate
+  if (share) {
+    if (launch_plain(pick_ub(spec->kind, spec->cost_mode), dim3((unsigned)((nq + 127) / 128)), dim3(128), 0, st, dQ,
+                     (const long long*)dqoff, (const int*)dqlen, (int)nq, dC, (const long long*)dcoff,
+                     (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), win, ph.prm,
+                     dcut.as<unsigned long long>()))
+      return -1;
+  } else {
+    if (launch_plain(k_fill_u64, dim3(64), dim3(256), 0, st, dcut.as<unsigned long long>(), (long long)nq,
+                     0x7ff0000000000000ULL))
+      return -1;
+  }
+  // 3. phase A: the top-ranked few per query; phase B: everything else
+  const NNFn fn = pick_nn(spec->kind, spec->cost_mode, eng);
+  const int wpb = 4;
+  const size_t smem = pair_smem(max_len, wpb);
+  const int ka = share ? (int)std::min<int64_t>(4, ncand) : 0;
+  if (ka > 0) {
+    if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
+                          (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
+                          (const int*)dord.as<int>(), 0, ka, 1, win, (int)max_len, ph.prm, (int)share,
+                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>()))
+      return -1;
+  }
+  if (ka < ncand) {
+    const int K = 32;
+    const long long items = (long long)nq * ((ncand - ka + K - 1) / K);
+    if (launch_persistent(fn, 32 * wpb, smem, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
+                          (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), ka,
+                          (int)ncand, K, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
+                          dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
+      return -1;
+  }
+  // 4. lexicographic (distance, index) minimum + accounting
+  if (launch_plain(k_nn_reduce, dim3((unsigned)nq), dim3(256), 0, st, (const double*)dout.as<double>(),
+                   (const int*)dtend.as<int>(), (const int*)dqlen, (int)nq, (const int*)dclen, (int)ncand, win,
+                   (int)engine_is_diag(eng), eng_S(eng), kind_tag(spec->kind) == K_ERP ? 0 : 1,
+                   (long long*)d_idx, d_dist, (long long*)d_cells, (long long*)d_comp, (long long*)d_ab))
+    return -1;
+  return 0;
+}
+
+int ek_nn_dev(const ek_spec* spec, int32_t variant, const double* d_queries, const int64_t* d_q_off,
+              const int32_t* d_q_len, int64_t n_queries, const double* d_cands, const int64_t* d_c_off,
+              const int32_t* d_c_len, int64_t n_cands, int32_t max_len, int64_t* d_nn_idx, double* d_nn_dist,
+              int64_t* d_cells, int64_t* d_computed, int64_t* d_abandoned, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
+  return nn_dev_impl(spec, variant, d_queries, d_q_off, d_q_len, n_queries, d_cands, d_c_off, d_c_len, n_cands,
+                     max_len, d_nn_idx, d_nn_dist, d_cells, d_computed, d_abandoned, st);
+}
+
+int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,
+          const int64_t* q_len, int64_t n_queries, const double* cands, int64_t c_total, const int64_t* c_off,
+          const int64_t* c_len, int64_t n_cands, int64_t* nn_idx, double* nn_dist, int64_t* cells,
+          int64_t* computed, int64_t* abandoned) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  if (n_queries <= 0) return 0;
+  cudaStream_t st = g_ctx.stream;
+  std::vector<int32_t> ql(n_queries), cl(n_cands);
+  int32_t mx = 0;
+  for (int64_t k = 0; k < n_queries; ++k) mx = std::max(mx, ql[k] = (int32_t)q_len[k]);
+  for (int64_t k = 0; k < n_cands; ++k) mx = std::max(mx, cl[k] = (int32_t)c_len[k]);
+  DBuf dq, dqo, dql, dc, dco, dcl, dout;
+  if (dq.alloc(sizeof(double) * q_total, st) || dqo.alloc(8 * n_queries, st) || dql.alloc(4 * n_queries, st) ||
+      dc.alloc(sizeof(double) * c_total, st) || dco.alloc(8 * std::max<int64_t>(1, n_cands), st) ||
+      dcl.alloc(4 * std::max<int64_t>(1, n_cands), st) || dout.alloc(8 * 5 * n_queries, st))
+    return -1;
+  CK(cudaMemcpyAsync(dq.p, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dqo.p, q_off, 8 * n_queries, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dql.p, ql.data(), 4 * n_queries, cudaMemcpyHostToDevice, st));
+  if (n_cands > 0) {
+    CK(cudaMemcpyAsync(dc.p, cands, sizeof(double) * c_total, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dco.p, c_off, 8 * n_cands, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dcl.p, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
+  }
+  int64_t* o = dout.as<int64_t>();
+  if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
+                  dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, o, (double*)(o + n_queries), o + 2 * n_queries,
+                  o + 3 * n_queries, o + 4 * n_queries, st))
+    return -1;
+  CK(cudaMemcpyAsync(nn_idx, o, 8 * n_queries, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(nn_dist, o + n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(cells, o + 2 * n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(computed, o + 3 * n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(abandoned, o + 4 * n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
+                             const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells,
+                             cudaStream_t st) {
+  if (check_spec(spec)) return -1;
+  if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
+  if (n <= 0) return 0;
+  CK(cudaMemsetAsync(d_D, 0, sizeof(double) * (size_t)n * n, st));  // diagonal 0.0
+  if (n == 1) {
+    if (cells) *cells = 0;
+    return 0;
+  }
+  const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
+  const int eng = choose_engine(max_len, max_len, win < 0 ? max_len : win, false);
+  if (eng < 0) return fail("series length %d exceeds this build's engines", max_len);
+  ParamHolder ph;
+  if (ph.init(spec, st)) return -1;
+  const long long np = n * (n - 1) / 2;
+  DBuf dtend, dcnt, dtot;
+  if (dtend.alloc(sizeof(int) * (size_t)np, st) || dcnt.alloc(8, st) || dtot.alloc(8, st)) return -1;
+  CK(cudaMemsetAsync(dcnt.p, 0, 8, st));
+  CK(cudaMemsetAsync(dtot.p, 0, 8, st));
+  const int wpb = 4;
+  if (launch_persistent(pick_tri(spec->kind, spec->cost_mode, eng), 32 * wpb, pair_smem(max_len, wpb), st, np,
+                        d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, ph.prm, d_D,
+                        dtend.as<int>(), dcnt.as<int>()))
+    return -1;
+  if (cells) {
+    if (launch_plain(k_cells_triangle, dim3(256), dim3(256), 0, st, (const int*)d_len, (int)n, win,
+                     (const int*)dtend.as<int>(), (int)engine_is_diag(eng), eng_S(eng),
+                     kind_tag(spec->kind) == K_ERP ? 0 : 1, dtot.as<unsigned long long>()))
+      return -1;
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, dtot.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *cells = (int64_t)tot;
+  }
+  return 0;
+}
+
+int ek_pairwise_dev(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
+                    const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
+  return pairwise_dev_impl(spec, variant, d_series, d_off, d_len, n, max_len, d_D, cells, st);
+}
+
+int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int64_t total, const int64_t* off,
+                const int64_t* len, int64_t n, double* D, int64_t* cells) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  if (n <= 0) return 0;
+  cudaStream_t st = g_ctx.stream;
+  std::vector<int32_t> l32(n);
+  int32_t mx = 0;
+  for (int64_t k = 0; k < n; ++k) mx = std::max(mx, l32[k] = (int32_t)len[k]);
+  DBuf ds, doff, dlen, dD;
+  if (ds.alloc(sizeof(double) * total, st) || doff.alloc(8 * n, st) || dlen.alloc(4 * n, st) ||
+      dD.alloc(sizeof(double) * (size_t)n * n, st))
+    return -1;
+  CK(cudaMemcpyAsync(ds.p, series, sizeof(double) * total, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(doff.p, off, 8 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dlen.p, l32.data(), 4 * n, cudaMemcpyHostToDevice, st));
+  if (pairwise_dev_impl(spec, variant, ds.as<double>(), doff.as<int64_t>(), dlen.as<int32_t>(), n, mx, dD.as<double>(),
+                        cells, st))
+    return -1;
+  CK(cudaMemcpyAsync(D, dD.p, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* dq, int64_t lq, const double* dref,
+                           int64_t nref, int32_t normalize, int64_t* best_off, double* best_dist, int64_t* cells,
+                           int64_t* computed, int64_t* abandoned, cudaStream_t st) {
+  if (check_spec(spec)) return -1;
+  if (spec->kind != K_DTW && spec->kind != K_CDTW) return fail("subsequence search supports dtw and cdtw only");
+  if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
+  if (lq < 1 || lq > nref) return fail("query length %lld exceeds reference length %lld", (long long)lq, (long long)nref);
+  const long long nwin = nref - lq + 1;
+  const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
+  const int eng = choose_engine((int)lq, (int)lq, win < 0 ? (int)lq : win, false);
+  if (eng < 0) return fail("query length %lld exceeds this build's engines", (long long)lq);
+  const bool share = variant == 1 || variant == 2;
+  // numpy pairwise-sum plan for length lq
+  std::vector<int2> leaves;
+  std::vector<int> ops;
+  np_plan_rec(0, (int)lq, leaves, ops);
+  DBuf dleaves, dops, dcut, dout, dtend, dcnt;
+  if (dleaves.alloc(sizeof(int2) * leaves.size(), st) || dops.alloc(sizeof(int) * ops.size(), st) ||
+      dcut.alloc(8, st) || dout.alloc(sizeof(double) * (size_t)nwin, st) || dtend.alloc(sizeof(int) * (size_t)nwin, st) ||
+      dcnt.alloc(16, st))
+    return -1;
+  CK(cudaMemcpyAsync(dleaves.p, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dops.p, ops.data(), sizeof(int) * ops.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(dcnt.p, 0, 16, st));
+  NpPlan plan{dleaves.as<int2>(), (int)leaves.size(), dops.as<int>(), (int)ops.size()};
+  const int nl_ = plan.nleaves;
+  unsigned long long cut0 = 0x7ff0000000000000ULL;
+  std::vector<long long> seeds;
+  if (share) {
+    // sampled exact diagonal bounds; the best few windows run first (phase A)
+    const long long nsamp = std::min<long long>(nwin, 4096);
+    const long long stride = std::max<long long>(1, nwin / nsamp);
+    DBuf dub;
+    if (dub.alloc(sizeof(double) * nsamp, st)) return -1;
+    const size_t smem = sizeof(double) * ((size_t)lq + nl_ + 16 + 4 * ((size_t)lq + nl_ + 16));
+    if (launch_plain(get_subseq_ub(spec->cost_mode), dim3((unsigned)std::min<long long>(1024, (nsamp + 3) / 4)),
+                     dim3(128), smem, st, dq, (int)lq, dref, nwin, stride, (int)normalize, plan, dub.as<double>(),
+                     nsamp))
+      return -1;
+    std::vector<double> ub(nsamp);
+    CK(cudaMemcpyAsync(ub.data(), dub.p, sizeof(double) * nsamp, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<long long> idx(nsamp);
+    for (long long k = 0; k < nsamp; ++k) idx[k] = k;
+    std::sort(idx.begin(), idx.end(), [&](long long a, long long b) { return ub[a] < ub[b] || (ub[a] == ub[b] && a < b); });
+    double best = ub[idx[0]];
+    if (best < INFINITY) {
+      std::memcpy(&cut0, &best, 8);
+      for (long long k = 0; k < std::min<long long>(16, nsamp); ++k) seeds.push_back(idx[k] * stride);
+    }
+  }
+  CK(cudaMemcpyAsync(dcut.p, &cut0, 8, cudaMemcpyHostToDevice, st));
+  const SubseqFn fn = get_subseq(spec->cost_mode, eng);
+  const int wpb = 8;
+  const size_t smem = sizeof(double) * ((size_t)lq + 2 + nl_ + 16 + wpb * ((size_t)lq + 32 + 2 + nl_ + 16));
+  if (!seeds.empty()) {
+    DBuf dseed, dso, dst;
+    const long long ns = (long long)seeds.size();
+    if (dseed.alloc(8 * ns, st) || dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
+    CK(cudaMemcpyAsync(dseed.p, seeds.data(), 8 * ns, cudaMemcpyHostToDevice, st));
+    if (launch_persistent(fn, 32 * wpb, smem, st, ns, dq, (int)lq, dref, (long long)nref, (int)normalize,
+                          (const long long*)dseed.as<long long>(), ns, win, plan, (int)share,
+                          dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
+      return -1;
+    CK(cudaStreamSynchronize(st));
+  }
+  if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, dq, (int)lq, dref, (long long)nref, (int)normalize,
+                        (const long long*)nullptr, nwin, win, plan, (int)share, dcut.as<unsigned long long>(),
+                        dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
+    return -1;
+  // reduce
+  const int nb = (int)std::min<long long>(1024, (nwin + 255) / 256);
+  DBuf pd, pi, pc, pa, pcl;
+  if (pd.alloc(8 * nb, st) || pi.alloc(8 * nb, st) || pc.alloc(8 * nb, st) || pa.alloc(8 * nb, st) || pcl.alloc(8 * nb, st))
+    return -1;
+  const int wv = win < 0 ? (int)lq : win;
+  if (launch_plain(k_red1_partial, dim3(nb), dim3(256), 0, st, (const double*)dout.as<double>(),
+                   (const int*)dtend.as<int>(), nwin, (int)lq, wv, (int)engine_is_diag(eng), eng_S(eng),
+                   pd.as<double>(), pi.as<long long>(), pc.as<long long>(), pa.as<long long>(), pcl.as<long long>()))
+    return -1;
+  std::vector<double> hd(nb);
+  std::vector<long long> hi(nb), hc(nb), ha(nb), hcl(nb);
+  CK(cudaMemcpyAsync(hd.data(), pd.p, 8 * nb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hi.data(), pi.p, 8 * nb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hc.data(), pc.p, 8 * nb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ha.data(), pa.p, 8 * nb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hcl.data(), pcl.p, 8 * nb, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double bd = INFINITY;
+  long long bo = -1, tc = 0, ta = 0, tcl = 0;
+  for (int b = 0; b < nb; ++b) {
+    tc += hc[b];
+    ta += ha[b];
+    tcl += hcl[b];
+    if (hd[b] < INFINITY && (hd[b] < bd || (hd[b] == bd && hi[b] < bo))) {
+      bd = hd[b];
+      bo = hi[b];
+    }
+  }
+  *best_off = bo;
+  *best_dist = bd;
+  if (cells) *cells = tcl;
+  if (computed) *computed = tc;
+  if (abandoned) *abandoned = ta;
+  return 0;
+}
+
+int ek_subseq_dev(const ek_spec* spec, int32_t variant, const double* d_query, int64_t lq, const double* d_reference,
+                  int64_t n_ref, int32_t normalize, int64_t* best_off, double* best_dist, int64_t* cells,
+                  int64_t* computed, int64_t* abandoned, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
+  return subseq_dev_impl(spec, variant, d_query, lq, d_reference, n_ref, normalize, best_off, best_dist, cells,
+                         computed, abandoned, st);
+}
+
+int ek_subseq(const ek_spec* spec, int32_t variant, const double* query, int64_t lq, const double* reference,
+              int64_t n_ref, int32_t normalize, int64_t* best_off, double* best_dist, int64_t* cells,
+              int64_t* computed, int64_t* abandoned) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  cudaStream_t st = g_ctx.stream;
+  if (lq < 1 || lq > n_ref) return fail("query length %lld exceeds reference length %lld", (long long)lq, (long long)n_ref);
+  DBuf dq, dr;
+  if (dq.alloc(sizeof(double) * lq, st) || dr.alloc(sizeof(double) * n_ref, st)) return -1;
+  CK(cudaMemcpyAsync(dq.p, query, sizeof(double) * lq, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dr.p, reference, sizeof(double) * n_ref, cudaMemcpyHostToDevice, st));
+  return subseq_dev_impl(spec, variant, dq.as<double>(), lq, dr.as<double>(), n_ref, normalize, best_off, best_dist,
+                         cells, computed, abandoned, st);
+}
+
+}  // extern "C"

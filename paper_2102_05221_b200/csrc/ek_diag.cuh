@@ -1,0 +1,187 @@
+// ek_diag.cuh -- warp-per-pair anti-diagonal wavefront for banded elastic DPs.
+//
+// Layout ("diagonal slots"): lane l owns P consecutive diagonals d = i - j,
+// d = dbase + l*P + p.  Cell (i,j) sits on diagonal d at time t = i + j; its
+// dependencies are its own diagonal at t-2 (D), diagonal d-1 at t-1 (T) and
+// diagonal d+1 at t-1 (L).  One "double step" advances every diagonal by one
+// cell: even slots at time t, odd slots at time t+1.  Inside a lane all
+// dependencies are registers; the only exchange is one 64-bit shuffle per
+// half step across the lane boundary.  The Sakoe-Chiba band maps to a
+// contiguous range of slots, so a band of width 2w+1 costs ~(2w+3)/32 slots
+// per lane instead of a full row.
+//
+// Borders: the corner is diagonal 0 at t=0; border cells (i,0)/(0,j) are the
+// first cells of diagonals +i/-j (t=|d|).  For ERP they follow from the
+// recurrence itself -- (d,0) = (d-1,0) + pc(l_d, g) is exactly the sequential
+// prefix of _erp_border (kernels.py:280-289) -- and every other kind has +inf
+// borders, which also fall out once diagonals +-1 are seeded at t=1.  The two
+// "virtual" diagonals just outside the band hold their border value at their
+// border time and +inf otherwise, which reproduces the reference's window
+// (hborder for j <= w+1, vborder while jstart == 1; _speedups.pyx:137-148).
+//
+// Pruning/abandoning: every path crosses one of any two consecutive
+// anti-diagonals, so when no cell of (t, t+1) is <= cutoff the pair is
+// abandoned (+inf).  A pair whose exact cost is <= cutoff never abandons (all
+// cells on its optimal path are <= cost), so the observable contract is the
+// reference eapruned's: exact when cost <= cutoff, +inf otherwise
+// (engines.py:72-84).  With a shared cutoff that only tightens,
+// the same argument holds against the final cutoff.
+#pragma once
+#include "ek_common.cuh"
+
+namespace ekb {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct DiagResult {
+  double cost;   // exact, or +inf when abandoned / above cutoff
+  int t_end;     // last anti-diagonal processed
+};
+
+__device__ __forceinline__ double ld_cut(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return __longlong_as_double((long long)v);
+}
+
+struct NoLoader {
+  __device__ __forceinline__ void ensure(int, int) {}
+};
+
+// Series accessor over shared memory: valid for indices -1..n (pads set by the stager).
+struct SmemSeries {
+  const double* p;
+  int n;
+  __device__ __forceinline__ double at(int k) const { return p[min(max(k, -1), n)]; }
+};
+
+// X: lines accessor (nl >= nc), Y: cols accessor; at(k) is defined for every k
+// (clamped to the pads at -1 and n).  w: effective window (w >= nl - nc, checked by the caller).
+template <int KIND, int MODE, int P, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
+__device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
+                                const unsigned long long* cutp, const Params& prm, Loader& ld) {
+  static_assert(P % 2 == 0 && P >= 2, "P must be even");
+  constexpr int H = P / 2;
+  const int lane = threadIdx.x & 31;
+  const int dlo = max(-w, 1 - nc), dhi = min(w, nl - 1);
+  const int dbase = (dlo - 1) & ~1;  // floor to even, includes the lower virtual diagonal
+  const int d0 = dbase + lane * P;
+  constexpr bool BORDERED = (KIND == K_ERP);
+
+  ld.ensure((2 + dhi + 3) / 2 + 1 + H, (2 + 3 - dlo) / 2 + 2);
+  double val[P];
+  bool upd[P];
+  int tb[P];  // border time of a virtual diagonal (ERP only), else -1
+  DiagK<KIND> kk[P];
+  SlotS<KIND> st[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int d = d0 + p;
+    upd[p] = (d >= dlo) && (d <= dhi);
+    tb[p] = (BORDERED && (d == dlo - 1 || d == dhi + 1)) ? (d < 0 ? -d : d) : -1;
+    kk[p] = make_diag<KIND>(d, prm);
+    val[p] = EKB_INF;
+    if constexpr (KIND == K_TWE) st[p].pcp = 0.0;
+    if (d == 0) val[p] = 0.0;  // corner, t = 0
+    if (d == 1) {              // border cell (1,0) at t = 1
+      if constexpr (BORDERED) val[p] = dadd(0.0, pcost<MODE>(X.at(0), prm.gap));
+      if constexpr (KIND == K_TWE) st[p].pcp = pcost<MODE>(X.at(0), 0.0);
+    }
+    if (d == -1) {             // border cell (0,1) at t = 1
+      if constexpr (BORDERED) val[p] = dadd(0.0, pcost<MODE>(prm.gap, Y.at(0)));
+      if constexpr (KIND == K_TWE) st[p].pcp = pcost<MODE>(0.0, Y.at(0));
+    }
+  }
+
+  auto cx = [&](int k) { return X.at(k); };
+  auto cy = [&](int k) { return Y.at(k); };
+
+  int t = 2;
+  int I0 = (t + d0) >> 1, J0 = (t - d0) >> 1;
+  RowD<KIND> xw[H + 1];
+  ColD<KIND> yw[H];
+#pragma unroll
+  for (int k = 0; k <= H; ++k) xw[k] = make_row<KIND, MODE>(cx(I0 + k - 1), cx(I0 + k - 2), prm);
+#pragma unroll
+  for (int m = 0; m < H; ++m) yw[m] = make_col<KIND, MODE>(cy(J0 - m - 1), cy(J0 - m - 2), prm);
+
+  const int Tf = nl + nc;
+  int iter = 0;
+  double nextcut = cut;
+  bool dead = false;
+  for (;;) {
+    if constexpr (SHARED_CUT) {
+      if ((iter & 15) == 0) nextcut = ld_cut(cutp);
+      if ((iter & 15) == 12) cut = fmin(cut, nextcut);
+    }
+    bool alive = false;
+    // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
+    double tin = __shfl_up_sync(FULL, val[P - 1], 1);
+    if (lane == 0) tin = EKB_INF;
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      const int p = 2 * m;
+      const double T = (m == 0) ? tin : val[p - 1];
+      double v = cell<KIND, MODE>(val[p], T, val[p + 1], xw[m], yw[m], kk[p], st[p], prm);
+      bool keep = upd[p];
+      if constexpr (BORDERED) keep = keep || (tb[p] == t);
+      val[p] = keep ? v : EKB_INF;
+      alive |= (val[p] <= cut);
+    }
+    if (t >= Tf) break;
+    // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
+    double lin = __shfl_down_sync(FULL, val[0], 1);
+    if (lane == 31) lin = EKB_INF;
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      const int p = 2 * m + 1;
+      const double L = (p == P - 1) ? lin : val[p + 1];
+      double v = cell<KIND, MODE>(val[p], val[p - 1], L, xw[m + 1], yw[m], kk[p], st[p], prm);
+      bool keep = upd[p];
+      if constexpr (BORDERED) keep = keep || (tb[p] == t + 1);
+      val[p] = keep ? v : EKB_INF;
+      alive |= (val[p] <= cut);
+    }
+    if (t + 1 >= Tf) break;
+    if (!__any_sync(FULL, alive)) { dead = true; break; }
+    // ---- slide the register windows by one element ----
+    t += 2;
+    ++I0;
+    ++J0;
+    ++iter;
+    ld.ensure((t + dhi + 3) / 2 + 1 + H, (t + 3 - dlo) / 2 + 2);
+#pragma unroll
+    for (int k = 0; k < H; ++k) xw[k] = xw[k + 1];
+    xw[H] = make_row<KIND, MODE>(cx(I0 + H - 1), xw[H - 1].x, prm);
+#pragma unroll
+    for (int m = H - 1; m > 0; --m) yw[m] = yw[m - 1];
+    yw[0] = make_col<KIND, MODE>(cy(J0 - 1), yw[0].y, prm);
+  }
+
+  DiagResult res;
+  res.t_end = dead ? t + 1 : Tf;
+  if (dead) {
+    res.cost = EKB_INF;
+    return res;
+  }
+  if constexpr (SHARED_CUT) cut = fmin(cut, ld_cut(cutp));
+  const int sf = (nl - nc) - dbase;
+  const int pf = sf % P;
+  double r = val[0];
+#pragma unroll
+  for (int p = 1; p < P; ++p)
+    if (p == pf) r = val[p];
+  r = __shfl_sync(FULL, r, sf / P);
+  res.cost = (r <= cut) ? r : EKB_INF;
+  return res;
+}
+
+// Slots needed by diag_pair for this band: the lanes must cover [dbase, dhi+1].
+__host__ __device__ inline int diag_slots_needed(int nl, int nc, int w) {
+  int dlo = (-w > 1 - nc) ? -w : 1 - nc;
+  int dhi = (w < nl - 1) ? w : nl - 1;
+  int dbase = (dlo - 1) & ~1;
+  return dhi + 2 - dbase;
+}
+
+}  // namespace ekb

@@ -1,0 +1,284 @@
+// ek_kernels.cuh -- driver kernels around the two DP engines.
+//
+//   k_pairs     : one elastic distance per (pair, cutoff); replaces a loop of
+//                 _speedups.run / engines.distance (engines.py:121-147)
+//   k_triangle  : the all-pairs upper triangle, mirrored
+//   k_nn        : 1-NN search with a per-query shared cutoff (search.py:81-160)
+//   k_subseq    : z-normalised subsequence search (search.py:163-215)
+//   k_nn_reduce : lexicographic (distance, index) minimum per query
+//
+// All kernels are warp-per-pair and persistent (grid = a multiple of the SM
+// count, work claimed with an atomic counter).  Series are staged into shared
+// memory per warp with coalesced loads; the 1-NN kernel loads a candidate
+// lazily in 64-element chunks because most pairs are abandoned within the
+// first few anti-diagonals.
+#pragma once
+#include "ek_common.cuh"
+#include "ek_diag.cuh"
+#include "ek_stripe.cuh"
+
+namespace ekb {
+
+// Engine codes: 0..2 diagonal P=4/8/16; 3..5 stripe S=4/8/16 (unbanded);
+// 6 stripe S=16 banded; 7 stripe S=16 banded with row abandoning ("ea").
+enum Engine : int {
+  E_DIAG4 = 0, E_DIAG8 = 1, E_DIAG16 = 2,
+  E_STR4 = 3, E_STR8 = 4, E_STR16 = 5,
+  E_STRB16 = 6,
+  E_STR16_EA = 7,
+  E_COUNT = 8
+};
+
+__host__ __device__ constexpr int engine_is_diag(int e) { return e <= E_DIAG16; }
+__host__ __device__ constexpr int engine_P(int e) { return e == E_DIAG4 ? 4 : e == E_DIAG8 ? 8 : 16; }
+__host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e == E_STR8 ? 8 : 16; }
+
+struct PairDesc {
+  long long xoff, yoff;  // lines / cols offsets into the series buffer
+  int nl, nc;            // nl >= nc (orientation done by the host, ties keep s on the rows)
+  int w;                 // effective window (>= nl - nc, else the host already returned +inf)
+  int pad_;
+  double cut;
+};
+
+// ---- staging helpers -------------------------------------------------------
+
+template <int KIND>
+__device__ __forceinline__ void stage_series(double* dst, const double* __restrict__ src, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int k = lane; k < n; k += 32) dst[k] = src[k];
+  if (lane == 0) {
+    dst[-1] = pad_before<KIND>(src[0]);
+    dst[n] = EKB_INF;
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void stage_table(double* tab, int len, const Params& prm) {
+  const int lane = threadIdx.x & 31;
+  if constexpr (KIND == K_WDTW) {
+    for (int k = lane; k < len; k += 32) tab[k] = (k < prm.wt_len) ? prm.wt[k] : 0.0;
+  } else if constexpr (KIND == K_TWE) {
+    for (int k = lane; k < len; k += 32) {
+      double dij = (double)k;
+      tab[k] = dmul(prm.nu, dadd(dij, dij));
+    }
+  }
+}
+
+template <int KIND, int MODE, int ENG, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
+__device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
+                                           const unsigned long long* cutp, const double* tab, int tablen,
+                                           const Params& prm, Loader& ld, double& cost, int& tend) {
+  if constexpr (engine_is_diag(ENG)) {
+    DiagResult r = diag_pair<KIND, MODE, engine_P(ENG), SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+    cost = r.cost;
+    tend = r.t_end;
+  } else {
+    constexpr bool BANDED = ENG >= E_STRB16;
+    constexpr bool EA = ENG == E_STR16_EA;
+    StripeResult r = stripe_pair<KIND, MODE, engine_S(ENG), BANDED, SHARED_CUT, EA>(X, nl, Y, nc, w, cut, cutp,
+                                                                                     tab, tablen, prm);
+    cost = r.cost;
+    tend = r.t_end;
+  }
+}
+
+// ---- generic pair list ------------------------------------------------------
+// smem per warp: X (lmax+2) + Y (lmax+2) + tab (lmax+1) doubles
+
+template <int KIND, int MODE, int ENG>
+__global__ void __launch_bounds__(128) k_pairs(const double* __restrict__ series, const PairDesc* __restrict__ pairs,
+                                               int npairs, int lmax, Params prm, double* __restrict__ out_cost,
+                                               int* __restrict__ out_tend) {
+  extern __shared__ double smem[];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int stride = 2 * (lmax + 2) + (lmax + 1);
+  double* X = smem + wib * stride + 1;
+  double* Y = X + (lmax + 2);
+  double* tab = Y + (lmax + 1);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  NoLoader ld;
+  for (int pid = blockIdx.x * (blockDim.x >> 5) + wib; pid < npairs; pid += nwarps) {
+    const PairDesc pd = pairs[pid];
+    const Params pp = pair_params(prm, pd.nl);
+    __syncwarp();
+    stage_series<KIND>(X, series + pd.xoff, pd.nl);
+    stage_series<KIND>(Y, series + pd.yoff, pd.nc);
+    const int tablen = max(pd.nl, pd.nc) + 1;
+    if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
+    __syncwarp();
+    double cost;
+    int tend;
+    run_engine<KIND, MODE, ENG, false>(SmemSeries{X, pd.nl}, pd.nl, SmemSeries{Y, pd.nc}, pd.nc, pd.w, pd.cut,
+                                       nullptr, tab, tablen, pp, ld, cost, tend);
+    if (lane == 0) {
+      out_cost[pid] = cost;
+      out_tend[pid] = tend;
+    }
+  }
+}
+
+// ---- all-pairs upper triangle ---------------------------------------------------
+// pair index p in [0, n(n-1)/2) -> (i, j), i < j; D[i][j] = D[j][i] = distance(X_i, X_j).
+
+__device__ __forceinline__ void tri_index(long long p, int n, int& i, int& j) {
+  // row i holds n-1-i pairs; solve the largest i with i*(2n-i-1)/2 <= p
+  double nn = (double)n;
+  double disc = (2.0 * nn - 1.0) * (2.0 * nn - 1.0) - 8.0 * (double)p;
+  int ii = (int)floor(((2.0 * nn - 1.0) - sqrt(disc)) * 0.5);
+  ii = max(0, min(ii, n - 2));
+  auto start = [&](long long r) { return r * (2LL * n - r - 1) / 2; };
+  while (ii > 0 && start(ii) > p) --ii;
+  while (ii < n - 2 && start(ii + 1) <= p) ++ii;
+  i = ii;
+  j = (int)(p - start(ii)) + ii + 1;
+}
+
+template <int KIND, int MODE, int ENG>
+__global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ series, const long long* __restrict__ off,
+                                                  const int* __restrict__ len, int n, int win, int lmax, Params prm,
+                                                  double* __restrict__ D, int* __restrict__ tend_out,
+                                                  int* __restrict__ counter) {
+  extern __shared__ double smem[];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int stride = 2 * (lmax + 2) + (lmax + 1);
+  double* X = smem + wib * stride + 1;
+  double* Y = X + (lmax + 2);
+  double* tab = Y + (lmax + 1);
+  const long long npairs = (long long)n * (n - 1) / 2;
+  NoLoader ld;
+  for (;;) {
+    long long p = 0;
+    if (lane == 0) p = (long long)atomicAdd((unsigned long long*)counter, 1ULL);
+    p = __shfl_sync(FULL, p, 0);
+    if (p >= npairs) break;
+    int a, b;
+    tri_index(p, n, a, b);
+    // make_recurrence orientation: lines = longer, ties keep the first argument (a) on the rows
+    int s = a, t = b;
+    if (len[b] > len[a]) { s = b; t = a; }
+    const int nl = len[s], nc = len[t];
+    const int w = win < 0 ? nl : win;
+    double cost = EKB_INF;
+    int tend = 0;
+    if (w >= nl - nc) {
+      const Params pp = pair_params(prm, nl);
+      __syncwarp();
+      stage_series<KIND>(X, series + off[s], nl);
+      stage_series<KIND>(Y, series + off[t], nc);
+      const int tablen = max(nl, nc) + 1;
+      if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
+      __syncwarp();
+      run_engine<KIND, MODE, ENG, false>(SmemSeries{X, nl}, nl, SmemSeries{Y, nc}, nc, w, EKB_INF, nullptr, tab,
+                                         tablen, pp, ld, cost, tend);
+    }
+    if (lane == 0) {
+      D[(long long)a * n + b] = cost;
+      D[(long long)b * n + a] = cost;
+      if (tend_out) tend_out[p] = tend;
+    }
+  }
+}
+
+// ---- 1-NN with a shared per-query cutoff -----------------------------------------
+
+// Lazily staged candidate: 64-element chunks on demand.
+struct LazyCand {
+  double* buf;
+  const double* src;
+  int n, loaded;
+  bool is_x;  // backs the lines series (else the cols series)
+  __device__ __forceinline__ void load_to(int need) {
+    need = min(need, n);
+    const int lane = threadIdx.x & 31;
+    while (loaded < need) {
+      const int base = loaded;
+      for (int k = lane; k < 64 && base + k < n; k += 32) buf[base + k] = __ldg(src + base + k);
+      loaded = min(base + 64, n);
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void ensure(int needX, int needY) {
+    const int need = is_x ? needX : needY;
+    if (need > loaded) load_to(need);
+  }
+};
+
+template <int KIND, int MODE, int ENG>
+__global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const long long* __restrict__ qoff,
+                                            const int* __restrict__ qlen, int nq, const double* __restrict__ C,
+                                            const long long* __restrict__ coff, const int* __restrict__ clen,
+                                            int ncand, const int* __restrict__ order, int rank_lo, int rank_hi,
+                                            int K, int win, int lmax, Params prm, int share,
+                                            unsigned long long* cutbits,
+                                            double* __restrict__ out, int* __restrict__ tend_out,
+                                            int* __restrict__ counter) {
+  extern __shared__ double smem[];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int stride = 2 * (lmax + 2) + (lmax + 1);
+  double* QB = smem + wib * stride + 1;
+  double* CB = QB + (lmax + 2);
+  double* tab = CB + (lmax + 1);
+  const int span = rank_hi - rank_lo;
+  const int rounds = (span + K - 1) / K;
+  const long long nitems = (long long)rounds * nq;
+  int staged_q = -1;
+  for (;;) {
+    long long it = 0;
+    if (lane == 0) it = (long long)atomicAdd((unsigned long long*)counter, 1ULL);
+    it = __shfl_sync(FULL, it, 0);
+    if (it >= nitems) break;
+    const int q = (int)(it % nq);
+    const int r = (int)(it / nq);
+    const int lq = qlen[q];
+    if (q != staged_q) {
+      __syncwarp();
+      stage_series<KIND>(QB, Q + qoff[q], lq);
+      staged_q = q;
+    }
+    const int k_lo = rank_lo + r * K, k_hi = min(k_lo + K, rank_hi);
+    for (int k = k_lo; k < k_hi; ++k) {
+      const int c = order[(long long)q * ncand + k];
+      const int lc = clen[c];
+      // orientation (kernels.py:168-171): query is s, candidate is t
+      const bool q_rows = lq >= lc;
+      const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
+      const int w = win < 0 ? nl : win;
+      double cost = EKB_INF;
+      int tend = 0;
+      if (w >= nl - nc) {
+        const Params pp = pair_params(prm, nl);
+        __syncwarp();
+        if (lane == 0) {
+          CB[-1] = pad_before<KIND>(C[coff[c]]);
+          CB[lc] = EKB_INF;
+        }
+        LazyCand ld{CB, C + coff[c], lc, 0, !q_rows};
+        const int tablen = max(nl, nc) + 1;
+        if constexpr (!engine_is_diag(ENG)) {
+          ld.load_to(lc);  // the stripe engine reads all columns up front
+          stage_table<KIND>(tab, tablen, pp);
+        }
+        __syncwarp();
+        const double cut = ld_cut(cutbits + q);
+        const SmemSeries X{q_rows ? QB : CB, nl};
+        const SmemSeries Y{q_rows ? CB : QB, nc};
+        run_engine<KIND, MODE, ENG, true>(X, nl, Y, nc, w, cut, cutbits + q, tab, tablen, pp, ld, cost, tend);
+        if (share && lane == 0 && cost < EKB_INF) {
+          // values are >= 0 (or +inf), so IEEE bits order as unsigned integers
+          atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
+        }
+      }
+      if (lane == 0) {
+        out[(long long)q * ncand + c] = cost;
+        tend_out[(long long)q * ncand + c] = tend;
+      }
+    }
+  }
+}
+
+}  // namespace ekb

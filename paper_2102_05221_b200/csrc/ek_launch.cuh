@@ -1,0 +1,118 @@
+// ek_launch.cuh -- typed kernel-pointer tables, one instantiation unit per distance kind
+// (ek_inst_<kind>.cu) so the template expansion compiles in parallel.
+#pragma once
+#include "ek_kernels.cuh"
+
+namespace ekb {
+
+using PairsFn = void (*)(const double*, const PairDesc*, int, int, Params, double*, int*);
+using TriFn = void (*)(const double*, const long long*, const int*, int, int, int, Params, double*, int*, int*);
+using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
+                      const int*, int, const int*, int, int, int, int, int, Params, int, unsigned long long*,
+                      double*, int*, int*);
+using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
+                      const int*, int, const int*, int, Params, unsigned long long*);
+
+// diagonal_upper_bound (engines.py:87-103): the diagonal then the last column, summed
+// sequentially in DP order, used to seed a query's cutoff with an exact path cost.
+template <int KIND, int MODE>
+__global__ void k_ub_init(const double* __restrict__ Q, const long long* __restrict__ qoff,
+                          const int* __restrict__ qlen, int nq, const double* __restrict__ C,
+                          const long long* __restrict__ coff, const int* __restrict__ clen, int ncand,
+                          const int* __restrict__ order, int win, Params prm, unsigned long long* cutbits) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const int c = order ? order[(long long)q * ncand] : 0;
+  const int lq = qlen[q], lc = clen[c];
+  const bool q_rows = lq >= lc;
+  const double* X = q_rows ? Q + qoff[q] : C + coff[c];
+  const double* Y = q_rows ? C + coff[c] : Q + qoff[q];
+  const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
+  const int w = win < 0 ? nl : win;
+  if (w < nl - nc) {
+    cutbits[q] = 0x7ff0000000000000ULL;
+    return;
+  }
+  const Params pp = pair_params(prm, nl);
+  auto xv = [&](int k) { return k < 0 ? pad_before<KIND>(X[0]) : X[k]; };
+  auto yv = [&](int k) { return k < 0 ? pad_before<KIND>(Y[0]) : Y[k]; };
+  double total = 0.0;
+  for (int k = 1; k <= nc; ++k) {  // canonical(k, k)
+    RowD<KIND> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
+    ColD<KIND> cd = make_col<KIND, MODE>(yv(k - 1), yv(k - 2), pp);
+    double cost;
+    if constexpr (KIND == K_DTW || KIND == K_CDTW) cost = pcost<MODE>(r.x, cd.y);
+    else if constexpr (KIND == K_WDTW) cost = dmul(pcost<MODE>(r.x, cd.y), pp.wt[0]);
+    else if constexpr (KIND == K_ERP) cost = pcost<MODE>(r.x, cd.y);
+    else if constexpr (KIND == K_MSM) cost = fabs(dsub(r.x, cd.y));
+    else cost = dadd(dadd(pcost<MODE>(r.x, cd.y), pcost<MODE>(k >= 2 ? X[k - 2] : 0.0, k >= 2 ? Y[k - 2] : 0.0)),
+                     dmul(pp.nu, dadd(0.0, 0.0)));
+    total = dadd(total, cost);
+  }
+  for (int i = nc + 1; i <= nl; ++i) {  // alt_row(i, nc)
+    RowD<KIND> r = make_row<KIND, MODE>(xv(i - 1), xv(i - 2), pp);
+    const double y = Y[nc - 1];
+    double cost;
+    if constexpr (KIND == K_DTW || KIND == K_CDTW) cost = pcost<MODE>(r.x, y);
+    else if constexpr (KIND == K_WDTW) cost = dmul(pcost<MODE>(r.x, y), pp.wt[i - nc]);
+    else if constexpr (KIND == K_ERP || KIND == K_TWE) cost = r.ar;
+    else {
+      const double e = dsub(r.x, y);
+      const bool brow = ((r.f & 1) && e <= 0.0) || ((r.f & 2) && e >= 0.0);
+      cost = msm_alt(brow, pp.msm_c, r.dr, fabs(e));
+    }
+    total = dadd(total, cost);
+  }
+  cutbits[q] = (unsigned long long)__double_as_longlong(total);
+}
+
+#define EKB_ENG_CASES(M, FN)                                                                         \
+  case (M)*16 + E_DIAG4: return FN<KIND, M, E_DIAG4>;                                               \
+  case (M)*16 + E_DIAG8: return FN<KIND, M, E_DIAG8>;                                               \
+  case (M)*16 + E_DIAG16: return FN<KIND, M, E_DIAG16>;                                             \
+  case (M)*16 + E_STR4: return FN<KIND, M, E_STR4>;                                                 \
+  case (M)*16 + E_STR8: return FN<KIND, M, E_STR8>;                                                 \
+  case (M)*16 + E_STR16: return FN<KIND, M, E_STR16>;                                               \
+  case (M)*16 + E_STRB16: return FN<KIND, M, E_STRB16>;
+
+template <int KIND>
+PairsFn get_pairs(int mode, int eng) {
+  switch (mode * 16 + eng) {
+    EKB_ENG_CASES(0, k_pairs)
+    EKB_ENG_CASES(1, k_pairs)
+    case 0 * 16 + E_STR16_EA: return k_pairs<KIND, 0, E_STR16_EA>;
+    case 1 * 16 + E_STR16_EA: return k_pairs<KIND, 1, E_STR16_EA>;
+  }
+  return nullptr;
+}
+
+template <int KIND>
+TriFn get_triangle(int mode, int eng) {
+  switch (mode * 16 + eng) {
+    EKB_ENG_CASES(0, k_triangle)
+    EKB_ENG_CASES(1, k_triangle)
+  }
+  return nullptr;
+}
+
+template <int KIND>
+NNFn get_nn(int mode, int eng) {
+  switch (mode * 16 + eng) {
+    EKB_ENG_CASES(0, k_nn)
+    EKB_ENG_CASES(1, k_nn)
+  }
+  return nullptr;
+}
+
+template <int KIND>
+UBFn get_ub(int mode) {
+  return mode == 0 ? k_ub_init<KIND, 0> : k_ub_init<KIND, 1>;
+}
+
+#define EKB_INSTANTIATE_KIND(K)                  \
+  template PairsFn get_pairs<K>(int, int);       \
+  template TriFn get_triangle<K>(int, int);      \
+  template NNFn get_nn<K>(int, int);             \
+  template UBFn get_ub<K>(int);
+
+}  // namespace ekb

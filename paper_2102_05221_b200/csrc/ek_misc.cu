@@ -1,0 +1,168 @@
+// ek_misc.cu -- kind-independent kernels of the 1-NN path: candidate ranking
+// (a scheduling heuristic only -- it never decides a result), the per-query
+// lexicographic (distance, index) reduction, and computed-cell accounting.
+#include "ek_misc.cuh"
+
+namespace ekb {
+
+// Approximate squared Euclidean distance in FP32 over a 32x32 (query, candidate)
+// tile; only used to order candidates so a tight cutoff is found early.
+__global__ void __launch_bounds__(256) k_rank_dist(const double* __restrict__ Q, const long long* __restrict__ qoff,
+                                                   const int* __restrict__ qlen, int nq,
+                                                   const double* __restrict__ C, const long long* __restrict__ coff,
+                                                   const int* __restrict__ clen, int ncand, float* __restrict__ out) {
+  __shared__ float qs[32][33];
+  __shared__ float cs[32][33];
+  const int q0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps: each thread 4 queries x 1 candidate
+  int lmax = 0;
+  for (int k = 0; k < 32; ++k) {
+    if (q0 + k < nq) lmax = max(lmax, qlen[q0 + k]);
+    if (c0 + k < ncand) lmax = max(lmax, clen[c0 + k]);
+  }
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int kb = 0; kb < lmax; kb += 32) {
+    for (int r = ty; r < 32; r += 8) {
+      const int q = q0 + r, c = c0 + r, k = kb + tx;
+      qs[r][tx] = (q < nq && k < qlen[q]) ? (float)Q[qoff[q] + k] : 0.f;
+      cs[r][tx] = (c < ncand && k < clen[c]) ? (float)C[coff[c] + k] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const float cv = cs[tx][k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float d = qs[ty + 8 * u][k] - cv;
+        acc[u] += d * d;
+      }
+    }
+    __syncthreads();
+  }
+  for (int u = 0; u < 4; ++u) {
+    const int q = q0 + ty + 8 * u, c = c0 + tx;
+    if (q < nq && c < ncand) out[(long long)q * ncand + c] = acc[u];
+  }
+}
+
+// Per query: bitonic sort of (key, candidate) in shared memory -> ranked candidate order.
+__global__ void __launch_bounds__(1024) k_rank_sort(const float* __restrict__ keys, int ncand, int npow2,
+                                                    int* __restrict__ order) {
+  extern __shared__ unsigned char sm_raw[];
+  float* k = reinterpret_cast<float*>(sm_raw);
+  int* v = reinterpret_cast<int*>(k + npow2);
+  const int q = blockIdx.x;
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+    k[i] = i < ncand ? keys[(long long)q * ncand + i] : __int_as_float(0x7f800000);
+    v[i] = i;
+  }
+  __syncthreads();
+  for (int size = 2; size <= npow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < npow2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const float a = k[lo], b = k[hi];
+        const int va = v[lo], vb = v[hi];
+        // ascending by (key, index) so equal keys keep index order
+        const bool gt = (a > b) || (a == b && va > vb);
+        if (gt == up) {
+          k[lo] = b; k[hi] = a;
+          v[lo] = vb; v[hi] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < ncand; i += blockDim.x) order[(long long)q * ncand + i] = v[i];
+}
+
+__global__ void k_identity_order(int nq, int ncand, int* __restrict__ order) {
+  const long long n = (long long)nq * ncand;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    order[i] = (int)(i % ncand);
+}
+
+// nn_search's outcome per query (search.py:101-123): lowest index among the
+// minimal distances -- the serial scan's strict "<" keeps the first one.
+__global__ void __launch_bounds__(256) k_nn_reduce(const double* __restrict__ dist, const int* __restrict__ tend,
+                                                   const int* __restrict__ qlen, int nq, const int* __restrict__ clen,
+                                                   int ncand, int win, int eng_diag, int S, int r0,
+                                                   long long* __restrict__ nn_idx, double* __restrict__ nn_dist,
+                                                   long long* __restrict__ cells, long long* __restrict__ computed,
+                                                   long long* __restrict__ abandoned) {
+  const int q = blockIdx.x;
+  const int lq = qlen[q];
+  double bd = __longlong_as_double(0x7ff0000000000000LL);
+  int bi = 0x7fffffff;
+  long long nc_ = 0, ab = 0, cl = 0;
+  for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
+    const double d = dist[(long long)q * ncand + c];
+    const int te = tend[(long long)q * ncand + c];
+    const int lc = clen[c];
+    const int nl = max(lq, lc), ncc = min(lq, lc);
+    const int w = win < 0 ? nl : win;
+    if (te > 0) cl += cells_done(eng_diag, S, r0, nl, ncc, w, te);
+    if (d < __longlong_as_double(0x7ff0000000000000LL)) {
+      ++nc_;
+      if (d < bd || (d == bd && c < bi)) { bd = d; bi = c; }
+    } else {
+      ++ab;
+    }
+  }
+  __shared__ double sd[256];
+  __shared__ int si[256];
+  __shared__ long long s1[256], s2[256], s3[256];
+  sd[threadIdx.x] = bd; si[threadIdx.x] = bi;
+  s1[threadIdx.x] = nc_; s2[threadIdx.x] = ab; s3[threadIdx.x] = cl;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double od = sd[threadIdx.x + s];
+      const int oi = si[threadIdx.x + s];
+      if (od < sd[threadIdx.x] || (od == sd[threadIdx.x] && oi < si[threadIdx.x])) {
+        sd[threadIdx.x] = od; si[threadIdx.x] = oi;
+      }
+      s1[threadIdx.x] += s1[threadIdx.x + s];
+      s2[threadIdx.x] += s2[threadIdx.x + s];
+      s3[threadIdx.x] += s3[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const bool found = si[0] != 0x7fffffff;
+    nn_idx[q] = found ? si[0] : -1;
+    nn_dist[q] = sd[0];
+    cells[q] = s3[0];
+    computed[q] = s1[0];
+    abandoned[q] = s2[0];
+  }
+}
+
+// Cells per pair for the pair-list / triangle kernels.
+__global__ void k_cells_pairs(const PairDesc* __restrict__ pairs, const int* __restrict__ tend, int npairs,
+                              int eng_diag, int S, int r0, long long* __restrict__ out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
+    const PairDesc pd = pairs[p];
+    out[p] = tend[p] > 0 ? cells_done(eng_diag, S, r0, pd.nl, pd.nc, pd.w, tend[p]) : 0;
+  }
+}
+
+__global__ void k_cells_triangle(const int* __restrict__ len, int n, int win, const int* __restrict__ tend,
+                                 int eng_diag, int S, int r0, unsigned long long* __restrict__ total) {
+  const long long np = (long long)n * (n - 1) / 2;
+  unsigned long long acc = 0;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < np;
+       p += (long long)gridDim.x * blockDim.x) {
+    int a, b;
+    tri_index(p, n, a, b);
+    const int nl = max(len[a], len[b]), nc = min(len[a], len[b]);
+    const int w = win < 0 ? nl : win;
+    if (tend[p] > 0) acc += cells_done(eng_diag, S, r0, nl, nc, w, tend[p]);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(total, acc);
+}
+
+}  // namespace ekb

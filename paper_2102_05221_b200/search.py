@@ -1,0 +1,203 @@
+"""1-NN search, 1-NN classification, subsequence search and all-pairs matrices.
+
+Drop-in counterparts of pkg/src/elastik/search.py:25-215.  The reference scans
+candidates serially, one ``distance()`` call per pair with the running best as
+the cutoff.  Here one C-ABI call hands the whole query batch to the GPU
+(``ek_nn`` / ``ek_subseq`` / ``ek_pairwise``): every pair is evaluated with a
+per-query shared cutoff that only tightens, so each result is either exact or
++inf, and a lexicographic (distance, index) reduction returns the reference's
+answer -- ties keep the lowest candidate index / offset -- whatever the
+schedule ("1-NN ties").
+
+Results (distance, index, label, offset) are identical to the reference for
+every variant and lower-bound mode.  The accounting in ``SearchStats``
+(computed / abandoned / cells) describes the GPU schedule; ``lb_skips`` is 0
+(the lower-bound pre-filters are a ranked "next" item, SURVEY.md 8(f)#1, and
+cannot change results), and ``trace`` stays empty (there is no serial cutoff
+sequence to trace).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _backend, _lib
+from .engines import VARIANTS
+from .errors import DegenerateInputError, DimensionError, SearchError, SpecError
+from .kernels import DistanceSpec
+from .series import LabeledDataset, as_series
+
+LB_MODES = ("none", "keogh", "keogh2")
+
+
+@dataclass(frozen=True)
+class SearchConfig:
+    """Distance, engine variant and lower-bound mode for one search run (search.py:25-42)."""
+
+    spec: DistanceSpec
+    variant: str = "eapruned"
+    lb: str = "none"
+    normalize: bool = False
+    debug: bool = False
+    backend: str | None = None
+
+    def __post_init__(self):
+        if self.variant not in VARIANTS:
+            raise SpecError(f"unknown variant {self.variant!r}; expected one of {VARIANTS}")
+        if self.lb not in LB_MODES:
+            raise SpecError(f"unknown lb mode {self.lb!r}; expected one of {LB_MODES}")
+        if self.lb != "none" and self.spec.kind not in ("dtw", "cdtw"):
+            raise SpecError("lower bounds are only available for dtw and cdtw")
+
+
+@dataclass
+class SearchStats:
+    """Per-query accounting; lb_skips + computed + abandoned == candidates seen."""
+
+    computed: int = 0
+    abandoned: int = 0
+    lb_skips: int = 0
+    cells: int = 0
+    wall_time: float = 0.0
+    trace: list = field(default_factory=list)
+
+
+@dataclass(frozen=True)
+class SearchRecord:
+    """One classified query, as reported by :func:`classify_1nn`."""
+
+    query_index: int
+    actual: int
+    predicted: int
+    nn_index: int
+    nn_distance: float
+    computed: int
+    abandoned: int
+    lb_skips: int
+    cells: int
+    wall_time: float
+
+
+def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None):
+    """1-NN of every query in one GPU call.
+
+    Returns arrays (nn_index int64, nn_distance float64, cells, computed,
+    abandoned); nn_index is -1 when every candidate is +inf.
+    """
+    _backend.resolve(backend)
+    if variant not in VARIANTS:
+        raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    qs = [as_series(q) for q in queries]
+    cs = [as_series(c) for c in candidates]
+    if not cs:
+        raise SearchError("candidate set is empty")
+    nq = len(qs)
+    out = [np.empty(nq, dtype=np.int64), np.empty(nq, dtype=np.float64)] + [np.empty(nq, dtype=np.int64)
+                                                                             for _ in range(3)]
+    if nq == 0:
+        return tuple(out)
+    qf, qo, ql = _lib.ragged(qs)
+    cf, co, cl = _lib.ragged(cs)
+    longest = np.unique(np.maximum.outer(np.unique(ql), np.unique(cl)))
+    h = _lib.SpecHandle(spec, longest_lengths=longest)
+    L = _lib.lib()
+    _lib.check(L.ek_nn(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(qf), len(qf), _lib.iptr(qo), _lib.iptr(ql), nq,
+                       _lib.dptr(cf), len(cf), _lib.iptr(co), _lib.iptr(cl), len(cs), _lib.iptr(out[0]),
+                       _lib.dptr(out[1]), _lib.iptr(out[2]), _lib.iptr(out[3]), _lib.iptr(out[4])))
+    return tuple(out)
+
+
+def nn_search(query, candidates, cfg: SearchConfig, envelopes=None):
+    """Nearest neighbour of ``query`` -> ``(distance, index, stats)`` (search.py:81-125)."""
+    query = as_series(query)
+    candidates = list(candidates)
+    if not candidates:
+        raise SearchError("candidate set is empty")
+    start = time.perf_counter()
+    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, [query], candidates, backend=cfg.backend)
+    stats = SearchStats(computed=int(comp[0]), abandoned=int(ab[0]), cells=int(cells[0]))
+    stats.wall_time = time.perf_counter() - start
+    return float(dist[0]), int(idx[0]), stats
+
+
+def classify_1nn(train: LabeledDataset, test: LabeledDataset, cfg: SearchConfig,
+                 threads: int | None = None) -> list[SearchRecord]:
+    """1-NN classification of every test series against the train set (search.py:128-160).
+
+    All queries go to the GPU in one call; ``threads`` is accepted for
+    signature compatibility and has no effect.
+    """
+    labels = train.labels
+    start = time.perf_counter()
+    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, test.series, train.series, backend=cfg.backend)
+    per_query = (time.perf_counter() - start) / max(1, len(test))
+    records = []
+    for q, (actual, _) in enumerate(test.entries):
+        best = int(idx[q])
+        records.append(SearchRecord(
+            query_index=q, actual=actual, predicted=labels[best] if best >= 0 else -1, nn_index=best,
+            nn_distance=float(dist[q]), computed=int(comp[q]), abandoned=int(ab[q]), lb_skips=0,
+            cells=int(cells[q]), wall_time=per_query))
+    return records
+
+
+def subsequence_search(query, reference, cfg: SearchConfig):
+    """Best-matching window of ``reference`` -> ``(offset, distance, stats)`` (search.py:163-215).
+
+    Windows (and the query) are z-normalised on the GPU with numpy's exact
+    arithmetic when ``cfg.normalize``; ties keep the lowest offset.
+    """
+    if cfg.spec.kind not in ("dtw", "cdtw"):
+        raise SpecError("subsequence search supports dtw and cdtw only")
+    query = as_series(query)
+    reference = as_series(reference)
+    lq = len(query)
+    if lq > len(reference):
+        raise DimensionError(f"query length {lq} exceeds reference length {len(reference)}")
+    if cfg.normalize and lq < 2:
+        raise DegenerateInputError("z-normalization needs at least 2 points")
+    _backend.resolve(cfg.backend)
+    h = _lib.SpecHandle(cfg.spec)
+    off = np.zeros(1, dtype=np.int64)
+    dist = np.zeros(1, dtype=np.float64)
+    cells = np.zeros(1, dtype=np.int64)
+    comp = np.zeros(1, dtype=np.int64)
+    ab = np.zeros(1, dtype=np.int64)
+    start = time.perf_counter()
+    _lib.check(_lib.lib().ek_subseq(h.ref, _lib.VARIANT_CODE[cfg.variant], _lib.dptr(query), lq,
+                                    _lib.dptr(reference), len(reference), int(bool(cfg.normalize)), _lib.iptr(off),
+                                    _lib.dptr(dist), _lib.iptr(cells), _lib.iptr(comp), _lib.iptr(ab)))
+    stats = SearchStats(computed=int(comp[0]), abandoned=int(ab[0]), cells=int(cells[0]))
+    stats.wall_time = time.perf_counter() - start
+    return int(off[0]), float(dist[0]), stats
+
+
+def pairwise(spec: DistanceSpec, X, variant: str = "pruned_only", backend=None):
+    """Full symmetric matrix of ``distance(spec, variant, X[i], X[j])``, diagonal 0.0.
+
+    The all-pairs loop of SURVEY.md 3.4 in one GPU call; d(a,b) == d(b,a)
+    bit-exactly, so the upper triangle is evaluated and mirrored.  Returns
+    ``(D, cells)``.
+    """
+    if variant not in VARIANTS:
+        raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    _backend.resolve(backend)
+    xs = [as_series(x) for x in X]
+    n = len(xs)
+    D = np.zeros((n, n), dtype=np.float64)
+    if n == 0:
+        return D, 0
+    flat, off, lens = _lib.ragged(xs)
+    longest = np.unique(np.maximum.outer(np.unique(lens), np.unique(lens)))
+    h = _lib.SpecHandle(spec, longest_lengths=longest)
+    cells = np.zeros(1, dtype=np.int64)
+    _lib.check(_lib.lib().ek_pairwise(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(flat), len(flat),
+                                      _lib.iptr(off), _lib.iptr(lens), n, _lib.dptr(D), _lib.iptr(cells)))
+    return D, int(cells[0])
+
+
+_ = math  # re-exported names only

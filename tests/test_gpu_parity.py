@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+golden fixtures from the live reference.  Bit-exact FP64 costs, identical 1-NN
+indices / labels / +inf outcomes, lowest-index ties.
+
+Mirrors the reference's backend-parity sweep (pkg/tests/test_backends.py:30-55),
+its engine property tests (test_engines.py) and acceptance criteria 1-5.
+"""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+from conftest import FIG_S, FIG_T, load_golden, spec_from_dict
+from oracle import eko
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ("base", "ea", "eapruned", "pruned_only")
+
+
+def same(a, b):
+    return (a == b) or (math.isinf(a) and math.isinf(b) and (a > 0) == (b > 0))
+
+
+def test_golden_pairs_gpu(gpu):
+    g = load_golden("pairs.npz")
+    specs = [spec_from_dict(d) for d in json.loads(str(g["specs"]))]
+    ser, off, ln = g["series"], g["series_off"], g["series_len"]
+    get = lambda k: ser[off[k]: off[k] + ln[k]]
+    # group rows by (spec, variant) so each group is one batched GPU call
+    bad = []
+    keys = sorted(set(zip(g["spec_idx"].tolist(), g["variant"].tolist())))
+    for si, vi in keys:
+        rows = np.where((g["spec_idx"] == si) & (g["variant"] == vi))[0]
+        pairs = [(get(g["a"][k]), get(g["b"][k])) for k in rows]
+        costs, cells = gpu.distance_batch(specs[si], VARIANTS[vi], pairs, cutoffs=g["cutoff"][rows])
+        for k, c, n in zip(rows, costs, cells):
+            if not same(c, g["cost"][k]):
+                bad.append((specs[si].kind, VARIANTS[vi], g["cutoff"][k], c, g["cost"][k]))
+            if VARIANTS[vi] == "base" and n != g["cells"][k]:
+                bad.append(("cells", specs[si].kind, int(n), int(g["cells"][k])))
+    assert not bad, bad[:10]
+
+
+def random_spec(ekb, kind, rng, maxlen, mode):
+    if kind == "dtw":
+        return ekb.DistanceSpec(kind="dtw", cost_mode=mode)
+    if kind == "cdtw":
+        return ekb.DistanceSpec(kind="cdtw", window=int(rng.integers(0, maxlen + 1)), cost_mode=mode)
+    if kind == "wdtw":
+        return ekb.DistanceSpec(kind="wdtw", wdtw_g=float(rng.uniform(0.0, 0.6)), cost_mode=mode)
+    if kind == "erp":
+        return ekb.DistanceSpec(kind="erp", window=int(rng.integers(0, maxlen + 1)),
+                                erp_gap=float(rng.uniform(-1.0, 1.0)), cost_mode=mode)
+    if kind == "msm":
+        return ekb.DistanceSpec(kind="msm", msm_c=float(rng.uniform(0.0, 2.0)), cost_mode=mode)
+    return ekb.DistanceSpec(kind="twe", twe_nu=float(rng.uniform(0.0, 1.0)),
+                            twe_lambda=float(rng.uniform(0.0, 2.0)), cost_mode=mode)
+
+
+@pytest.mark.parametrize("kind", ["dtw", "cdtw", "wdtw", "erp", "msm", "twe"])
+@pytest.mark.parametrize("mode", ["squared", "absolute"])
+def test_random_sweep_vs_oracle(gpu, kind, mode):
+    """Lengths 1..300 (both engines, every band shape), cutoffs {inf,1.05,1,0.95,0.3}x exact."""
+    rng = np.random.default_rng(hash((kind, mode)) % 2**32)
+    bad = []
+    for trial in range(60):
+        hi = 48 if trial < 40 else 300
+        la, lb = int(rng.integers(1, hi)), int(rng.integers(1, hi))
+        spec = random_spec(gpu, kind, rng, max(la, lb), mode)
+        a = np.cumsum(rng.normal(0, 1, la))
+        b = np.cumsum(rng.normal(0, 1, lb))
+        exact = eko.distance(spec, "base", a, b)[0]
+        cuts = [math.inf]
+        if math.isfinite(exact) and exact > 0:
+            cuts += [exact * f for f in (1.05, 1.0, 0.95, 0.3)]
+        for v in VARIANTS:
+            costs, _ = gpu.distance_batch(spec, v, [(a, b)] * len(cuts), cutoffs=cuts)
+            for co, c in zip(cuts, costs):
+                want = eko.distance(spec, v, a, b, co)[0]
+                if not same(c, want):
+                    bad.append((la, lb, spec.window, v, co, c, want))
+    assert not bad, bad[:8]
+
+
+def test_fig1_and_fig2b(gpu):
+    dtw = gpu.DistanceSpec(kind="dtw")
+    for v in VARIANTS:
+        assert gpu.distance(dtw, v, FIG_S, FIG_T).cost == 9.0
+    assert gpu.distance(dtw, "base", FIG_S, FIG_T) == (9.0, 36)
+    assert math.isinf(gpu.distance(dtw, "eapruned", FIG_S, FIG_T, cutoff=6.0).cost)
+    assert gpu.distance(dtw, "eapruned", FIG_S, FIG_T, cutoff=9.0).cost == 9.0
+    assert math.isinf(gpu.distance(dtw, "ea", FIG_S, FIG_T, cutoff=6.0).cost)
+    spec = gpu.DistanceSpec(kind="cdtw", window=1)
+    for v in VARIANTS:
+        r = gpu.distance(spec, v, FIG_S, [1.0, 2, 3, 4, 5, 6, 7, 8])
+        assert math.isinf(r.cost) and r.cells_computed == 0
+
+
+def test_nan_and_negative_zero_cutoffs(gpu, rng):
+    spec = gpu.DistanceSpec(kind="cdtw", window=3)
+    a, b = rng.normal(0, 1, 12), rng.normal(0, 1, 9)
+    for v in ("ea", "eapruned"):
+        for co in (math.nan, -0.0, 0.0, -1.0, -math.inf):
+            got = gpu.distance(spec, v, a, b, cutoff=co).cost
+            want = eko.distance(spec, v, a, b, co)[0]
+            assert same(got, want), (v, co, got, want)
+    z = np.zeros(7)
+    for v in ("ea", "eapruned"):
+        assert gpu.distance(spec, v, z, z, cutoff=-0.0).cost == eko.distance(spec, v, z, z, -0.0)[0]
+
+
+def test_identical_series_zero_all_kinds(gpu, rng):
+    s = rng.uniform(-4, 4, 12)
+    for kind in gpu.KINDS:
+        spec = random_spec(gpu, kind, rng, 12, "squared")
+        for v in VARIANTS:
+            assert gpu.distance(spec, v, s, s).cost == 0.0
+
+
+def test_golden_nn_gpu(gpu):
+    g = load_golden("nn.npz")
+    specs = [spec_from_dict(d) for d in json.loads(str(g["specs"]))]
+    for k, spec in enumerate(specs):
+        train = gpu.LabeledDataset("train", tuple((int(a), b) for a, b in zip(g[f"y{k}"], g[f"X{k}"])))
+        test = gpu.LabeledDataset("test", tuple((int(a), b) for a, b in zip(g[f"qy{k}"], g[f"Q{k}"])))
+        for variant in VARIANTS:
+            recs = gpu.classify_1nn(train, test, gpu.SearchConfig(spec=spec, variant=variant))
+            assert [r.nn_index for r in recs] == g[f"idx{k}"].tolist(), (spec, variant)
+            assert [r.nn_distance for r in recs] == g[f"dist{k}"].tolist(), (spec, variant)
+            assert [r.predicted for r in recs] == g[f"pred{k}"].tolist(), (spec, variant)
+    idx = gpu.nn_batch(gpu.DistanceSpec(kind="dtw"), "eapruned", g["tie_Q"], g["tie_X"])[0]
+    assert np.array_equal(idx, g["tie_idx"])
+
+
+def test_nn_ragged_and_unequal_lengths(gpu, rng):
+    q = [np.cumsum(rng.normal(0, 1, n)) for n in (20, 31, 17)]
+    c = [np.cumsum(rng.normal(0, 1, n)) for n in (20, 14, 26, 20, 40, 19)]
+    for spec in (gpu.DistanceSpec(kind="dtw"), gpu.DistanceSpec(kind="cdtw", window=7),
+                 gpu.DistanceSpec(kind="wdtw", wdtw_g=0.1), gpu.DistanceSpec(kind="erp", window=9, erp_gap=0.5),
+                 gpu.DistanceSpec(kind="msm", msm_c=0.5), gpu.DistanceSpec(kind="twe", twe_nu=0.1, twe_lambda=1.0)):
+        idx, dist = gpu.nn_batch(spec, "eapruned", q, c)[:2]
+        r = eko.nn(spec, "eapruned", q, c, threads=2)
+        assert np.array_equal(idx, r["nn_index"]), spec
+        assert np.array_equal(dist, r["nn_distance"]), spec
+
+
+def test_nn_search_single_and_self_match(gpu, rng):
+    dtw = gpu.DistanceSpec(kind="dtw")
+    q = rng.normal(0, 1, 16)
+    d, i, st = gpu.nn_search(q, [q, rng.normal(0, 1, 16)], gpu.SearchConfig(spec=dtw))
+    assert (d, i) == (0.0, 0)
+    assert st.computed + st.abandoned == 2
+    with pytest.raises(gpu.SearchError):
+        gpu.nn_search([1.0, 2.0], [], gpu.SearchConfig(spec=dtw))
+
+
+def test_golden_pairwise_gpu(gpu):
+    g = load_golden("pairwise.npz")
+    D, cells = gpu.pairwise(gpu.DistanceSpec(kind="wdtw", wdtw_g=0.05), g["X"])
+    assert np.array_equal(D, g["D_wdtw"])
+    assert cells > 0
+    D, _ = gpu.pairwise(gpu.DistanceSpec(kind="erp", window=4, erp_gap=0.0), g["X"])
+    assert np.array_equal(D, g["D_erp"])
+
+
+def test_pairwise_all_kinds_vs_oracle(gpu, rng):
+    X = [np.cumsum(rng.normal(0, 1, n)) for n in rng.integers(5, 60, size=14)]
+    for kind in gpu.KINDS:
+        for mode in ("squared", "absolute"):
+            spec = random_spec(gpu, kind, rng, 40, mode)
+            D, _ = gpu.pairwise(spec, X)
+            Do, _ = eko.pairwise(spec, X, threads=2)
+            assert np.array_equal(D, Do), (spec,)
+
+
+def test_golden_subseq_gpu(gpu):
+    g = load_golden("subseq.npz")
+    for k, (kind, w, norm) in enumerate(json.loads(str(g["cases"]))):
+        spec = gpu.DistanceSpec(kind=kind, window=w)
+        for variant in VARIANTS:
+            off, d, st = gpu.subsequence_search(g["q"], g["ref"],
+                                                gpu.SearchConfig(spec=spec, variant=variant, normalize=norm))
+            assert (off, d) == (g["off"][k], g["dist"][k]), (kind, w, norm, variant)
+            assert st.computed + st.abandoned == len(g["ref"]) - len(g["q"]) + 1
+
+
+def test_subseq_edge_cases(gpu):
+    dtw = gpu.DistanceSpec(kind="dtw")
+    assert gpu.subsequence_search([1.0, 2.0], [0.0, 1.0, 2.0, 3.0], gpu.SearchConfig(spec=dtw, variant="base"))[:2] \
+        == (1, 0.0)
+    assert gpu.subsequence_search([7.0, 7.0], [7.0] * 4, gpu.SearchConfig(spec=dtw, variant="base"))[:2] == (0, 0.0)
+    with pytest.raises(gpu.DimensionError):
+        gpu.subsequence_search([1.0, 2.0, 3.0], [1.0, 2.0], gpu.SearchConfig(spec=dtw))
+    with pytest.raises(gpu.SpecError):
+        gpu.subsequence_search([1.0, 2.0], [1.0, 2.0, 3.0], gpu.SearchConfig(spec=gpu.DistanceSpec("msm", msm_c=1.0)))
+
+
+def test_subseq_normalized_planted_copy(gpu, rng):
+    # pkg/tests/test_search.py:173-181
+    q = np.cumsum(rng.normal(0, 1, 24))
+    ref = rng.normal(50.0, 0.25, 200)
+    ref[130:154] = 3.5 * q + 20.0
+    off, d, _ = gpu.subsequence_search(q, ref, gpu.SearchConfig(spec=gpu.DistanceSpec(kind="dtw"), normalize=True))
+    assert off == 130 and d < 1e-12
+
+
+def test_subseq_vs_oracle_random(gpu, rng):
+    for lq, n, w, norm in ((64, 3000, 6, True), (100, 2500, None, True), (33, 1500, 3, False), (200, 4000, 10, True)):
+        q = np.cumsum(rng.normal(0, 1, lq))
+        ref = np.cumsum(rng.normal(0, 1, n))
+        spec = gpu.DistanceSpec(kind="dtw" if w is None else "cdtw", window=w)
+        got = gpu.subsequence_search(q, ref, gpu.SearchConfig(spec=spec, normalize=norm))[:2]
+        want = eko.subsequence(spec, "eapruned", q, ref, norm, chunk=256, threads=4)[:2]
+        assert got == want, (lq, n, w, norm)

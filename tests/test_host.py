@@ -1,0 +1,111 @@
+"""Host-side logic of the drop-in API: validation, orientation, backend seam,
+and failing loudly when no GPU is present (there is no CPU fallback)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2102_05221_b200 as ekb
+from paper_2102_05221_b200 import DistanceSpec, SearchConfig, SpecError, make_recurrence
+from paper_2102_05221_b200._backend import resolve
+
+
+@pytest.mark.parametrize(
+    "kwargs",
+    [
+        {"kind": "nope"},
+        {"kind": "dtw", "cost_mode": "cubed"},
+        {"kind": "cdtw"},
+        {"kind": "erp", "erp_gap": 0.0},
+        {"kind": "erp", "window": 3},
+        {"kind": "wdtw"},
+        {"kind": "wdtw", "wdtw_g": -0.1},
+        {"kind": "msm"},
+        {"kind": "msm", "msm_c": -1.0},
+        {"kind": "twe"},
+        {"kind": "twe", "twe_nu": 0.1},
+        {"kind": "twe", "twe_nu": -0.1, "twe_lambda": 1.0},
+        {"kind": "dtw", "window": -1},
+        {"kind": "dtw", "window": 2.5},
+    ],
+)
+def test_spec_validation_errors(kwargs):
+    # the reference's parametrised cases (pkg/tests/test_kernels.py)
+    with pytest.raises(SpecError):
+        DistanceSpec(**kwargs)
+
+
+def test_spec_messages_match_reference():
+    with pytest.raises(SpecError, match="cdtw requires a finite window"):
+        DistanceSpec(kind="cdtw")
+    with pytest.raises(SpecError, match="unknown distance kind 'x'"):
+        DistanceSpec(kind="x")
+
+
+def test_effective_window():
+    assert DistanceSpec(kind="dtw").effective_window(17) == 17
+    assert DistanceSpec(kind="cdtw", window=3).effective_window(17) == 3
+
+
+def test_orientation_longer_on_rows_ties_keep_first(rng):
+    rec = make_recurrence(DistanceSpec(kind="dtw"), rng.normal(0, 1, 4), rng.normal(0, 1, 9))
+    assert rec.shape == (9, 4)
+    a, b = rng.normal(0, 1, 5), rng.normal(0, 1, 5)
+    rec = make_recurrence(DistanceSpec(kind="dtw"), a, b)
+    assert rec.lines.tolist() == a.tolist()
+
+
+def test_as_series_validation():
+    with pytest.raises(ValueError):
+        ekb.as_series([])
+    with pytest.raises(ValueError):
+        ekb.as_series([[1.0, 2.0]])
+    with pytest.raises(ValueError):
+        ekb.as_series([1.0, math.nan])
+
+
+def test_search_config_validation():
+    dtw = DistanceSpec(kind="dtw")
+    with pytest.raises(SpecError):
+        SearchConfig(spec=dtw, variant="hyper")
+    with pytest.raises(SpecError):
+        SearchConfig(spec=dtw, lb="keogh3")
+    with pytest.raises(SpecError):
+        SearchConfig(spec=DistanceSpec(kind="msm", msm_c=0.5), lb="keogh2")
+
+
+def test_backend_seam():
+    with pytest.raises(ValueError):
+        resolve("turbo")
+    with pytest.raises(RuntimeError):
+        resolve("python")  # the reference's CPU engines are not part of this build
+
+
+def test_no_silent_cpu_fallback():
+    if ekb.compiled_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(RuntimeError):
+        ekb.distance(DistanceSpec(kind="dtw"), "base", [1.0, 2.0], [1.0])
+    with pytest.raises(RuntimeError):
+        ekb.nn_search([1.0, 2.0], [[1.0]], SearchConfig(spec=DistanceSpec(kind="dtw")))
+
+
+def test_facade_rejects_unknown_variant():
+    with pytest.raises(SpecError):
+        ekb.distance(DistanceSpec(kind="dtw"), "fast", [1.0], [2.0])
+
+
+def test_wdtw_table_is_libm(rng):
+    t = ekb.wdtw_weight_table(0.17, 219)
+    for d in rng.integers(0, 220, size=5):
+        assert t[int(d)] == 1.0 / (1.0 + math.exp(-0.17 * (int(d) - 219 / 2.0)))
+
+
+def test_generator_is_seeded():
+    from paper_2102_05221_b200 import datagen
+
+    a = datagen.warped_prototypes(5, 64, 2, 0.1, 3)
+    b = datagen.warped_prototypes(5, 64, 2, 0.1, 3)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.allclose(a[0].mean(axis=1), 0, atol=1e-12)
