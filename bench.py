@@ -1,0 +1,526 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 elastic-distance engine on BASELINE.json's workloads.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config c2] [--all]
+
+Headline (one JSON line on rank 0): BASELINE.json configs[1] -- CDTW (w = 10%)
+1-NN with early abandoning, 256 queries x 4096 candidates, length 512, warped-
+prototype data (seeded, synthetic).  A step = one full 1-NN pass (all queries)
+with inputs resident in HBM; L2 is flushed (256 MiB write) between steps.
+`e2e` runs the same workload through the public Python API from host arrays.
+
+Multi-GPU: one process per GPU (torchrun); every rank searches its own 256
+queries against the same candidates -- queries shard with no data-path
+collective, so scaling is "weak"; the step time is the max over ranks.
+
+`--impl reference` times the reference's own compiled kernel
+(oracle/_ref/_speedups*.so, built from /root/reference/pkg/src/elastik/_speedups.pyx)
+driven by the restated nn_search loop, in a process pool over all host cores,
+on a bounded sample of queries per step; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "1-NN queries/s"
+UNIT = "queries/s"
+OPS_PER_CELL = {"dtw": 5, "cdtw": 5, "wdtw": 6, "erp": 7, "msm": 10, "twe": 9}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def dist_init(backend):
+    import torch.distributed as dist
+
+    rank, _, world = dist_env()
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group(backend=backend, rank=rank, world_size=world)
+    return rank, world
+
+
+def dist_max(x: float, device="cpu") -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+def shard_seed(base: int, rank: int) -> int:
+    """Weak scaling: rank r searches its own query set (same candidates)."""
+    return base + 1 + 1000 * rank
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 8:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[4 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- workloads
+
+def spec_for(name):
+    from paper_2102_05221_b200 import DistanceSpec
+
+    return {
+        "c1": DistanceSpec(kind="dtw"),
+        "c2": DistanceSpec(kind="cdtw", window=51),
+        "c3w": DistanceSpec(kind="wdtw", wdtw_g=0.05),
+        "c3e": DistanceSpec(kind="erp", window=25, erp_gap=0.0),
+        "c4m": DistanceSpec(kind="msm", msm_c=1.0),
+        "c4t": DistanceSpec(kind="twe", twe_nu=0.001, twe_lambda=1.0),
+        "c5": DistanceSpec(kind="cdtw", window=51),
+    }[name]
+
+
+def nn_data(name, rank=0):
+    from paper_2102_05221_b200 import datagen
+
+    wl = {"c1": datagen.C1, "c2": datagen.C2, "c4m": datagen.C4, "c4t": datagen.C4}[name]
+    C, cl, protos = datagen.warped_prototypes(wl.n_candidates, wl.length, wl.classes, wl.sigma, wl.seed)
+    Q, ql, _ = datagen.warped_prototypes(wl.n_queries, wl.length, wl.classes, wl.sigma,
+                                         shard_seed(wl.seed, rank), protos=protos)
+    return wl, Q, ql, C, cl
+
+
+WORKLOAD_NAMES = {
+    "c1": "c1_dtw_1nn_16x256_L128", "c2": "c2_cdtw_w51_1nn_256x4096_L512",
+    "c3w": "c3_wdtw_g0.05_allpairs_1024_L256", "c3e": "c3_erp_gap0_w25_allpairs_1024_L256",
+    "c4m": "c4_msm_c1_1nn_512x8192_L512", "c4t": "c4_twe_nu0.001_lam1_1nn_512x8192_L512",
+    "c5": "c5_cdtw_w51_subseq_q1024_stream2^20",
+}
+
+
+# ---------------------------------------------------------------- our arm
+
+class Runner:
+    """Device-resident inputs + one timed 'step' for each workload kind."""
+
+    def __init__(self, name, rank, device):
+        import torch
+
+        from paper_2102_05221_b200 import _lib
+
+        self.name, self.rank, self.device = name, rank, device
+        self.torch = torch
+        self.L = _lib.lib()
+        self.lib = _lib
+        self.spec = spec_for(name)
+        self.kind = self.spec.kind
+        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)
+        if name in ("c1", "c2", "c4m", "c4t"):
+            wl, Q, ql, C, cl = nn_data(name, rank)
+            self.host = (Q, C)
+            self.nq, self.nc, self.Lq = Q.shape[0], C.shape[0], Q.shape[1]
+            self.dQ, self.dC = t(Q.reshape(-1), torch.float64), t(C.reshape(-1), torch.float64)
+            self.dqo = t(np.arange(self.nq) * self.Lq, torch.int64)
+            self.dco = t(np.arange(self.nc) * self.Lq, torch.int64)
+            self.dql = t(np.full(self.nq, self.Lq), torch.int32)
+            self.dcl = t(np.full(self.nc, self.Lq), torch.int32)
+            self.out = torch.empty(5 * self.nq, dtype=torch.int64, device=device)
+            self.h = _lib.SpecHandle(self.spec, longest_lengths=[self.Lq])
+            self.units = self.nq
+            self.pairs = self.nq * self.nc
+            self.cell_full = self.Lq * self.Lq
+            self.unit = "queries/s"
+        elif name in ("c3w", "c3e"):
+            from paper_2102_05221_b200 import datagen
+
+            X, _ = datagen.pairwise_workload(seed=3003 + rank)
+            self.host = (X,)
+            self.n, self.Lq = X.shape
+            self.dX = t(X.reshape(-1), torch.float64)
+            self.doff = t(np.arange(self.n) * self.Lq, torch.int64)
+            self.dlen = t(np.full(self.n, self.Lq), torch.int32)
+            self.dD = torch.empty(self.n * self.n, dtype=torch.float64, device=device)
+            self.h = _lib.SpecHandle(self.spec, longest_lengths=[self.Lq])
+            self.units = 1
+            self.pairs = self.n * (self.n - 1) // 2
+            self.cell_full = self.Lq * self.Lq
+            self.unit = "matrices/s"
+        else:  # c5
+            from paper_2102_05221_b200 import datagen
+
+            stream, q = datagen.subsequence_workload(seed=5005 + rank)
+            self.host = (q, stream)
+            self.Lq, self.nref = len(q), len(stream)
+            self.dq, self.dref = t(q, torch.float64), t(stream, torch.float64)
+            self.h = _lib.SpecHandle(self.spec)
+            self.units = self.nref - self.Lq + 1
+            self.pairs = self.units
+            self.cell_full = self.Lq * self.Lq
+            self.unit = "windows/s"
+        self.last = {}
+
+    def step(self, stream_handle):
+        import ctypes as C
+
+        lib = self.lib
+        if self.name in ("c1", "c2", "c4m", "c4t"):
+            o = self.out.data_ptr()
+            lib.check(self.L.ek_nn_dev(self.h.ref, 2, self.dQ.data_ptr(), self.dqo.data_ptr(), self.dql.data_ptr(),
+                                       self.nq, self.dC.data_ptr(), self.dco.data_ptr(), self.dcl.data_ptr(), self.nc,
+                                       self.Lq, o, o + 8 * self.nq, o + 16 * self.nq, o + 24 * self.nq,
+                                       o + 32 * self.nq, stream_handle))
+        elif self.name in ("c3w", "c3e"):
+            cells = np.zeros(1, dtype=np.int64)
+            lib.check(self.L.ek_pairwise_dev(self.h.ref, 3, self.dX.data_ptr(), self.doff.data_ptr(),
+                                             self.dlen.data_ptr(), self.n, self.Lq, self.dD.data_ptr(),
+                                             lib.iptr(cells), stream_handle))
+            self.last["cells"] = int(cells[0])
+        else:
+            off = np.zeros(1, dtype=np.int64)
+            d = np.zeros(1)
+            cells = np.zeros(1, dtype=np.int64)
+            comp = np.zeros(1, dtype=np.int64)
+            ab = np.zeros(1, dtype=np.int64)
+            lib.check(self.L.ek_subseq_dev(self.h.ref, 2, self.dq.data_ptr(), self.Lq, self.dref.data_ptr(),
+                                           self.nref, 1, lib.iptr(off), lib.dptr(d), lib.iptr(cells),
+                                           lib.iptr(comp), lib.iptr(ab), stream_handle))
+            self.last.update(cells=int(cells[0]), offset=int(off[0]), dist=float(d[0]))
+            _ = C
+
+    def cells_after_step(self):
+        if self.name in ("c1", "c2", "c4m", "c4t"):
+            return int(self.out[2 * self.nq: 3 * self.nq].sum().item())
+        return self.last.get("cells", 0)
+
+    def e2e_call(self):
+        """The same workload through the public API from host arrays (H2D + D2H inside)."""
+        import paper_2102_05221_b200 as ekb
+        from paper_2102_05221_b200 import SearchConfig
+
+        if self.name in ("c1", "c2", "c4m", "c4t"):
+            Q, C = self.host
+            ekb.nn_batch(self.spec, "eapruned", list(Q), list(C))
+            return Q.nbytes + C.nbytes + 12 * (Q.shape[0] + C.shape[0]), 40 * Q.shape[0]
+        if self.name in ("c3w", "c3e"):
+            (X,) = self.host
+            ekb.pairwise(self.spec, list(X), variant="pruned_only")
+            return X.nbytes + 16 * X.shape[0], 8 * X.shape[0] ** 2 + 8
+        q, stream = self.host
+        ekb.subsequence_search(q, stream, SearchConfig(spec=self.spec, variant="eapruned", normalize=True))
+        return q.nbytes + stream.nbytes, 40
+
+
+def phase_times(L):
+    import ctypes as C
+
+    ms = (C.c_double * 16)()
+    names = (C.c_char_p * 16)()
+    n = L.ek_phase_times(ms, names, 16)
+    return {names[k].decode(): ms[k] for k in range(n)}
+
+
+def time_steps(r, steps, warmup, flush):
+    """Per-step device times (CUDA events on the launching stream), L2 flushed between steps."""
+    torch = r.torch
+    s = torch.cuda.current_stream()
+    h = s.cuda_stream
+    assert h != 0, "run on a non-default stream: the library maps handle 0 to its own stream"
+    for _ in range(warmup):
+        flush.zero_()
+        r.step(h)
+    torch.cuda.synchronize()
+    r.L.ek_set_profiling(1)
+    r.L.ek_launch_count(1)
+    dist_barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    phases, cells = [], []
+    t0 = time.perf_counter()
+    for k in range(steps):
+        flush.zero_()  # L2 flush (256 MiB write), outside the event pair
+        ev[k][0].record(s)
+        r.step(h)
+        ev[k][1].record(s)
+        ev[k][1].synchronize()
+        phases.append(phase_times(r.L))
+        cells.append(r.cells_after_step())
+    torch.cuda.synchronize()
+    dist_barrier()
+    wall = time.perf_counter() - t0
+    launches = int(r.L.ek_launch_count(0))
+    r.L.ek_set_profiling(0)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    return step_ms, phases, cells, launches, wall
+
+
+def cpu_baseline_nn(name, budget_queries=None):
+    """The reference's compiled kernel (oracle/_ref) over all host cores on a query sample."""
+    from oracle import refdrive
+
+    cores = len(os.sched_getaffinity(0))
+    wl, Q, ql, C, cl = nn_data(name, 0)
+    spec = spec_for(name)
+    if budget_queries is None:
+        per_q = {"c1": 0.05, "c2": 0.3, "c4m": 2.5, "c4t": 1.8}[name]  # core-seconds per query
+        budget_queries = int(max(cores, min(Q.shape[0], 20.0 * cores / per_q)))
+    nq = min(Q.shape[0], budget_queries)
+    kind = "reference" if refdrive.available() else "port"
+    t0 = time.perf_counter()
+    if kind == "reference":
+        idx, dist, cells = refdrive.nn_pool(spec, "eapruned", Q[:nq], C, procs=cores)
+    else:
+        from oracle import eko
+
+        r = eko.nn(spec, "eapruned", Q[:nq], C, threads=cores)
+        idx, dist, cells = r["nn_index"], r["nn_distance"], r["cells"]
+    wall = time.perf_counter() - t0
+    return {"value": nq / wall, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{nq} of {Q.shape[0]} queries x {C.shape[0]} candidates ({wall:.1f} s wall, "
+                      f"{'process pool' if kind == 'reference' else 'threads'})",
+            "cells": int(np.sum(cells)), "idx": idx, "dist": dist}
+
+
+def cpu_baseline_other(name):
+    from oracle import eko, refdrive
+
+    cores = len(os.sched_getaffinity(0))
+    spec = spec_for(name)
+    kind = "reference" if refdrive.available() else "port"
+    if name in ("c3w", "c3e"):
+        from paper_2102_05221_b200 import datagen
+
+        X, _ = datagen.pairwise_workload()
+        rows = list(range(0, 1024, max(1, 1024 // (8 * cores))))[: 4 * cores]
+        t0 = time.perf_counter()
+        if kind == "reference":
+            refdrive.pairwise_pool(spec, X, rows=rows, procs=cores)
+        else:
+            eko.pairwise(spec, X[: len(rows)], threads=cores)
+        wall = time.perf_counter() - t0
+        npairs = sum(1023 - i for i in rows)
+        total = 1024 * 1023 // 2
+        return {"value": (npairs / total) / wall, "unit": "matrices/s", "cores": cores, "kind": kind,
+                "sample": f"{len(rows)} upper-triangle rows ({npairs} of {total} pairs), {wall:.1f} s"}
+    from paper_2102_05221_b200 import datagen
+
+    stream, q = datagen.subsequence_workload()
+    nwin = len(stream) - len(q) + 1
+    span = min(nwin, 4096 * cores)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        refdrive.subsequence_pool(spec, "eapruned", q, stream[: span + len(q) - 1], True, chunk=2048, procs=cores)
+    else:
+        eko.subsequence(spec, "eapruned", q, stream[: span + len(q) - 1], True, chunk=2048, threads=cores)
+    wall = time.perf_counter() - t0
+    return {"value": span / wall, "unit": "windows/s", "cores": cores, "kind": kind,
+            "sample": f"first {span} of {nwin} windows (chunks of 2048, independent cutoffs), {wall:.1f} s"}
+
+
+def run_ours(args):
+    import torch
+
+    rank, world = dist_init("nccl")
+    _, local, _ = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2102_05221_b200 import _lib
+
+    L = _lib.lib()
+    _lib.check(L.ek_init(local))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    names = [args.config] + ([n for n in WORKLOAD_NAMES if n != args.config] if args.all else [])
+    results = {}
+    peak_ops = L.ek_fp64_peak_ops()
+    work_stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(work_stream)  # events and library launches share this stream
+    for name in names:
+        r = Runner(name, rank, dev)
+        steps = args.steps if name == args.config else max(1, min(args.steps, 3))
+        warm = args.warmup if name == args.config else 1
+        with ClockSampler(local) as clk:
+            step_ms, phases, cells, launches, wall = time_steps(r, steps, warm, flush)
+        ms = float(np.mean(step_ms))
+        ms_max = dist_max(ms, dev)
+        value = world * r.units / (ms_max / 1e3)
+        kern = [k for k in phases[0] if k.startswith(("nn_phase", "triangle", "subseq_phase"))]
+        kern_ms = float(np.mean([sum(p[k] for k in kern) for p in phases]))
+        mean_cells = float(np.mean(cells))
+        ops = mean_cells * OPS_PER_CELL[r.kind]
+        achieved = ops / (kern_ms / 1e3) / 1e12
+        peak = peak_ops / 1e12
+        res = {
+            "value": value, "unit": r.unit, "ms_per_step": ms_max, "step_ms": step_ms,
+            "effective_gcups": world * r.pairs * r.cell_full / (ms_max / 1e3) / 1e9,
+            "computed_gcups": world * mean_cells / (ms_max / 1e3) / 1e9,
+            "computed_cells_per_step": mean_cells,
+            "phases_ms": {k: float(np.mean([p.get(k, 0.0) for p in phases])) for k in phases[0]},
+            "roofline": {"bound": "fp64_alu", "kernel": "+".join(kern), "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak > 0 else None, "traffic": None,
+                         "ops_per_cell": OPS_PER_CELL[r.kind],
+                         "peak_source": "measured FP64 DADD/DMUL microbenchmark (ek_fp64_peak_ops), "
+                                        "MEASURED_PEAKS.json has no FP64 entry"},
+            "gpu_launches": launches // max(1, steps), "clocks": clk.summary(), "wall_s": wall,
+        }
+        # end to end through the public API with host buffers
+        if rank == 0 and not args.no_e2e:
+            t_e2e = []
+            for k in range(max(1, min(steps, 5)) + 1):
+                t0 = time.perf_counter()
+                hb, db = r.e2e_call()
+                if k:
+                    t_e2e.append(time.perf_counter() - t0)
+            res["e2e"] = {"value": r.units / float(np.mean(t_e2e)), "unit": r.unit, "h2d_bytes_per_step": int(hb),
+                          "d2h_bytes_per_step": int(db), "path": "public Python API (pageable numpy in, numpy out)"}
+        results[name] = res
+        del r
+        torch.cuda.empty_cache()
+    if rank != 0:
+        return
+    head = results[args.config]
+    line = {
+        "metric": METRIC if args.config in ("c1", "c2", "c4m", "c4t") else f"{head['unit']}",
+        "value": head["value"], "unit": head["unit"], "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded warped-prototype generator, paper_2102_05221_b200/datagen.py)",
+        "config": {"workload": WORKLOAD_NAMES[args.config], "spec": repr(spec_for(args.config)),
+                   "variant": "eapruned", "l2": "flushed between steps (256 MiB write)",
+                   "shard": "queries per rank (same candidates), no data-path collective"},
+        "effective_gcups": head["effective_gcups"], "computed_gcups": head["computed_gcups"],
+        "roofline": head["roofline"], "phases_ms": head["phases_ms"], "gpu_launches": head["gpu_launches"],
+        "clocks": head["clocks"],
+    }
+    if "e2e" in head:
+        line["e2e"] = head["e2e"]
+    prof = os.path.join(REPO, "profiles", f"ncu_{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            line["roofline"]["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    if not args.no_cpu_baseline:
+        cb = cpu_baseline_nn(args.config) if args.config in ("c1", "c2", "c4m", "c4t") else \
+            cpu_baseline_other(args.config)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if args.all:
+        line["per_config"] = {n: {k: v for k, v in res.items() if k not in ("step_ms",)} for n, res in results.items()
+                              if n != args.config}
+    print(json.dumps(line), flush=True)
+
+
+def run_reference(args):
+    """The reference's CPU implementation, rank 0 only."""
+    rank, world = dist_env()[0], dist_env()[2]
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    vals = []
+    samples = []
+    for k in range(args.warmup + args.steps):
+        if args.config in ("c1", "c2", "c4m", "c4t"):
+            cb = cpu_baseline_nn(args.config, budget_queries=max(cores, {"c1": 16}.get(args.config, 2 * cores)))
+        else:
+            cb = cpu_baseline_other(args.config)
+        if k >= args.warmup:
+            vals.append(cb["value"])
+            samples.append(cb["sample"])
+    value = float(np.mean(vals))
+    line = {
+        "metric": METRIC if args.config in ("c1", "c2", "c4m", "c4t") else cb["unit"], "value": value,
+        "unit": cb["unit"], "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / value if value else None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic (seeded warped-prototype generator)",
+        "config": {"workload": WORKLOAD_NAMES[args.config], "spec": repr(spec_for(args.config)), "variant": "eapruned"},
+        "cpu_baseline": {"value": value, "unit": cb["unit"], "cores": cores, "kind": cb["kind"],
+                         "sample": samples[-1]},
+        "e2e": {"value": value, "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=tuple(WORKLOAD_NAMES), default="c2")
+    ap.add_argument("--all", action="store_true", help="also measure every other BASELINE config")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to the contract minimum of 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
+    _ = math

@@ -46,7 +46,7 @@ typedef struct ek_spec {
   double msm_c;
   double twe_nu;
   double twe_lambda;
-  const double* wdtw_tables;     /* host (or device for _dev calls) */
+  const double* wdtw_tables;     /* host memory, also for _dev calls */
   const int64_t* wdtw_table_off; /* indexed by longest length m */
   int64_t wdtw_max_len;
 } ek_spec;
@@ -100,6 +100,14 @@ int ek_subseq_dev(const ek_spec* spec, int32_t variant, const double* d_query, i
 
 /* Number of kernel launches the library issued since the last reset (bench accounting). */
 int64_t ek_launch_count(int32_t reset);
+
+/* Measurement helpers (bench.py): record CUDA events between the phases of the
+ * next ek_nn / ek_pairwise / ek_subseq call (host or _dev); read back per-phase device times. */
+void ek_set_profiling(int32_t on);
+int32_t ek_phase_times(double* ms, const char** names, int32_t max);
+
+/* Measured FP64 (non-tensor) DADD/DMUL throughput of the device, ops/s. */
+double ek_fp64_peak_ops(void);
 
 #ifdef __cplusplus
 }

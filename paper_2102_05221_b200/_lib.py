@@ -40,6 +40,9 @@ EXPORTS = {
     "ek_device_count": ([], C.c_int),
     "ek_init": ([C.c_int], C.c_int),
     "ek_launch_count": ([C.c_int32], C.c_int64),
+    "ek_set_profiling": ([C.c_int32], None),
+    "ek_phase_times": ([_dp, C.POINTER(C.c_char_p), C.c_int32], C.c_int32),
+    "ek_fp64_peak_ops": ([], C.c_double),
     "ek_distance_batch": ([C.POINTER(EkSpec), C.c_int32, C.c_int64, _dp, C.c_int64, _i64p, _i64p, _i64p, _i64p,
                            _dp, _i64p, _dp, _i64p], C.c_int),
     "ek_nn": ([C.POINTER(EkSpec), C.c_int32, _dp, C.c_int64, _i64p, _i64p, C.c_int64, _dp, C.c_int64, _i64p, _i64p,

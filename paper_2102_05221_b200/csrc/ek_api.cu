@@ -76,6 +76,25 @@ struct Ctx {
 Ctx g_ctx;
 std::mutex g_mu;
 
+// optional phase timing (bench.py): events recorded on the launching stream
+bool g_prof = false;
+constexpr int kMaxMarks = 16;
+cudaEvent_t g_ev[kMaxMarks];
+const char* g_evname[kMaxMarks];
+int g_nev = 0;
+bool g_ev_init = false;
+
+void mark_reset() { g_nev = 0; }
+void mark(cudaStream_t st, const char* name) {
+  if (!g_prof || g_nev >= kMaxMarks) return;
+  if (!g_ev_init) {
+    for (int k = 0; k < kMaxMarks; ++k) cudaEventCreate(&g_ev[k]);
+    g_ev_init = true;
+  }
+  g_evname[g_nev] = name;
+  cudaEventRecord(g_ev[g_nev++], st);
+}
+
 int ensure_ctx() {
   if (g_ctx.ready) return 0;
   int n = 0;
@@ -86,6 +105,11 @@ int ensure_ctx() {
   if (pr.major < 10) return fail("device %d is sm_%d%d; this library is built for sm_100a", g_ctx.dev, pr.major, pr.minor);
   g_ctx.nsm = pr.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking));
+  // keep stream-ordered allocations cached between calls (no re-mapping per call)
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, g_ctx.dev));
+  unsigned long long keep = ~0ULL;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   g_ctx.ready = true;
   return 0;
 }
@@ -145,7 +169,7 @@ __global__ void k_red1_partial(const double* __restrict__ d, const int* __restri
   long long bi = 0x7fffffffffffffffLL, nc = 0, na = 0, cl = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double v = d[i];
-    if (tend[i] > 0) cl += cells_done(eng_diag, S, 1, lq, lq, w, tend[i]);
+    cl += tend[i];  // per-window evaluated cells (k_subseq)
     if (v < __longlong_as_double(0x7ff0000000000000LL)) {
       ++nc;
       if (v < bd || (v == bd && i < bi)) { bd = v; bi = i; }
@@ -270,7 +294,7 @@ struct ParamHolder {
   }
 };
 
-size_t pair_smem(int lmax, int wpb) { return sizeof(double) * (size_t)wpb * (2 * (lmax + 2) + (lmax + 1)); }
+size_t pair_smem(int lmax, int eng, int wpb) { return sizeof(double) * (size_t)wpb * warp_stride(lmax, eng); }
 
 // numpy pairwise-sum plan (see ek_subseq.cuh)
 void np_plan_rec(int start, int n, std::vector<int2>& leaves, std::vector<int>& ops) {
@@ -369,26 +393,20 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
   for (int eng = 0; eng < E_COUNT; ++eng) {
     const size_t n = groups[eng].size();
     if (!n) continue;
-    DBuf dp, dc, dt, dcl;
-    if (dp.alloc(sizeof(PairDesc) * n, st) || dc.alloc(sizeof(double) * n, st) || dt.alloc(sizeof(int) * n, st) ||
-        dcl.alloc(sizeof(long long) * n, st))
+    DBuf dp, dc, dt;
+    if (dp.alloc(sizeof(PairDesc) * n, st) || dc.alloc(sizeof(double) * n, st) || dt.alloc(sizeof(int) * n, st))
       return -1;
     CK(cudaMemcpyAsync(dp.p, groups[eng].data(), sizeof(PairDesc) * n, cudaMemcpyHostToDevice, st));
     const int wpb = 4;
-    const size_t smem = pair_smem(glmax[eng], wpb);
+    const size_t smem = pair_smem(glmax[eng], eng, wpb);
     if (launch_persistent(pick_pairs(spec->kind, spec->cost_mode, eng), 32 * wpb, smem, st, (long long)n,
                           (const double*)dser.as<double>(), (const PairDesc*)dp.as<PairDesc>(), (int)n,
                           glmax[eng], ph.prm, dc.as<double>(), dt.as<int>()))
       return -1;
-    if (launch_plain(k_cells_pairs, dim3((unsigned)std::min<size_t>(1024, (n + 255) / 256)), dim3(256), 0, st,
-                     (const PairDesc*)dp.as<PairDesc>(), (const int*)dt.as<int>(), (int)n,
-                     (int)engine_is_diag(eng), eng_S(eng), kind_tag(spec->kind) == K_ERP ? 0 : 1,
-                     dcl.as<long long>()))
-      return -1;
     std::vector<double> hc(n);
-    std::vector<long long> hcl(n);
+    std::vector<int> hcl(n);
     CK(cudaMemcpyAsync(hc.data(), dc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hcl.data(), dcl.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hcl.data(), dt.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (size_t k = 0; k < n; ++k) {
       out_cost[gidx[eng][k]] = hc[k];
@@ -407,6 +425,8 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
   if (nq <= 0) return 0;
   if (ncand <= 0) return fail("candidate set is empty");
+  mark_reset();
+  mark(st, "start");
   const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
   const int wmax = win < 0 ? max_len : win;
   const int eng = choose_engine(max_len, max_len, wmax, false);
@@ -437,9 +457,10 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   } else {
     if (launch_plain(k_identity_order, dim3(1024), dim3(256), 0, st, (int)nq, (int)ncand, dord.as<int>())) return -1;
   }
+  mark(st, "rank");
   // 2. cutoff seed: exact diagonal upper bound of each query's top-ranked candidate
   if (share) {
-    if (launch_plain(pick_ub(spec->kind, spec->cost_mode), dim3((unsigned)((nq + 127) / 128)), dim3(128), 0, st, dQ,
+    if (launch_plain(pick_ub(spec->kind, spec->cost_mode), dim3((unsigned)((nq + 3) / 4)), dim3(128), 0, st, dQ,
                      (const long long*)dqoff, (const int*)dqlen, (int)nq, dC, (const long long*)dcoff,
                      (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), win, ph.prm,
                      dcut.as<unsigned long long>()))
@@ -449,10 +470,11 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                      0x7ff0000000000000ULL))
       return -1;
   }
+  mark(st, "seed_cutoff");
   // 3. phase A: the top-ranked few per query; phase B: everything else
   const NNFn fn = pick_nn(spec->kind, spec->cost_mode, eng);
   const int wpb = 4;
-  const size_t smem = pair_smem(max_len, wpb);
+  const size_t smem = pair_smem(max_len, eng, wpb);
   const int ka = share ? (int)std::min<int64_t>(4, ncand) : 0;
   if (ka > 0) {
     if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
@@ -461,6 +483,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>()))
       return -1;
   }
+  mark(st, "nn_phaseA");
   if (ka < ncand) {
     const int K = 32;
     const long long items = (long long)nq * ((ncand - ka + K - 1) / K);
@@ -470,12 +493,14 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
       return -1;
   }
+  mark(st, "nn_phaseB");
   // 4. lexicographic (distance, index) minimum + accounting
   if (launch_plain(k_nn_reduce, dim3((unsigned)nq), dim3(256), 0, st, (const double*)dout.as<double>(),
                    (const int*)dtend.as<int>(), (const int*)dqlen, (int)nq, (const int*)dclen, (int)ncand, win,
                    (int)engine_is_diag(eng), eng_S(eng), kind_tag(spec->kind) == K_ERP ? 0 : 1,
                    (long long*)d_idx, d_dist, (long long*)d_cells, (long long*)d_comp, (long long*)d_ab))
     return -1;
+  mark(st, "reduce");
   return 0;
 }
 
@@ -546,20 +571,19 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
   const long long np = n * (n - 1) / 2;
-  DBuf dtend, dcnt, dtot;
-  if (dtend.alloc(sizeof(int) * (size_t)np, st) || dcnt.alloc(8, st) || dtot.alloc(8, st)) return -1;
+  mark_reset();
+  mark(st, "start");
+  DBuf dcnt, dtot;
+  if (dcnt.alloc(8, st) || dtot.alloc(8, st)) return -1;
   CK(cudaMemsetAsync(dcnt.p, 0, 8, st));
   CK(cudaMemsetAsync(dtot.p, 0, 8, st));
   const int wpb = 4;
-  if (launch_persistent(pick_tri(spec->kind, spec->cost_mode, eng), 32 * wpb, pair_smem(max_len, wpb), st, np,
+  if (launch_persistent(pick_tri(spec->kind, spec->cost_mode, eng), 32 * wpb, pair_smem(max_len, eng, wpb), st, np,
                         d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, ph.prm, d_D,
-                        dtend.as<int>(), dcnt.as<int>()))
+                        dtot.as<unsigned long long>(), dcnt.as<int>()))
     return -1;
+  mark(st, "triangle");
   if (cells) {
-    if (launch_plain(k_cells_triangle, dim3(256), dim3(256), 0, st, (const int*)d_len, (int)n, win,
-                     (const int*)dtend.as<int>(), (int)engine_is_diag(eng), eng_S(eng),
-                     kind_tag(spec->kind) == K_ERP ? 0 : 1, dtot.as<unsigned long long>()))
-      return -1;
     unsigned long long tot = 0;
     CK(cudaMemcpyAsync(&tot, dtot.p, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -625,6 +649,8 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   CK(cudaMemcpyAsync(dops.p, ops.data(), sizeof(int) * ops.size(), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(dcnt.p, 0, 16, st));
   NpPlan plan{dleaves.as<int2>(), (int)leaves.size(), dops.as<int>(), (int)ops.size()};
+  mark_reset();
+  mark(st, "start");
   const int nl_ = plan.nleaves;
   unsigned long long cut0 = 0x7ff0000000000000ULL;
   std::vector<long long> seeds;
@@ -652,9 +678,10 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     }
   }
   CK(cudaMemcpyAsync(dcut.p, &cut0, 8, cudaMemcpyHostToDevice, st));
+  mark(st, "seed_bounds");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
   const int wpb = 8;
-  const size_t smem = sizeof(double) * ((size_t)lq + 2 + nl_ + 16 + wpb * ((size_t)lq + 32 + 2 + nl_ + 16));
+  const size_t smem = sizeof(double) * ((size_t)subseq_head((int)lq, nl_, eng) + wpb * (size_t)subseq_warp((int)lq, nl_));
   if (!seeds.empty()) {
     DBuf dseed, dso, dst;
     const long long ns = (long long)seeds.size();
@@ -666,10 +693,12 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
       return -1;
     CK(cudaStreamSynchronize(st));
   }
+  mark(st, "subseq_phaseA");
   if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, dq, (int)lq, dref, (long long)nref, (int)normalize,
                         (const long long*)nullptr, nwin, win, plan, (int)share, dcut.as<unsigned long long>(),
                         dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
     return -1;
+  mark(st, "subseq_phaseB");
   // reduce
   const int nb = (int)std::min<long long>(1024, (nwin + 255) / 256);
   DBuf pd, pi, pc, pa, pcl;
@@ -730,6 +759,81 @@ int ek_subseq(const ek_spec* spec, int32_t variant, const double* query, int64_t
   CK(cudaMemcpyAsync(dr.p, reference, sizeof(double) * n_ref, cudaMemcpyHostToDevice, st));
   return subseq_dev_impl(spec, variant, dq.as<double>(), lq, dr.as<double>(), n_ref, normalize, best_off, best_dist,
                          cells, computed, abandoned, st);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+void ek_set_profiling(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_prof = on != 0;
+}
+
+// Device time (ms) between consecutive phase marks of the last profiled call;
+// names[k] labels the phase ending at mark k+1.  Returns the number of phases.
+int32_t ek_phase_times(double* ms, const char** names, int32_t max) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int n = 0;
+  for (int k = 1; k < g_nev && n < max; ++k, ++n) {
+    cudaEventSynchronize(g_ev[k]);
+    float v = 0.f;
+    cudaEventElapsedTime(&v, g_ev[k - 1], g_ev[k]);
+    ms[n] = v;
+    if (names) names[n] = g_evname[k];
+  }
+  return n;
+}
+
+}  // extern "C"
+
+// ---- FP64 roofline denominator (bench.py) ---------------------------------------
+
+namespace {
+
+__global__ void k_fp64_peak(double* out, int iters, double a, double b) {
+  // 8 independent DADD/DMUL chains per thread: the FP64 pipe's throughput
+  double r0 = threadIdx.x * 1e-9, r1 = r0 + 1, r2 = r0 + 2, r3 = r0 + 3, r4 = r0 + 4, r5 = r0 + 5, r6 = r0 + 6,
+         r7 = r0 + 7;
+  for (int i = 0; i < iters; ++i) {
+    r0 = __dadd_rn(r0, a); r1 = __dmul_rn(r1, b); r2 = __dadd_rn(r2, a); r3 = __dmul_rn(r3, b);
+    r4 = __dadd_rn(r4, a); r5 = __dmul_rn(r5, b); r6 = __dadd_rn(r6, a); r7 = __dmul_rn(r7, b);
+  }
+  const double s = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+
+}  // namespace
+
+extern "C" {
+
+// Measured FP64 (non-tensor) add/mul throughput of this device in ops/s (best of 5).
+double ek_fp64_peak_ops(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1.0;
+  cudaStream_t st = g_ctx.stream;
+  double* d = nullptr;
+  if (cudaMalloc(&d, 8) != cudaSuccess) return -1.0;
+  const int block = 256, iters = 1 << 14;
+  const int grid = g_ctx.nsm * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_fp64_peak<<<grid, block, 0, st>>>(d, 256, 1.0000001, 0.9999999);
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, st);
+    k_fp64_peak<<<grid, block, 0, st>>>(d, iters, 1.0000001, 0.9999999);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return (double)grid * block * iters * 8.0 / (best * 1e-3);
 }
 
 }  // extern "C"

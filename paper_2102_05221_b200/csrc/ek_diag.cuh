@@ -18,6 +18,9 @@
 // "virtual" diagonals just outside the band hold their border value at their
 // border time and +inf otherwise, which reproduces the reference's window
 // (hborder for j <= w+1, vborder while jstart == 1; _speedups.pyx:137-148).
+// Cells before a diagonal's border time evaluate to +inf (their inputs are
+// +inf and the padded series values are finite); cells past the end of the
+// matrix are never read by a cell inside it.
 //
 // Pruning/abandoning: every path crosses one of any two consecutive
 // anti-diagonals, so when no cell of (t, t+1) is <= cutoff the pair is
@@ -25,7 +28,10 @@
 // cells on its optimal path are <= cost), so the observable contract is the
 // reference eapruned's: exact when cost <= cutoff, +inf otherwise
 // (engines.py:72-84).  With a shared cutoff that only tightens,
-// the same argument holds against the final cutoff.
+// the same argument holds against the final cutoff.  The liveness test compares
+// the high 32-bit words of the IEEE images (values are >= +0 or +inf, the
+// cutoff is canonicalised by the host: NaN -> -inf, -0.0 -> +0.0), which is
+// conservative -- it can only keep a pair alive longer, never change a result.
 #pragma once
 #include "ek_common.cuh"
 
@@ -44,34 +50,49 @@ __device__ __forceinline__ double ld_cut(const unsigned long long* p) {
   return __longlong_as_double((long long)v);
 }
 
+__device__ __forceinline__ int hi_word(double v) { return __double2hiint(v); }
+
+// Loader protocol: next_t(dlo, dhi, H) = first double-step time at which the
+// engine needs data beyond what is staged; ensure(t, dlo, dhi, H) stages more.
 struct NoLoader {
-  __device__ __forceinline__ void ensure(int, int) {}
+  __device__ __forceinline__ int next_t(int, int, int) const { return 0x7fffffff; }
+  __device__ __forceinline__ void ensure(int, int, int, int) {}
 };
 
-// Series accessor over shared memory: valid for indices -1..n (pads set by the stager).
+// Padding (elements) the diagonal engine may read beyond either end of a
+// series, for P slots per lane: i = (t + d)/2 ranges over [-16P-2, n + 16P + 2].
+__host__ __device__ constexpr int diag_pad(int P) { return 16 * P + 8; }
+
+// Series accessor over shared memory padded on both sides (see stage_series):
+// index -1 holds the kind's "previous of the first element", indices < -1 hold
+// 0.0, indices >= n hold +inf.
 struct SmemSeries {
   const double* p;
   int n;
-  __device__ __forceinline__ double at(int k) const { return p[min(max(k, -1), n)]; }
+  __device__ __forceinline__ double at(int k) const { return p[k]; }
 };
 
-// X: lines accessor (nl >= nc), Y: cols accessor; at(k) is defined for every k
-// (clamped to the pads at -1 and n).  w: effective window (w >= nl - nc, checked by the caller).
+// X: lines accessor (nl >= nc), Y: cols accessor.  w: effective window
+// (w >= nl - nc, checked by the caller).
 template <int KIND, int MODE, int P, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
 __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
                                 const unsigned long long* cutp, const Params& prm, Loader& ld) {
   static_assert(P % 2 == 0 && P >= 2, "P must be even");
   constexpr int H = P / 2;
+  constexpr bool BORDERED = (KIND == K_ERP);
   const int lane = threadIdx.x & 31;
   const int dlo = max(-w, 1 - nc), dhi = min(w, nl - 1);
   const int dbase = (dlo - 1) & ~1;  // floor to even, includes the lower virtual diagonal
   const int d0 = dbase + lane * P;
-  constexpr bool BORDERED = (KIND == K_ERP);
 
-  ld.ensure((2 + dhi + 3) / 2 + 1 + H, (2 + 3 - dlo) / 2 + 2);
+  int t_load = ld.next_t(dlo, dhi, H);
+  if (t_load <= 2) {
+    ld.ensure(2, dlo, dhi, H);
+    t_load = ld.next_t(dlo, dhi, H);
+  }
   double val[P];
   bool upd[P];
-  int tb[P];  // border time of a virtual diagonal (ERP only), else -1
+  int tb[P];  // ERP: border time of a virtual diagonal, else -1
   DiagK<KIND> kk[P];
   SlotS<KIND> st[P];
 #pragma unroll
@@ -93,54 +114,63 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     }
   }
 
-  auto cx = [&](int k) { return X.at(k); };
-  auto cy = [&](int k) { return Y.at(k); };
-
   int t = 2;
   int I0 = (t + d0) >> 1, J0 = (t - d0) >> 1;
   RowD<KIND> xw[H + 1];
   ColD<KIND> yw[H];
 #pragma unroll
-  for (int k = 0; k <= H; ++k) xw[k] = make_row<KIND, MODE>(cx(I0 + k - 1), cx(I0 + k - 2), prm);
+  for (int k = 0; k <= H; ++k) xw[k] = make_row<KIND, MODE>(X.at(I0 + k - 1), X.at(I0 + k - 2), prm);
 #pragma unroll
-  for (int m = 0; m < H; ++m) yw[m] = make_col<KIND, MODE>(cy(J0 - m - 1), cy(J0 - m - 2), prm);
+  for (int m = 0; m < H; ++m) yw[m] = make_col<KIND, MODE>(Y.at(J0 - m - 1), Y.at(J0 - m - 2), prm);
 
   const int Tf = nl + nc;
   int iter = 0;
   double nextcut = cut;
+  int cut_hi = hi_word(cut);
   bool dead = false;
   for (;;) {
     if constexpr (SHARED_CUT) {
       if ((iter & 15) == 0) nextcut = ld_cut(cutp);
-      if ((iter & 15) == 12) cut = fmin(cut, nextcut);
+      if ((iter & 15) == 12) {
+        cut = fmin(cut, nextcut);
+        cut_hi = hi_word(cut);
+      }
     }
     bool alive = false;
     // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
     double tin = __shfl_up_sync(FULL, val[P - 1], 1);
-    if (lane == 0) tin = EKB_INF;
+    if constexpr (BORDERED) {
+      if (lane == 0) tin = EKB_INF;
+    }
 #pragma unroll
     for (int m = 0; m < H; ++m) {
       const int p = 2 * m;
       const double T = (m == 0) ? tin : val[p - 1];
-      double v = cell<KIND, MODE>(val[p], T, val[p + 1], xw[m], yw[m], kk[p], st[p], prm);
-      bool keep = upd[p];
-      if constexpr (BORDERED) keep = keep || (tb[p] == t);
-      val[p] = keep ? v : EKB_INF;
-      alive |= (val[p] <= cut);
+      const double v = cell<KIND, MODE>(val[p], T, val[p + 1], xw[m], yw[m], kk[p], st[p], prm);
+      if constexpr (BORDERED) {
+        val[p] = (upd[p] || tb[p] == t) ? v : EKB_INF;
+      } else {
+        if (upd[p]) val[p] = v;
+      }
+      alive |= hi_word(val[p]) <= cut_hi;
     }
     if (t >= Tf) break;
     // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
     double lin = __shfl_down_sync(FULL, val[0], 1);
-    if (lane == 31) lin = EKB_INF;
+    if constexpr (BORDERED) {
+      if (lane == 31) lin = EKB_INF;
+    }
 #pragma unroll
     for (int m = 0; m < H; ++m) {
       const int p = 2 * m + 1;
       const double L = (p == P - 1) ? lin : val[p + 1];
-      double v = cell<KIND, MODE>(val[p], val[p - 1], L, xw[m + 1], yw[m], kk[p], st[p], prm);
-      bool keep = upd[p];
-      if constexpr (BORDERED) keep = keep || (tb[p] == t + 1);
-      val[p] = keep ? v : EKB_INF;
-      alive |= (val[p] <= cut);
+      const double v = cell<KIND, MODE>(val[p], val[p - 1], L, xw[m + 1], yw[m], kk[p], st[p], prm);
+      if constexpr (BORDERED) {
+        val[p] = (upd[p] || tb[p] == t + 1) ? v : EKB_INF;
+      } else {
+        if (upd[p]) val[p] = v;
+      }
+      alive |= hi_word(val[p]) <= cut_hi;
     }
     if (t + 1 >= Tf) break;
     if (!__any_sync(FULL, alive)) { dead = true; break; }
@@ -149,13 +179,16 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     ++I0;
     ++J0;
     ++iter;
-    ld.ensure((t + dhi + 3) / 2 + 1 + H, (t + 3 - dlo) / 2 + 2);
+    if (t >= t_load) {
+      ld.ensure(t, dlo, dhi, H);
+      t_load = ld.next_t(dlo, dhi, H);
+    }
 #pragma unroll
     for (int k = 0; k < H; ++k) xw[k] = xw[k + 1];
-    xw[H] = make_row<KIND, MODE>(cx(I0 + H - 1), xw[H - 1].x, prm);
+    xw[H] = make_row<KIND, MODE>(X.at(I0 + H - 1), xw[H - 1].x, prm);
 #pragma unroll
     for (int m = H - 1; m > 0; --m) yw[m] = yw[m - 1];
-    yw[0] = make_col<KIND, MODE>(cy(J0 - 1), yw[0].y, prm);
+    yw[0] = make_col<KIND, MODE>(Y.at(J0 - 1), yw[0].y, prm);
   }
 
   DiagResult res;

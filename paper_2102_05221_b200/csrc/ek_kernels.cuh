@@ -4,14 +4,14 @@
 //                 _speedups.run / engines.distance (engines.py:121-147)
 //   k_triangle  : the all-pairs upper triangle, mirrored
 //   k_nn        : 1-NN search with a per-query shared cutoff (search.py:81-160)
-//   k_subseq    : z-normalised subsequence search (search.py:163-215)
-//   k_nn_reduce : lexicographic (distance, index) minimum per query
+//   (k_subseq in ek_subseq.cuh, k_nn_reduce in ek_misc.cu)
 //
-// All kernels are warp-per-pair and persistent (grid = a multiple of the SM
-// count, work claimed with an atomic counter).  Series are staged into shared
-// memory per warp with coalesced loads; the 1-NN kernel loads a candidate
-// lazily in 64-element chunks because most pairs are abandoned within the
-// first few anti-diagonals.
+// All kernels are warp-per-pair and persistent (grid = SM count x resident
+// blocks, work claimed with an atomic counter).  Series are staged into padded
+// per-warp shared-memory buffers with coalesced loads; the 1-NN kernel stages a
+// candidate lazily in 128-element chunks (most pairs are abandoned within the
+// first few anti-diagonals) and prefetches the next candidate's first chunk into
+// registers while the current pair runs.
 #pragma once
 #include "ek_common.cuh"
 #include "ek_diag.cuh"
@@ -32,6 +32,15 @@ enum Engine : int {
 __host__ __device__ constexpr int engine_is_diag(int e) { return e <= E_DIAG16; }
 __host__ __device__ constexpr int engine_P(int e) { return e == E_DIAG4 ? 4 : e == E_DIAG8 ? 8 : 16; }
 __host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e == E_STR8 ? 8 : 16; }
+// elements an engine may read beyond either end of a staged series
+__host__ __device__ constexpr int engine_pad(int e) {
+  return engine_is_diag(e) ? diag_pad(engine_P(e)) : 40;  // stripe: rows stream past the ends by < 32
+}
+// per-warp shared-memory layout: [pad | X lmax | pad][pad | Y lmax | pad][tab lmax+1]
+__host__ __device__ constexpr int series_slot(int lmax, int pad) { return lmax + 2 * pad; }
+__host__ __device__ constexpr int warp_stride(int lmax, int e) {
+  return 2 * series_slot(lmax, engine_pad(e)) + (engine_is_diag(e) ? 0 : lmax + 1);
+}
 
 struct PairDesc {
   long long xoff, yoff;  // lines / cols offsets into the series buffer
@@ -43,14 +52,21 @@ struct PairDesc {
 
 // ---- staging helpers -------------------------------------------------------
 
+// pads: index -1 = the kind's predecessor of element 0, [-pad, -2] = 0.0, [n, n+pad) = +inf
 template <int KIND>
-__device__ __forceinline__ void stage_series(double* dst, const double* __restrict__ src, int n) {
+__device__ __forceinline__ void stage_pads(double* dst, int n, int pad, double first) {
+  const int lane = threadIdx.x & 31;
+  for (int k = lane + 1; k <= pad; k += 32) {
+    dst[-k] = (k == 1) ? pad_before<KIND>(first) : 0.0;
+    dst[n + k - 1] = EKB_INF;
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void stage_series(double* dst, const double* __restrict__ src, int n, int pad) {
   const int lane = threadIdx.x & 31;
   for (int k = lane; k < n; k += 32) dst[k] = src[k];
-  if (lane == 0) {
-    dst[-1] = pad_before<KIND>(src[0]);
-    dst[n] = EKB_INF;
-  }
+  stage_pads<KIND>(dst, n, pad, src[0]);
 }
 
 template <int KIND>
@@ -84,28 +100,48 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
   }
 }
 
+// Band cells an engine evaluated before it stopped at t_end (warp-parallel; every
+// lane returns the total): the diagonal engine evaluates each band cell with
+// i + j <= t_end, the stripe engine row i of lane l while l <= r0 + t_end - 1 - i.
+template <int ENG>
+__device__ __forceinline__ int warp_cells(int nl, int nc, int w, int tend, int r0) {
+  const int lane = threadIdx.x & 31;
+  constexpr bool DIAG = engine_is_diag(ENG);
+  constexpr int S = engine_S(ENG);
+  const int imax = DIAG ? min(nl, tend - 1) : min(nl, r0 + tend - 1);
+  int c = 0;
+  for (int i = 1 + lane; i <= imax; i += 32) {
+    const int jlo = max(1, i - w);
+    int jhi = min(nc, i + w);
+    jhi = DIAG ? min(jhi, tend - i) : min(jhi, (r0 + tend - i) * S);
+    c += max(0, jhi - jlo + 1);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  return c;
+}
+
 // ---- generic pair list ------------------------------------------------------
-// smem per warp: X (lmax+2) + Y (lmax+2) + tab (lmax+1) doubles
 
 template <int KIND, int MODE, int ENG>
 __global__ void __launch_bounds__(128) k_pairs(const double* __restrict__ series, const PairDesc* __restrict__ pairs,
                                                int npairs, int lmax, Params prm, double* __restrict__ out_cost,
                                                int* __restrict__ out_tend) {
   extern __shared__ double smem[];
+  constexpr int PAD = engine_pad(ENG);
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int stride = 2 * (lmax + 2) + (lmax + 1);
-  double* X = smem + wib * stride + 1;
-  double* Y = X + (lmax + 2);
-  double* tab = Y + (lmax + 1);
+  double* X = smem + wib * warp_stride(lmax, ENG) + PAD;
+  double* Y = X + series_slot(lmax, PAD);
+  double* tab = Y - PAD + series_slot(lmax, PAD);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   NoLoader ld;
   for (int pid = blockIdx.x * (blockDim.x >> 5) + wib; pid < npairs; pid += nwarps) {
     const PairDesc pd = pairs[pid];
     const Params pp = pair_params(prm, pd.nl);
     __syncwarp();
-    stage_series<KIND>(X, series + pd.xoff, pd.nl);
-    stage_series<KIND>(Y, series + pd.yoff, pd.nc);
+    stage_series<KIND>(X, series + pd.xoff, pd.nl, PAD);
+    stage_series<KIND>(Y, series + pd.yoff, pd.nc, PAD);
     const int tablen = max(pd.nl, pd.nc) + 1;
     if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
     __syncwarp();
@@ -113,9 +149,10 @@ __global__ void __launch_bounds__(128) k_pairs(const double* __restrict__ series
     int tend;
     run_engine<KIND, MODE, ENG, false>(SmemSeries{X, pd.nl}, pd.nl, SmemSeries{Y, pd.nc}, pd.nc, pd.w, pd.cut,
                                        nullptr, tab, tablen, pp, ld, cost, tend);
+    const int cells = warp_cells<ENG>(pd.nl, pd.nc, pd.w, tend, KIND == K_ERP ? 0 : 1);
     if (lane == 0) {
       out_cost[pid] = cost;
-      out_tend[pid] = tend;
+      out_tend[pid] = cells;
     }
   }
 }
@@ -139,17 +176,18 @@ __device__ __forceinline__ void tri_index(long long p, int n, int& i, int& j) {
 template <int KIND, int MODE, int ENG>
 __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ series, const long long* __restrict__ off,
                                                   const int* __restrict__ len, int n, int win, int lmax, Params prm,
-                                                  double* __restrict__ D, int* __restrict__ tend_out,
+                                                  double* __restrict__ D, unsigned long long* __restrict__ cells_total,
                                                   int* __restrict__ counter) {
   extern __shared__ double smem[];
+  constexpr int PAD = engine_pad(ENG);
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int stride = 2 * (lmax + 2) + (lmax + 1);
-  double* X = smem + wib * stride + 1;
-  double* Y = X + (lmax + 2);
-  double* tab = Y + (lmax + 1);
+  double* X = smem + wib * warp_stride(lmax, ENG) + PAD;
+  double* Y = X + series_slot(lmax, PAD);
+  double* tab = Y - PAD + series_slot(lmax, PAD);
   const long long npairs = (long long)n * (n - 1) / 2;
   NoLoader ld;
+  unsigned long long my_cells = 0;
   for (;;) {
     long long p = 0;
     if (lane == 0) p = (long long)atomicAdd((unsigned long long*)counter, 1ULL);
@@ -167,25 +205,28 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
     if (w >= nl - nc) {
       const Params pp = pair_params(prm, nl);
       __syncwarp();
-      stage_series<KIND>(X, series + off[s], nl);
-      stage_series<KIND>(Y, series + off[t], nc);
+      stage_series<KIND>(X, series + off[s], nl, PAD);
+      stage_series<KIND>(Y, series + off[t], nc, PAD);
       const int tablen = max(nl, nc) + 1;
       if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
       __syncwarp();
       run_engine<KIND, MODE, ENG, false>(SmemSeries{X, nl}, nl, SmemSeries{Y, nc}, nc, w, EKB_INF, nullptr, tab,
                                          tablen, pp, ld, cost, tend);
+      my_cells += (unsigned long long)warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1);
     }
     if (lane == 0) {
       D[(long long)a * n + b] = cost;
       D[(long long)b * n + a] = cost;
-      if (tend_out) tend_out[p] = tend;
     }
   }
+  if (lane == 0 && cells_total) atomicAdd(cells_total, my_cells);
 }
 
 // ---- 1-NN with a shared per-query cutoff -----------------------------------------
 
-// Lazily staged candidate: 64-element chunks on demand.
+constexpr int kChunk = 128;  // candidate staging granule (4 doubles per lane)
+
+// Lazily staged candidate; the first chunk arrives prefetched.
 struct LazyCand {
   double* buf;
   const double* src;
@@ -196,14 +237,24 @@ struct LazyCand {
     const int lane = threadIdx.x & 31;
     while (loaded < need) {
       const int base = loaded;
-      for (int k = lane; k < 64 && base + k < n; k += 32) buf[base + k] = __ldg(src + base + k);
-      loaded = min(base + 64, n);
+#pragma unroll
+      for (int u = 0; u < kChunk / 32; ++u) {
+        const int k = base + u * 32 + lane;
+        if (k < n) buf[k] = __ldg(src + k);
+      }
+      loaded = min(base + kChunk, n);
     }
     __syncwarp();
   }
-  __device__ __forceinline__ void ensure(int needX, int needY) {
-    const int need = is_x ? needX : needY;
-    if (need > loaded) load_to(need);
+  // diag engine protocol (see ek_diag.cuh): data needed by the double step at t
+  // and the window slide after it: lines up to (t+dhi+3)/2+1+H, cols up to (t+3-dlo)/2+2.
+  __device__ __forceinline__ int next_t(int dlo, int dhi, int H) const {
+    if (loaded >= n) return 0x7fffffff;
+    return is_x ? 2 * (loaded - 2 - H) - dhi - 5 : 2 * (loaded - 3) + dlo - 5;
+  }
+  __device__ __forceinline__ void ensure(int t, int dlo, int dhi, int H) {
+    const int ahead = t + 2 * kChunk;  // stage one chunk ahead of the wavefront
+    load_to(is_x ? (ahead + dhi + 3) / 2 + 2 + H : (ahead + 3 - dlo) / 2 + 3);
   }
 };
 
@@ -213,20 +264,20 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
                                             const long long* __restrict__ coff, const int* __restrict__ clen,
                                             int ncand, const int* __restrict__ order, int rank_lo, int rank_hi,
                                             int K, int win, int lmax, Params prm, int share,
-                                            unsigned long long* cutbits,
-                                            double* __restrict__ out, int* __restrict__ tend_out,
-                                            int* __restrict__ counter) {
+                                            unsigned long long* cutbits, double* __restrict__ out,
+                                            int* __restrict__ tend_out, int* __restrict__ counter) {
   extern __shared__ double smem[];
+  constexpr int PAD = engine_pad(ENG);
+  constexpr int PF = kChunk / 32;
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int stride = 2 * (lmax + 2) + (lmax + 1);
-  double* QB = smem + wib * stride + 1;
-  double* CB = QB + (lmax + 2);
-  double* tab = CB + (lmax + 1);
+  double* QB = smem + wib * warp_stride(lmax, ENG) + PAD;
+  double* CB = QB + series_slot(lmax, PAD);
+  double* tab = CB - PAD + series_slot(lmax, PAD);
   const int span = rank_hi - rank_lo;
   const int rounds = (span + K - 1) / K;
   const long long nitems = (long long)rounds * nq;
-  int staged_q = -1;
+  int staged_q = -1, cb_len = -1;
   for (;;) {
     long long it = 0;
     if (lane == 0) it = (long long)atomicAdd((unsigned long long*)counter, 1ULL);
@@ -237,34 +288,58 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
     const int lq = qlen[q];
     if (q != staged_q) {
       __syncwarp();
-      stage_series<KIND>(QB, Q + qoff[q], lq);
+      stage_series<KIND>(QB, Q + qoff[q], lq, PAD);
       staged_q = q;
     }
     const int k_lo = rank_lo + r * K, k_hi = min(k_lo + K, rank_hi);
+    // this item's candidates, one per lane (K <= 32), and the first one's chunk
+    const int ord = (k_lo + lane < k_hi) ? order[(long long)q * ncand + k_lo + lane] : 0;
+    int c_next = __shfl_sync(FULL, ord, 0);
+    double pf[PF];
+    {
+      const double* s = C + coff[c_next];
+      const int lc = clen[c_next];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < lc) ? __ldg(s + u * 32 + lane) : 0.0;
+    }
+    double cut = ld_cut(cutbits + q);
+    double pending = cut;  // cutoff refresh issued at the end of the previous pair
     for (int k = k_lo; k < k_hi; ++k) {
-      const int c = order[(long long)q * ncand + k];
+      cut = fmin(cut, pending);
+      const int c = c_next;
       const int lc = clen[c];
+      const double* csrc = C + coff[c];
       // orientation (kernels.py:168-171): query is s, candidate is t
       const bool q_rows = lq >= lc;
       const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
       const int w = win < 0 ? nl : win;
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < PF; ++u)
+        if (u * 32 + lane < lc) CB[u * 32 + lane] = pf[u];
+      const double first = __shfl_sync(FULL, pf[0], 0);
+      if (lc != cb_len || KIND == K_MSM) {
+        stage_pads<KIND>(CB, lc, PAD, first);
+        cb_len = lc;
+      }
+      if (k + 1 < k_hi) {  // prefetch the next candidate's first chunk
+        c_next = __shfl_sync(FULL, ord, k + 1 - k_lo);
+        const double* s = C + coff[c_next];
+        const int ln = clen[c_next];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < ln) ? __ldg(s + u * 32 + lane) : 0.0;
+      }
       double cost = EKB_INF;
       int tend = 0;
       if (w >= nl - nc) {
         const Params pp = pair_params(prm, nl);
-        __syncwarp();
-        if (lane == 0) {
-          CB[-1] = pad_before<KIND>(C[coff[c]]);
-          CB[lc] = EKB_INF;
-        }
-        LazyCand ld{CB, C + coff[c], lc, 0, !q_rows};
+        LazyCand ld{CB, csrc, lc, min(kChunk, lc), !q_rows};
         const int tablen = max(nl, nc) + 1;
         if constexpr (!engine_is_diag(ENG)) {
           ld.load_to(lc);  // the stripe engine reads all columns up front
           stage_table<KIND>(tab, tablen, pp);
         }
         __syncwarp();
-        const double cut = ld_cut(cutbits + q);
         const SmemSeries X{q_rows ? QB : CB, nl};
         const SmemSeries Y{q_rows ? CB : QB, nc};
         run_engine<KIND, MODE, ENG, true>(X, nl, Y, nc, w, cut, cutbits + q, tab, tablen, pp, ld, cost, tend);
@@ -272,11 +347,14 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
           // values are >= 0 (or +inf), so IEEE bits order as unsigned integers
           atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
         }
+        if (share) cut = fmin(cut, cost);
       }
+      const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) : 0;
       if (lane == 0) {
         out[(long long)q * ncand + c] = cost;
-        tend_out[(long long)q * ncand + c] = tend;
+        tend_out[(long long)q * ncand + c] = cells;
       }
+      if (share) pending = ld_cut(cutbits + q);
     }
   }
 }

@@ -6,7 +6,8 @@
 namespace ekb {
 
 using PairsFn = void (*)(const double*, const PairDesc*, int, int, Params, double*, int*);
-using TriFn = void (*)(const double*, const long long*, const int*, int, int, int, Params, double*, int*, int*);
+using TriFn = void (*)(const double*, const long long*, const int*, int, int, int, Params, double*,
+                      unsigned long long*, int*);
 using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, int, int, int, int, Params, int, unsigned long long*,
                       double*, int*, int*);
@@ -15,12 +16,42 @@ using UBFn = void (*)(const double*, const long long*, const int*, int, const do
 
 // diagonal_upper_bound (engines.py:87-103): the diagonal then the last column, summed
 // sequentially in DP order, used to seed a query's cutoff with an exact path cost.
+// One warp per query: lanes evaluate 32 terms at a time, lane 0 adds them in order.
 template <int KIND, int MODE>
-__global__ void k_ub_init(const double* __restrict__ Q, const long long* __restrict__ qoff,
-                          const int* __restrict__ qlen, int nq, const double* __restrict__ C,
-                          const long long* __restrict__ coff, const int* __restrict__ clen, int ncand,
-                          const int* __restrict__ order, int win, Params prm, unsigned long long* cutbits) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ double ub_term(const double* X, const double* Y, int nc, int k, const Params& pp) {
+  auto xv = [&](int i) { return i < 0 ? pad_before<KIND>(X[0]) : X[i]; };
+  auto yv = [&](int j) { return j < 0 ? pad_before<KIND>(Y[0]) : Y[j]; };
+  if (k <= nc) {  // canonical(k, k)
+    const RowD<KIND> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
+    const double y = yv(k - 1);
+    if constexpr (KIND == K_WDTW) return dmul(pcost<MODE>(r.x, y), pp.wt[0]);
+    else if constexpr (KIND == K_MSM) return fabs(dsub(r.x, y));
+    else if constexpr (KIND == K_TWE)
+      return dadd(dadd(pcost<MODE>(r.x, y), pcost<MODE>(k >= 2 ? X[k - 2] : 0.0, k >= 2 ? Y[k - 2] : 0.0)),
+                  dmul(pp.nu, dadd(0.0, 0.0)));
+    else return pcost<MODE>(r.x, y);
+  }
+  // alt_row(k, nc) for the rows below the diagonal's end
+  const RowD<KIND> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
+  const double y = Y[nc - 1];
+  if constexpr (KIND == K_WDTW) return dmul(pcost<MODE>(r.x, y), pp.wt[k - nc]);
+  else if constexpr (KIND == K_ERP || KIND == K_TWE) return r.ar;
+  else if constexpr (KIND == K_MSM) {
+    const double e = dsub(r.x, y);
+    const bool brow = ((r.f & 1) && e <= 0.0) || ((r.f & 2) && e >= 0.0);
+    return msm_alt(brow, pp.msm_c, r.dr, fabs(e));
+  } else return pcost<MODE>(r.x, y);
+}
+
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(128) k_ub_init(const double* __restrict__ Q, const long long* __restrict__ qoff,
+                                                 const int* __restrict__ qlen, int nq, const double* __restrict__ C,
+                                                 const long long* __restrict__ coff, const int* __restrict__ clen,
+                                                 int ncand, const int* __restrict__ order, int win, Params prm,
+                                                 unsigned long long* cutbits) {
+  __shared__ double terms[4][32];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * 4 + wib;
   if (q >= nq) return;
   const int c = order ? order[(long long)q * ncand] : 0;
   const int lq = qlen[q], lc = clen[c];
@@ -30,40 +61,22 @@ __global__ void k_ub_init(const double* __restrict__ Q, const long long* __restr
   const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
   const int w = win < 0 ? nl : win;
   if (w < nl - nc) {
-    cutbits[q] = 0x7ff0000000000000ULL;
+    if (lane == 0) cutbits[q] = 0x7ff0000000000000ULL;
     return;
   }
   const Params pp = pair_params(prm, nl);
-  auto xv = [&](int k) { return k < 0 ? pad_before<KIND>(X[0]) : X[k]; };
-  auto yv = [&](int k) { return k < 0 ? pad_before<KIND>(Y[0]) : Y[k]; };
   double total = 0.0;
-  for (int k = 1; k <= nc; ++k) {  // canonical(k, k)
-    RowD<KIND> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
-    ColD<KIND> cd = make_col<KIND, MODE>(yv(k - 1), yv(k - 2), pp);
-    double cost;
-    if constexpr (KIND == K_DTW || KIND == K_CDTW) cost = pcost<MODE>(r.x, cd.y);
-    else if constexpr (KIND == K_WDTW) cost = dmul(pcost<MODE>(r.x, cd.y), pp.wt[0]);
-    else if constexpr (KIND == K_ERP) cost = pcost<MODE>(r.x, cd.y);
-    else if constexpr (KIND == K_MSM) cost = fabs(dsub(r.x, cd.y));
-    else cost = dadd(dadd(pcost<MODE>(r.x, cd.y), pcost<MODE>(k >= 2 ? X[k - 2] : 0.0, k >= 2 ? Y[k - 2] : 0.0)),
-                     dmul(pp.nu, dadd(0.0, 0.0)));
-    total = dadd(total, cost);
-  }
-  for (int i = nc + 1; i <= nl; ++i) {  // alt_row(i, nc)
-    RowD<KIND> r = make_row<KIND, MODE>(xv(i - 1), xv(i - 2), pp);
-    const double y = Y[nc - 1];
-    double cost;
-    if constexpr (KIND == K_DTW || KIND == K_CDTW) cost = pcost<MODE>(r.x, y);
-    else if constexpr (KIND == K_WDTW) cost = dmul(pcost<MODE>(r.x, y), pp.wt[i - nc]);
-    else if constexpr (KIND == K_ERP || KIND == K_TWE) cost = r.ar;
-    else {
-      const double e = dsub(r.x, y);
-      const bool brow = ((r.f & 1) && e <= 0.0) || ((r.f & 2) && e >= 0.0);
-      cost = msm_alt(brow, pp.msm_c, r.dr, fabs(e));
+  for (int base = 1; base <= nl; base += 32) {
+    const int k = base + lane;
+    terms[wib][lane] = (k <= nl) ? ub_term<KIND, MODE>(X, Y, nc, k, pp) : 0.0;
+    __syncwarp();
+    if (lane == 0) {
+      const int m = min(32, nl - base + 1);
+      for (int u = 0; u < m; ++u) total = dadd(total, terms[wib][u]);
     }
-    total = dadd(total, cost);
+    __syncwarp();
   }
-  cutbits[q] = (unsigned long long)__double_as_longlong(total);
+  if (lane == 0) cutbits[q] = (unsigned long long)__double_as_longlong(total);
 }
 
 #define EKB_ENG_CASES(M, FN)                                                                         \

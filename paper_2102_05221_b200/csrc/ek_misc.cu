@@ -93,17 +93,12 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const double* __restrict__ di
                                                    long long* __restrict__ cells, long long* __restrict__ computed,
                                                    long long* __restrict__ abandoned) {
   const int q = blockIdx.x;
-  const int lq = qlen[q];
   double bd = __longlong_as_double(0x7ff0000000000000LL);
   int bi = 0x7fffffff;
   long long nc_ = 0, ab = 0, cl = 0;
   for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
     const double d = dist[(long long)q * ncand + c];
-    const int te = tend[(long long)q * ncand + c];
-    const int lc = clen[c];
-    const int nl = max(lq, lc), ncc = min(lq, lc);
-    const int w = win < 0 ? nl : win;
-    if (te > 0) cl += cells_done(eng_diag, S, r0, nl, ncc, w, te);
+    cl += tend[(long long)q * ncand + c];  // per-pair evaluated cells (k_nn)
     if (d < __longlong_as_double(0x7ff0000000000000LL)) {
       ++nc_;
       if (d < bd || (d == bd && c < bi)) { bd = d; bi = c; }
@@ -138,31 +133,6 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const double* __restrict__ di
     computed[q] = s1[0];
     abandoned[q] = s2[0];
   }
-}
-
-// Cells per pair for the pair-list / triangle kernels.
-__global__ void k_cells_pairs(const PairDesc* __restrict__ pairs, const int* __restrict__ tend, int npairs,
-                              int eng_diag, int S, int r0, long long* __restrict__ out) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
-    const PairDesc pd = pairs[p];
-    out[p] = tend[p] > 0 ? cells_done(eng_diag, S, r0, pd.nl, pd.nc, pd.w, tend[p]) : 0;
-  }
-}
-
-__global__ void k_cells_triangle(const int* __restrict__ len, int n, int win, const int* __restrict__ tend,
-                                 int eng_diag, int S, int r0, unsigned long long* __restrict__ total) {
-  const long long np = (long long)n * (n - 1) / 2;
-  unsigned long long acc = 0;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < np;
-       p += (long long)gridDim.x * blockDim.x) {
-    int a, b;
-    tri_index(p, n, a, b);
-    const int nl = max(len[a], len[b]), nc = min(len[a], len[b]);
-    const int w = win < 0 ? nl : win;
-    if (tend[p] > 0) acc += cells_done(eng_diag, S, r0, nl, nc, w, tend[p]);
-  }
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(total, acc);
 }
 
 }  // namespace ekb

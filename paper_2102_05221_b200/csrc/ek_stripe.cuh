@@ -42,8 +42,8 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   const int lf = (nc - 1) / S;      // lane holding column nc
   const bool lane_on = jbase < nc;
 
-  auto cy = [&](int k) { return Y.at(k); };
-  auto cx = [&](int k) { return X.at(k); };
+  auto cy = [&](int k) { return Y.at(min(max(k, -1), nc)); };  // column records: once per pair
+  auto cx = [&](int k) { return X.at(k); };                      // rows: padded by >= 40
 
   ColD<KIND> cols[S];
   double val[S];
