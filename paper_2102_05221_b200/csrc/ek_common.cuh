@@ -96,16 +96,20 @@ EKB_DI ColD<KIND> make_col(double y, double yp, const Params& p) {
 }
 
 // ---- per-diagonal constant and per-slot state ----
-template <int KIND> struct DiagK {};
-template <> struct DiagK<K_WDTW> { double w; };
+// off: +inf for a diagonal outside the band (its cells must stay +inf), 0.0 inside;
+// the DTW family adds it to the move cost, which replaces two selects per cell.
+template <int KIND> struct DiagK { double off; };
+template <> struct DiagK<K_WDTW> { double w, off; };
 template <> struct DiagK<K_TWE> { double tw; };
 template <int KIND> struct SlotS {};
 template <> struct SlotS<K_TWE> { double pcp; };  // pc(l_{i-2}, c_{j-2}) = previous cell's pc on this diagonal
 
 template <int KIND>
-EKB_DI DiagK<KIND> make_diag(int d, const Params& p) {
+EKB_DI DiagK<KIND> make_diag(int d, const Params& p, bool in_band = true) {
   DiagK<KIND> k;
   int ad = d < 0 ? -d : d;
+  if constexpr (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW || KIND == K_ERP || KIND == K_MSM)
+    k.off = in_band ? 0.0 : EKB_INF;
   if constexpr (KIND == K_WDTW) k.w = (ad < p.wt_len) ? p.wt[ad] : 0.0;  // wt[|i-j|]
   if constexpr (KIND == K_TWE) {
     double dij = (double)ad;
@@ -122,14 +126,16 @@ EKB_DI double msm_alt(bool between, double c, double dother, double de) {
 }
 
 // One cell.  D, T, L are the dependency values; the result is the reference's
-// value bit-for-bit whenever the dependencies are.
-template <int KIND, int MODE>
+// value bit-for-bit whenever the dependencies are.  (For the DTW family the
+// band offset k.off is folded into the cost: cost + 0.0 == cost exactly.)
+template <int KIND, int MODE, bool OFF = true>
 EKB_DI double cell(double D, double T, double L, const RowD<KIND>& r, const ColD<KIND>& c,
                    const DiagK<KIND>& k, SlotS<KIND>& st, const Params& p) {
   if constexpr (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW) {
     // all three move costs are equal: min(D+c, T+c, L+c) == min(D,T,L)+c (monotone rounding)
     double cost = pcost<MODE>(r.x, c.y);
     if constexpr (KIND == K_WDTW) cost = dmul(cost, k.w);
+    if constexpr (OFF) cost = dadd(cost, k.off);  // +0.0 in band (exact), +inf outside
     double m = dmin_ref(D, T);
     m = dmin_ref(m, L);
     return dadd(m, cost);

@@ -80,6 +80,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   static_assert(P % 2 == 0 && P >= 2, "P must be even");
   constexpr int H = P / 2;
   constexpr bool BORDERED = (KIND == K_ERP);
+  // the DTW family masks out-of-band diagonals through their cost (+inf offset)
+  constexpr bool COST_MASK = (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW);
   const int lane = threadIdx.x & 31;
   const int dlo = max(-w, 1 - nc), dhi = min(w, nl - 1);
   const int dbase = (dlo - 1) & ~1;  // floor to even, includes the lower virtual diagonal
@@ -100,7 +102,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     const int d = d0 + p;
     upd[p] = (d >= dlo) && (d <= dhi);
     tb[p] = (BORDERED && (d == dlo - 1 || d == dhi + 1)) ? (d < 0 ? -d : d) : -1;
-    kk[p] = make_diag<KIND>(d, prm);
+    kk[p] = make_diag<KIND>(d, prm, upd[p] || !COST_MASK);
     val[p] = EKB_INF;
     if constexpr (KIND == K_TWE) st[p].pcp = 0.0;
     if (d == 0) val[p] = 0.0;  // corner, t = 0
@@ -124,75 +126,80 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   for (int m = 0; m < H; ++m) yw[m] = make_col<KIND, MODE>(Y.at(J0 - m - 1), Y.at(J0 - m - 2), prm);
 
   const int Tf = nl + nc;
-  int iter = 0;
-  double nextcut = cut;
   int cut_hi = hi_word(cut);
   bool dead = false;
-  for (;;) {
+  bool done = false;
+  while (!done) {
+    double nextcut = cut;
+    if constexpr (SHARED_CUT) nextcut = ld_cut(cutp);  // consumed after this block of double steps
+#pragma unroll 1
+    for (int u = 0; u < 16; ++u) {
+      bool alive = false;
+      // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
+      double tin = __shfl_up_sync(FULL, val[P - 1], 1);
+      if constexpr (BORDERED) {
+        if (lane == 0) tin = EKB_INF;
+      }
+#pragma unroll
+      for (int m = 0; m < H; ++m) {
+        const int p = 2 * m;
+        const double T = (m == 0) ? tin : val[p - 1];
+        const double v = cell<KIND, MODE>(val[p], T, val[p + 1], xw[m], yw[m], kk[p], st[p], prm);
+        if constexpr (BORDERED) {
+          val[p] = (upd[p] || tb[p] == t) ? v : EKB_INF;
+        } else if constexpr (COST_MASK) {
+          val[p] = v;
+        } else {
+          val[p] = upd[p] ? v : EKB_INF;
+        }
+        alive |= hi_word(val[p]) <= cut_hi;
+      }
+      // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
+      double lin = __shfl_down_sync(FULL, val[0], 1);
+      if constexpr (BORDERED) {
+        if (lane == 31) lin = EKB_INF;
+      }
+#pragma unroll
+      for (int m = 0; m < H; ++m) {
+        const int p = 2 * m + 1;
+        const double L = (p == P - 1) ? lin : val[p + 1];
+        const double v = cell<KIND, MODE>(val[p], val[p - 1], L, xw[m + 1], yw[m], kk[p], st[p], prm);
+        if constexpr (BORDERED) {
+          val[p] = (upd[p] || tb[p] == t + 1) ? v : EKB_INF;
+        } else if constexpr (COST_MASK) {
+          val[p] = v;
+        } else {
+          val[p] = upd[p] ? v : EKB_INF;
+        }
+        alive |= hi_word(val[p]) <= cut_hi;
+      }
+      // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
+      // slot, which half step B (odd slots) leaves untouched
+      if (t + 1 >= Tf) { done = true; break; }
+      if (!__any_sync(FULL, alive)) { dead = true; done = true; break; }
+      // ---- slide the register windows by one element ----
+      t += 2;
+      ++I0;
+      ++J0;
+      if (t >= t_load) {
+        ld.ensure(t, dlo, dhi, H);
+        t_load = ld.next_t(dlo, dhi, H);
+      }
+#pragma unroll
+      for (int k = 0; k < H; ++k) xw[k] = xw[k + 1];
+      xw[H] = make_row<KIND, MODE>(X.at(I0 + H - 1), xw[H - 1].x, prm);
+#pragma unroll
+      for (int m = H - 1; m > 0; --m) yw[m] = yw[m - 1];
+      yw[0] = make_col<KIND, MODE>(Y.at(J0 - 1), yw[0].y, prm);
+    }
     if constexpr (SHARED_CUT) {
-      if ((iter & 15) == 0) nextcut = ld_cut(cutp);
-      if ((iter & 15) == 12) {
-        cut = fmin(cut, nextcut);
-        cut_hi = hi_word(cut);
-      }
+      cut = fmin(cut, nextcut);
+      cut_hi = hi_word(cut);
     }
-    bool alive = false;
-    // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
-    double tin = __shfl_up_sync(FULL, val[P - 1], 1);
-    if constexpr (BORDERED) {
-      if (lane == 0) tin = EKB_INF;
-    }
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      const int p = 2 * m;
-      const double T = (m == 0) ? tin : val[p - 1];
-      const double v = cell<KIND, MODE>(val[p], T, val[p + 1], xw[m], yw[m], kk[p], st[p], prm);
-      if constexpr (BORDERED) {
-        val[p] = (upd[p] || tb[p] == t) ? v : EKB_INF;
-      } else {
-        if (upd[p]) val[p] = v;
-      }
-      alive |= hi_word(val[p]) <= cut_hi;
-    }
-    if (t >= Tf) break;
-    // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
-    double lin = __shfl_down_sync(FULL, val[0], 1);
-    if constexpr (BORDERED) {
-      if (lane == 31) lin = EKB_INF;
-    }
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      const int p = 2 * m + 1;
-      const double L = (p == P - 1) ? lin : val[p + 1];
-      const double v = cell<KIND, MODE>(val[p], val[p - 1], L, xw[m + 1], yw[m], kk[p], st[p], prm);
-      if constexpr (BORDERED) {
-        val[p] = (upd[p] || tb[p] == t + 1) ? v : EKB_INF;
-      } else {
-        if (upd[p]) val[p] = v;
-      }
-      alive |= hi_word(val[p]) <= cut_hi;
-    }
-    if (t + 1 >= Tf) break;
-    if (!__any_sync(FULL, alive)) { dead = true; break; }
-    // ---- slide the register windows by one element ----
-    t += 2;
-    ++I0;
-    ++J0;
-    ++iter;
-    if (t >= t_load) {
-      ld.ensure(t, dlo, dhi, H);
-      t_load = ld.next_t(dlo, dhi, H);
-    }
-#pragma unroll
-    for (int k = 0; k < H; ++k) xw[k] = xw[k + 1];
-    xw[H] = make_row<KIND, MODE>(X.at(I0 + H - 1), xw[H - 1].x, prm);
-#pragma unroll
-    for (int m = H - 1; m > 0; --m) yw[m] = yw[m - 1];
-    yw[0] = make_col<KIND, MODE>(Y.at(J0 - 1), yw[0].y, prm);
   }
 
   DiagResult res;
-  res.t_end = dead ? t + 1 : Tf;
+  res.t_end = dead ? t + 1 : Tf;  // last anti-diagonal evaluated
   if (dead) {
     res.cost = EKB_INF;
     return res;

@@ -117,7 +117,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
     for (int s = 0; s < S; ++s) {
       const int j = jbase + 1 + s;
       const double up = val[s];
-      DiagK<KIND> k;
+      DiagK<KIND> k{};  // off = 0.0: the stripe engine masks the band itself
       if constexpr (KIND == K_WDTW) k.w = tab[min(abs(i - j), tablen - 1)];
       if constexpr (TWE) k.tw = tab[min(abs(i - j), tablen - 1)];
       SlotS<KIND> stt;
@@ -126,7 +126,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
         stt.pcp = dpc;
         upc = pcr[s];
       }
-      double v = cell<KIND, MODE>(dgl, up, lft, rd, cols[s], k, stt, prm);
+      double v = cell<KIND, MODE, false>(dgl, up, lft, rd, cols[s], k, stt, prm);
       if constexpr (BANDED) v = (s >= a && s <= b) ? v : EKB_INF;
       if constexpr (TWE) {
         pcr[s] = stt.pcp;  // pc(l_i, c_j) for the next row
