@@ -230,7 +230,7 @@ class Runner:
             o = self.out.data_ptr()
             lib.check(self.L.ek_nn_dev(self.h.ref, 2, self.dQ.data_ptr(), self.dqo.data_ptr(), self.dql.data_ptr(),
                                        self.nq, self.dC.data_ptr(), self.dco.data_ptr(), self.dcl.data_ptr(), self.nc,
-                                       self.Lq, o, o + 8 * self.nq, o + 16 * self.nq, o + 24 * self.nq,
+                                       self.Lq, 1, o, o + 8 * self.nq, o + 16 * self.nq, o + 24 * self.nq,
                                        o + 32 * self.nq, stream_handle))
         elif self.name in ("c3w", "c3e"):
             cells = np.zeros(1, dtype=np.int64)

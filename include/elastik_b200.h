@@ -73,11 +73,13 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
           const int64_t* c_len, int64_t n_cands, int64_t* nn_idx, double* nn_dist, int64_t* cells,
           int64_t* computed, int64_t* abandoned);
 
-/* Same with device-resident inputs/outputs (lengths as int32, offsets int64) on `stream`. */
+/* Same with device-resident inputs/outputs (lengths as int32, offsets int64) on `stream`.
+ * dense != 0 promises every series has length max_len (enables the LB_Keogh pre-filter
+ * for dtw/cdtw, which drops only candidates whose bound proves a +inf result). */
 int ek_nn_dev(const ek_spec* spec, int32_t variant, const double* d_queries, const int64_t* d_q_off,
               const int32_t* d_q_len, int64_t n_queries, const double* d_cands, const int64_t* d_c_off,
-              const int32_t* d_c_len, int64_t n_cands, int32_t max_len, int64_t* d_nn_idx, double* d_nn_dist,
-              int64_t* d_cells, int64_t* d_computed, int64_t* d_abandoned, void* stream);
+              const int32_t* d_c_len, int64_t n_cands, int32_t max_len, int32_t dense, int64_t* d_nn_idx,
+              double* d_nn_dist, int64_t* d_cells, int64_t* d_computed, int64_t* d_abandoned, void* stream);
 
 /* Full symmetric matrix D[n*n] of distance(spec, variant, X_i, X_j); diagonal 0.0.
  * cells: total band cells evaluated. */

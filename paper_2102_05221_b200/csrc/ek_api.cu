@@ -419,8 +419,8 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
 
 static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, const int64_t* dqoff,
                        const int32_t* dqlen, int64_t nq, const double* dC, const int64_t* dcoff, const int32_t* dclen,
-                       int64_t ncand, int32_t max_len, int64_t* d_idx, double* d_dist, int64_t* d_cells,
-                       int64_t* d_comp, int64_t* d_ab, cudaStream_t st) {
+                       int64_t ncand, int32_t max_len, int32_t dense, int64_t* d_idx, double* d_dist,
+                       int64_t* d_cells, int64_t* d_comp, int64_t* d_ab, cudaStream_t st) {
   if (check_spec(spec)) return -1;
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
   if (nq <= 0) return 0;
@@ -432,10 +432,12 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   const int eng = choose_engine(max_len, max_len, wmax, false);
   if (eng < 0) return fail("series length %d with window %d exceeds this build's engines", max_len, wmax);
   const bool share = variant == 1 || variant == 2;  // base / pruned_only compute every candidate exactly
+  // LB_Keogh pre-filter (dtw/cdtw, equal lengths): drops candidates whose bound proves +inf
+  const bool use_lb = share && dense && (spec->kind == K_DTW || spec->kind == K_CDTW) && ncand > 4;
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
   const long long npairs = (long long)nq * ncand;
-  DBuf dord, dkeys, dout, dtend, dcut, dcnt;
+  DBuf dord, dkeys, dout, dtend, dcut, dcnt, denv;
   if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dout.alloc(sizeof(double) * (size_t)npairs, st) ||
       dtend.alloc(sizeof(int) * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
       dcnt.alloc(sizeof(int) * 4 * 2, st))
@@ -480,17 +482,39 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
                           (const int*)dord.as<int>(), 0, ka, 1, win, (int)max_len, ph.prm, (int)share,
-                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>()))
+                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>(),
+                          (const int*)nullptr, (const double*)nullptr, (const double*)nullptr))
       return -1;
   }
   mark(st, "nn_phaseA");
-  if (ka < ncand) {
-    const int K = 32;
-    const long long items = (long long)nq * ((ncand - ka + K - 1) / K);
+  const double* env_up = nullptr;
+  const double* env_lo = nullptr;
+  if (use_lb) {
+    // envelopes of the candidates; phase B tests lb_keogh per pair before its DP
+    const int L = max_len;
+    if (denv.alloc(sizeof(double) * 2 * (size_t)L * ncand, st)) return -1;
+    double* up = denv.as<double>();
+    double* lo = up + (size_t)L * ncand;
+    if (launch_plain(k_envelope, dim3((unsigned)ncand), dim3(256), sizeof(double) * 5 * (size_t)L, st, dC,
+                     (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, up, lo))
+      return -1;
+    env_up = up;
+    env_lo = lo;
+    mark(st, "envelope");
+  }
+  // phase B in two segments: the next-best ranks (where the survivors concentrate)
+  // one pair per item for load balance, the rest in items of 8
+  const int kb1 = (int)std::min<int64_t>(ncand, ka + 64);
+  const int seg_lo[2] = {ka, kb1}, seg_hi[2] = {kb1, (int)ncand}, seg_k[2] = {1, 8};
+  for (int sgi = 0; sgi < 2; ++sgi) {
+    if (seg_lo[sgi] >= seg_hi[sgi]) continue;
+    const int K = seg_k[sgi];
+    const long long items = (long long)nq * ((seg_hi[sgi] - seg_lo[sgi] + K - 1) / K);
     if (launch_persistent(fn, 32 * wpb, smem, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
-                          (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), ka,
-                          (int)ncand, K, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
-                          dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
+                          (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(),
+                          seg_lo[sgi], seg_hi[sgi], K, win, (int)max_len, ph.prm, (int)share,
+                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
+                          dcnt.as<int>() + 2 + 2 * sgi, (const int*)nullptr, env_up, env_lo))
       return -1;
   }
   mark(st, "nn_phaseB");
@@ -506,13 +530,13 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
 
 int ek_nn_dev(const ek_spec* spec, int32_t variant, const double* d_queries, const int64_t* d_q_off,
               const int32_t* d_q_len, int64_t n_queries, const double* d_cands, const int64_t* d_c_off,
-              const int32_t* d_c_len, int64_t n_cands, int32_t max_len, int64_t* d_nn_idx, double* d_nn_dist,
-              int64_t* d_cells, int64_t* d_computed, int64_t* d_abandoned, void* stream) {
+              const int32_t* d_c_len, int64_t n_cands, int32_t max_len, int32_t dense, int64_t* d_nn_idx,
+              double* d_nn_dist, int64_t* d_cells, int64_t* d_computed, int64_t* d_abandoned, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (ensure_ctx()) return -1;
   cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
   return nn_dev_impl(spec, variant, d_queries, d_q_off, d_q_len, n_queries, d_cands, d_c_off, d_c_len, n_cands,
-                     max_len, d_nn_idx, d_nn_dist, d_cells, d_computed, d_abandoned, st);
+                     max_len, dense, d_nn_idx, d_nn_dist, d_cells, d_computed, d_abandoned, st);
 }
 
 int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,
@@ -527,6 +551,10 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   int32_t mx = 0;
   for (int64_t k = 0; k < n_queries; ++k) mx = std::max(mx, ql[k] = (int32_t)q_len[k]);
   for (int64_t k = 0; k < n_cands; ++k) mx = std::max(mx, cl[k] = (int32_t)c_len[k]);
+  // dense: every series has length mx (required by the transposed LB envelopes)
+  int32_t dense = 1;
+  for (int64_t k = 0; k < n_queries && dense; ++k) dense = ql[k] == mx;
+  for (int64_t k = 0; k < n_cands && dense; ++k) dense = cl[k] == mx;
   DBuf dq, dqo, dql, dc, dco, dcl, dout;
   if (dq.alloc(sizeof(double) * q_total, st) || dqo.alloc(8 * n_queries, st) || dql.alloc(4 * n_queries, st) ||
       dc.alloc(sizeof(double) * c_total, st) || dco.alloc(8 * std::max<int64_t>(1, n_cands), st) ||
@@ -542,7 +570,7 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   }
   int64_t* o = dout.as<int64_t>();
   if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
-                  dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, o, (double*)(o + n_queries), o + 2 * n_queries,
+                  dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, dense, o, (double*)(o + n_queries), o + 2 * n_queries,
                   o + 3 * n_queries, o + 4 * n_queries, st))
     return -1;
   CK(cudaMemcpyAsync(nn_idx, o, 8 * n_queries, cudaMemcpyDeviceToHost, st));

@@ -16,6 +16,7 @@
 #include "ek_common.cuh"
 #include "ek_diag.cuh"
 #include "ek_stripe.cuh"
+#include "ek_lb.cuh"
 
 namespace ekb {
 
@@ -65,8 +66,16 @@ __device__ __forceinline__ void stage_pads(double* dst, int n, int pad, double f
 template <int KIND>
 __device__ __forceinline__ void stage_series(double* dst, const double* __restrict__ src, int n, int pad) {
   const int lane = threadIdx.x & 31;
-  for (int k = lane; k < n; k += 32) dst[k] = src[k];
-  stage_pads<KIND>(dst, n, pad, src[0]);
+  int k = lane;
+  for (; k + 7 * 32 < n; k += 8 * 32) {  // eight loads in flight per lane before the stores
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + k + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dst[k + 32 * u] = v[u];
+  }
+  for (; k < n; k += 32) dst[k] = __ldg(src + k);
+  stage_pads<KIND>(dst, n, pad, __ldg(src));
 }
 
 template <int KIND>
@@ -265,7 +274,9 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
                                             int ncand, const int* __restrict__ order, int rank_lo, int rank_hi,
                                             int K, int win, int lmax, Params prm, int share,
                                             unsigned long long* cutbits, double* __restrict__ out,
-                                            int* __restrict__ tend_out, int* __restrict__ counter) {
+                                            int* __restrict__ tend_out, int* __restrict__ counter,
+                                            const int* __restrict__ counts, const double* __restrict__ env_up,
+                                            const double* __restrict__ env_lo) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
   constexpr int PF = kChunk / 32;
@@ -286,17 +297,25 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
     const int q = (int)(it % nq);
     const int r = (int)(it / nq);
     const int lq = qlen[q];
+    const int hi_q = counts ? min(rank_hi, counts[q]) : rank_hi;  // LB survivors per query
+    const int k_lo = rank_lo + r * K, k_hi = min(k_lo + K, hi_q);
+    if (k_lo >= k_hi) continue;
     if (q != staged_q) {
       __syncwarp();
       stage_series<KIND>(QB, Q + qoff[q], lq, PAD);
       staged_q = q;
     }
-    const int k_lo = rank_lo + r * K, k_hi = min(k_lo + K, rank_hi);
     // this item's candidates, one per lane (K <= 32), and the first one's chunk
     const int ord = (k_lo + lane < k_hi) ? order[(long long)q * ncand + k_lo + lane] : 0;
     int c_next = __shfl_sync(FULL, ord, 0);
+    // LB_Keogh pre-test (dtw/cdtw, equal lengths; env_up != nullptr): prefetch the next
+    // candidate's first envelope chunk; otherwise its first data chunk
+    const bool use_lb = env_up != nullptr;
     double pf[PF];
-    {
+    double eu[LB_BATCH], el[LB_BATCH];
+    if (use_lb) {
+      lb_load(env_up + (long long)c_next * lmax, env_lo + (long long)c_next * lmax, 0, lmax, eu, el);
+    } else {
       const double* s = C + coff[c_next];
       const int lc = clen[c_next];
 #pragma unroll
@@ -313,25 +332,51 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
       const bool q_rows = lq >= lc;
       const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
       const int w = win < 0 ? nl : win;
-      __syncwarp();
+      bool evaluate = w >= nl - nc;
+      if (use_lb) {
+        double eu0[LB_BATCH], el0[LB_BATCH];
 #pragma unroll
-      for (int u = 0; u < PF; ++u)
-        if (u * 32 + lane < lc) CB[u * 32 + lane] = pf[u];
-      const double first = __shfl_sync(FULL, pf[0], 0);
-      if (lc != cb_len || KIND == K_MSM) {
-        stage_pads<KIND>(CB, lc, PAD, first);
-        cb_len = lc;
-      }
-      if (k + 1 < k_hi) {  // prefetch the next candidate's first chunk
-        c_next = __shfl_sync(FULL, ord, k + 1 - k_lo);
-        const double* s = C + coff[c_next];
-        const int ln = clen[c_next];
+        for (int b = 0; b < LB_BATCH; ++b) {
+          eu0[b] = eu[b];
+          el0[b] = el[b];
+        }
+        if (k + 1 < k_hi) {  // prefetch the next candidate's first envelope batch
+          c_next = __shfl_sync(FULL, ord, k + 1 - k_lo);
+          lb_load(env_up + (long long)c_next * lmax, env_lo + (long long)c_next * lmax, 0, lmax, eu, el);
+        }
+        evaluate = evaluate && warp_lb_pass<MODE>(QB, env_up + (long long)c * lmax, env_lo + (long long)c * lmax,
+                                                  lc, lb_threshold(cut), eu0, el0);
+        if (evaluate) {  // survivor: stage its first chunk now
+          __syncwarp();
 #pragma unroll
-        for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < ln) ? __ldg(s + u * 32 + lane) : 0.0;
+          for (int u = 0; u < PF; ++u)
+            if (u * 32 + lane < lc) CB[u * 32 + lane] = __ldg(csrc + u * 32 + lane);
+          if (lc != cb_len) {
+            stage_pads<KIND>(CB, lc, PAD, 0.0);
+            cb_len = lc;
+          }
+        }
+      } else {
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < PF; ++u)
+          if (u * 32 + lane < lc) CB[u * 32 + lane] = pf[u];
+        const double first = __shfl_sync(FULL, pf[0], 0);
+        if (lc != cb_len || KIND == K_MSM) {
+          stage_pads<KIND>(CB, lc, PAD, first);
+          cb_len = lc;
+        }
+        if (k + 1 < k_hi) {  // prefetch the next candidate's first chunk
+          c_next = __shfl_sync(FULL, ord, k + 1 - k_lo);
+          const double* s = C + coff[c_next];
+          const int ln = clen[c_next];
+#pragma unroll
+          for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < ln) ? __ldg(s + u * 32 + lane) : 0.0;
+        }
       }
       double cost = EKB_INF;
       int tend = 0;
-      if (w >= nl - nc) {
+      if (evaluate) {
         const Params pp = pair_params(prm, nl);
         LazyCand ld{CB, csrc, lc, min(kChunk, lc), !q_rows};
         const int tablen = max(nl, nc) + 1;

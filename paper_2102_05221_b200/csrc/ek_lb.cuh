@@ -1,0 +1,77 @@
+// ek_lb.cuh -- LB_Keogh pre-test for dtw/cdtw 1-NN.
+//
+// Reference: lower_bounds.build_envelope / lb_keogh (pkg/src/elastik/lower_bounds.py:23-84)
+// and their use as a skip test in search.nn_search (search.py:104-112).  Here the
+// bound is a *scheduling* filter: a candidate is dropped only when its bound
+// proves the DP result would be +inf anyway, so the 1-NN answer is unchanged
+// (result invariance across lb modes: pkg/tests/test_search.py:59-76).
+//
+// Soundness in floating point: every alignment path in the band matches each
+// query point i with some candidate point j, |i-j| <= w, so its cost is at
+// least sum_i dist(q_i, [L_i, U_i]).  The computed bound carries at most ~4n
+// ulps of relative error and the DP value at most ~2n ulps (n <= 2^13 terms of
+// non-negative sums), so a candidate is skipped only when
+// lb > cutoff * (1 + 2^-32), far above both error bounds.
+// (k_envelope, which builds the envelopes, lives in ek_misc.cu.)
+#pragma once
+#include "ek_common.cuh"
+#include "ek_diag.cuh"
+
+namespace ekb {
+
+// Warp-cooperative lb_keogh(q, env(c)) test with early exit.  Points are taken in
+// batches of LB_BATCH x 32 (lane = point within a 32-point chunk); the first batch
+// arrives prefetched, later batches are loaded together so their latency overlaps.
+// The test fails as soon as the running total exceeds thr.
+constexpr int LB_BATCH = 4;
+
+template <int MODE>
+__device__ __forceinline__ double lb_terms(const double* qs, int base, int L, const double (&u)[LB_BATCH],
+                                           const double (&l)[LB_BATCH]) {
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+#pragma unroll
+  for (int b = 0; b < LB_BATCH; ++b) {
+    const int k = base + b * 32 + lane;
+    if (k < L) {
+      const double qi = qs[k];
+      const double d = qi > u[b] ? qi - u[b] : (qi < l[b] ? l[b] - qi : 0.0);
+      t += MODE == 0 ? d * d : d;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+  return t;
+}
+
+__device__ __forceinline__ void lb_load(const double* __restrict__ up, const double* __restrict__ lo, int base, int L,
+                                        double (&u)[LB_BATCH], double (&l)[LB_BATCH]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int b = 0; b < LB_BATCH; ++b) {
+    const int k = base + b * 32 + lane;
+    u[b] = k < L ? __ldg(up + k) : 0.0;
+    l[b] = k < L ? __ldg(lo + k) : 0.0;
+  }
+}
+
+// Returns true when the candidate must still be evaluated.
+template <int MODE>
+__device__ __forceinline__ bool warp_lb_pass(const double* qs, const double* __restrict__ up,
+                                             const double* __restrict__ lo, int L, double thr,
+                                             const double (&u0)[LB_BATCH], const double (&l0)[LB_BATCH]) {
+  double total = lb_terms<MODE>(qs, 0, L, u0, l0);
+  if (total > thr) return false;
+  for (int base = 32 * LB_BATCH; base < L; base += 32 * LB_BATCH) {
+    double u[LB_BATCH], l[LB_BATCH];
+    lb_load(up, lo, base, L, u, l);
+    total += lb_terms<MODE>(qs, base, L, u, l);
+    if (total > thr) return false;
+  }
+  return true;
+}
+
+// lb > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header)
+__device__ __forceinline__ double lb_threshold(double cut) { return cut * (1.0 + 2.3283064365386963e-10); }
+
+}  // namespace ekb

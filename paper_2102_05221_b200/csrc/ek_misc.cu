@@ -135,4 +135,59 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const double* __restrict__ di
   }
 }
 
+// Sliding max/min over [k-w, k+w] (build_envelope, lower_bounds.py:23-57) for every
+// candidate, row-major (env[c * L + k]) so a warp reads 32 consecutive points.  One block per candidate: doubling max/min tables in shared
+// memory give max(x[s .. s+2w]) (clamped); windows cut by the left edge are scanned
+// directly; a window covering the whole series is the global max/min.
+__global__ void __launch_bounds__(256) k_envelope(const double* __restrict__ C, const long long* __restrict__ coff,
+                                                  int L, int ncand, int w, double* __restrict__ up,
+                                                  double* __restrict__ lo) {
+  extern __shared__ double sm[];
+  double* x = sm;
+  double* mx = sm + L;
+  double* mn = sm + 2 * L;
+  double* tmx = sm + 3 * L;
+  double* tmn = sm + 4 * L;
+  const int c = blockIdx.x;
+  const double* src = C + coff[c];
+  for (int k = threadIdx.x; k < L; k += blockDim.x) x[k] = mx[k] = mn[k] = src[k];
+  __syncthreads();
+  const long long want = 2LL * w + 1;
+  int span = 1;
+  while (span < want && span < L) {
+    const int step = (int)min((long long)span, want - span);
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+      const int k2 = min(k + step, L - 1);
+      tmx[k] = fmax(mx[k], mx[k2]);
+      tmn[k] = fmin(mn[k], mn[k2]);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+      mx[k] = tmx[k];
+      mn[k] = tmn[k];
+    }
+    __syncthreads();
+    span += step;
+  }
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    double u, l;
+    if (k >= w) {  // [k-w, min(k+w, L-1)] == table run starting at k-w
+      u = mx[k - w];
+      l = mn[k - w];
+    } else if ((long long)k + w >= L - 1) {  // the whole series
+      u = mx[0];
+      l = mn[0];
+    } else {  // [0, k+w], shorter than the table's runs
+      u = x[0];
+      l = x[0];
+      for (int j = 1; j <= k + w; ++j) {
+        u = fmax(u, x[j]);
+        l = fmin(l, x[j]);
+      }
+    }
+    up[(long long)c * L + k] = u;
+    lo[(long long)c * L + k] = l;
+  }
+}
+
 }  // namespace ekb

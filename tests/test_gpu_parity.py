@@ -215,3 +215,22 @@ def test_subseq_vs_oracle_random(gpu, rng):
         got = gpu.subsequence_search(q, ref, gpu.SearchConfig(spec=spec, normalize=norm))[:2]
         want = eko.subsequence(spec, "eapruned", q, ref, norm, chunk=256, threads=4)[:2]
         assert got == want, (lq, n, w, norm)
+
+
+@pytest.mark.parametrize("kind,window,mode", [("cdtw", 12, "squared"), ("dtw", None, "squared"),
+                                              ("cdtw", 7, "absolute")])
+def test_nn_lb_filter_scale(gpu, kind, window, mode):
+    """Dense dtw/cdtw 1-NN takes the LB_Keogh pre-filter path: results must not change."""
+    from paper_2102_05221_b200 import datagen
+
+    C, cl, protos = datagen.warped_prototypes(1024, 128, 8, 0.1, 77)
+    Q, ql, _ = datagen.warped_prototypes(48, 128, 8, 0.1, 78, protos=protos)
+    Q[5] = C[300]  # exact duplicate -> distance 0, lowest index must win
+    C[301] = C[300]
+    spec = gpu.DistanceSpec(kind=kind, window=window, cost_mode=mode)
+    idx, dist, cells, comp, ab = gpu.nn_batch(spec, "eapruned", Q, C)
+    r = eko.nn(spec, "eapruned", Q, C, threads=4)
+    assert np.array_equal(idx, r["nn_index"])
+    assert np.array_equal(dist, r["nn_distance"])
+    assert idx[5] == 300 and dist[5] == 0.0
+    assert np.all(comp + ab == len(C))
