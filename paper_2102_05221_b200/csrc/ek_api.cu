@@ -273,6 +273,7 @@ struct ParamHolder {
   Params prm{};
   int init(const ek_spec* sp, cudaStream_t st) {
     prm.gap = sp->erp_gap;
+    prm.zero = 0.0;
     prm.msm_c = sp->msm_c;
     prm.nu = sp->twe_nu;
     prm.lam = sp->twe_lambda;

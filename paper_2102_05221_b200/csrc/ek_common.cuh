@@ -16,6 +16,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 namespace ekb {
 
@@ -27,6 +28,7 @@ enum Mode : int { M_SQ = 0, M_ABS = 1 };
 
 struct Params {
   double gap, msm_c, nu, lam;
+  double zero;  // 0.0 supplied at run time (keeps band offsets as full 64-bit registers)
   // WDTW weight tables, host-computed with libm exp (kernels.py:80-92): the table for
   // longest length m (m+1 entries, indexed by |i-j|) starts at wt_all + wt_off[m].
   const double* wt_all;
@@ -109,7 +111,7 @@ EKB_DI DiagK<KIND> make_diag(int d, const Params& p, bool in_band = true) {
   DiagK<KIND> k;
   int ad = d < 0 ? -d : d;
   if constexpr (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW || KIND == K_ERP || KIND == K_MSM)
-    k.off = in_band ? 0.0 : EKB_INF;
+    k.off = in_band ? p.zero : EKB_INF;
   if constexpr (KIND == K_WDTW) k.w = (ad < p.wt_len) ? p.wt[ad] : 0.0;  // wt[|i-j|]
   if constexpr (KIND == K_TWE) {
     double dij = (double)ad;

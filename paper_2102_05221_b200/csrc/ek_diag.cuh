@@ -72,6 +72,17 @@ struct SmemSeries {
   __device__ __forceinline__ double at(int k) const { return p[k]; }
 };
 
+// Runs f(integral_constant<S>) for S = S0 .. U-1 until one returns true.
+template <int S0, int U, class F>
+__device__ __forceinline__ bool unrolled_steps(F& f) {
+  if constexpr (S0 == U) {
+    return false;
+  } else {
+    if (f(std::integral_constant<int, S0>{})) return true;
+    return unrolled_steps<S0 + 1, U>(f);
+  }
+}
+
 // X: lines accessor (nl >= nc), Y: cols accessor.  w: effective window
 // (w >= nl - nc, checked by the caller).
 template <int KIND, int MODE, int P, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
@@ -128,69 +139,104 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   const int Tf = nl + nc;
   int cut_hi = hi_word(cut);
   bool dead = false;
-  bool done = false;
-  while (!done) {
-    double nextcut = cut;
-    if constexpr (SHARED_CUT) nextcut = ld_cut(cutp);  // consumed after this block of double steps
-#pragma unroll 1
-    for (int u = 0; u < 16; ++u) {
-      bool alive = false;
-      // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
-      double tin = __shfl_up_sync(FULL, val[P - 1], 1);
-      if constexpr (BORDERED) {
-        if (lane == 0) tin = EKB_INF;
-      }
+
+  // One double step.  With ROT the register windows are rings whose rotation
+  // (rx for xw, ry for yw) is a compile-time function of the unrolled step S,
+  // so sliding costs no register moves; otherwise the windows shift in place.
+  constexpr bool ROT = (H <= 2);
+  constexpr int U = ROT ? H * (H + 1) : 1;
+  auto dstep = [&](auto S_) -> bool {
+    constexpr int S = decltype(S_)::value;
+    constexpr int rx = ROT ? S % (H + 1) : 0;
+    constexpr int ry = ROT ? (H - S % H) % H : 0;
+    auto XW = [&](int k) -> RowD<KIND>& { return xw[(k + rx) % (H + 1)]; };
+    auto YW = [&](int m) -> ColD<KIND>& { return yw[(m + ry) % H]; };
+    bool alive = false;
+    // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
+    double tin = __shfl_up_sync(FULL, val[P - 1], 1);
+    if constexpr (BORDERED) {
+      if (lane == 0) tin = EKB_INF;
+    }
 #pragma unroll
-      for (int m = 0; m < H; ++m) {
-        const int p = 2 * m;
-        const double T = (m == 0) ? tin : val[p - 1];
-        const double v = cell<KIND, MODE>(val[p], T, val[p + 1], xw[m], yw[m], kk[p], st[p], prm);
-        if constexpr (BORDERED) {
-          val[p] = (upd[p] || tb[p] == t) ? v : EKB_INF;
-        } else if constexpr (COST_MASK) {
-          val[p] = v;
-        } else {
-          val[p] = upd[p] ? v : EKB_INF;
-        }
-        alive |= hi_word(val[p]) <= cut_hi;
-      }
-      // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
-      double lin = __shfl_down_sync(FULL, val[0], 1);
+    for (int m = 0; m < H; ++m) {
+      const int p = 2 * m;
+      const double T = (m == 0) ? tin : val[p - 1];
+      const double v = cell<KIND, MODE>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm);
       if constexpr (BORDERED) {
-        if (lane == 31) lin = EKB_INF;
+        val[p] = (upd[p] || tb[p] == t) ? v : EKB_INF;
+      } else if constexpr (COST_MASK) {
+        val[p] = v;
+      } else {
+        val[p] = upd[p] ? v : EKB_INF;
       }
+      alive |= hi_word(val[p]) <= cut_hi;
+    }
+    // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
+    double lin = __shfl_down_sync(FULL, val[0], 1);
+    if constexpr (BORDERED) {
+      if (lane == 31) lin = EKB_INF;
+    }
 #pragma unroll
-      for (int m = 0; m < H; ++m) {
-        const int p = 2 * m + 1;
-        const double L = (p == P - 1) ? lin : val[p + 1];
-        const double v = cell<KIND, MODE>(val[p], val[p - 1], L, xw[m + 1], yw[m], kk[p], st[p], prm);
-        if constexpr (BORDERED) {
-          val[p] = (upd[p] || tb[p] == t + 1) ? v : EKB_INF;
-        } else if constexpr (COST_MASK) {
-          val[p] = v;
-        } else {
-          val[p] = upd[p] ? v : EKB_INF;
-        }
-        alive |= hi_word(val[p]) <= cut_hi;
+    for (int m = 0; m < H; ++m) {
+      const int p = 2 * m + 1;
+      const double L = (p == P - 1) ? lin : val[p + 1];
+      const double v = cell<KIND, MODE>(val[p], val[p - 1], L, XW(m + 1), YW(m), kk[p], st[p], prm);
+      if constexpr (BORDERED) {
+        val[p] = (upd[p] || tb[p] == t + 1) ? v : EKB_INF;
+      } else if constexpr (COST_MASK) {
+        val[p] = v;
+      } else {
+        val[p] = upd[p] ? v : EKB_INF;
       }
-      // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
-      // slot, which half step B (odd slots) leaves untouched
-      if (t + 1 >= Tf) { done = true; break; }
-      if (!__any_sync(FULL, alive)) { dead = true; done = true; break; }
-      // ---- slide the register windows by one element ----
-      t += 2;
-      ++I0;
-      ++J0;
+      alive |= hi_word(val[p]) <= cut_hi;
+    }
+    // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
+    // slot, which half step B (odd slots) leaves untouched
+    if (t + 1 >= Tf) return true;
+    if (!__any_sync(FULL, alive)) {
+      dead = true;
+      return true;
+    }
+    // ---- slide the register windows by one element ----
+    t += 2;
+    ++I0;
+    ++J0;
+    if constexpr (!ROT) {
       if (t >= t_load) {
         ld.ensure(t, dlo, dhi, H);
         t_load = ld.next_t(dlo, dhi, H);
       }
+    }
+    if constexpr (ROT) {
+      // logical xw[H] of the next step is ring slot rx; logical yw[0] is ring slot (ry+H-1)%H
+      const double xprev = XW(H).x;
+      const double yprev = YW(0).y;
+      xw[rx] = make_row<KIND, MODE>(X.at(I0 + H - 1), xprev, prm);
+      yw[(ry + H - 1) % H] = make_col<KIND, MODE>(Y.at(J0 - 1), yprev, prm);
+    } else {
 #pragma unroll
       for (int k = 0; k < H; ++k) xw[k] = xw[k + 1];
       xw[H] = make_row<KIND, MODE>(X.at(I0 + H - 1), xw[H - 1].x, prm);
 #pragma unroll
       for (int m = H - 1; m > 0; --m) yw[m] = yw[m - 1];
       yw[0] = make_col<KIND, MODE>(Y.at(J0 - 1), yw[0].y, prm);
+    }
+    return false;
+  };
+  constexpr int REP = (U >= 16) ? 1 : 16 / U;  // unrolled blocks between cutoff refreshes
+  bool finished = false;
+  while (!finished) {
+    double nextcut = cut;
+    if constexpr (SHARED_CUT) nextcut = ld_cut(cutp);  // consumed after this block of double steps
+#pragma unroll 1
+    for (int b = 0; b < REP && !finished; ++b) {
+      if constexpr (ROT) {  // stage series data for the whole unrolled block at once
+        if (t + 2 * U >= t_load) {
+          ld.ensure(t + 2 * U, dlo, dhi, H);
+          t_load = ld.next_t(dlo, dhi, H);
+        }
+      }
+      finished = unrolled_steps<0, U>(dstep);
     }
     if constexpr (SHARED_CUT) {
       cut = fmin(cut, nextcut);
