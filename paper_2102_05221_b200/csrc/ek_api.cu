@@ -484,23 +484,19 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
                           (const int*)dord.as<int>(), 0, ka, 1, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>(),
-                          (const int*)nullptr, (const double*)nullptr, (const double*)nullptr))
+                          (const float2*)nullptr))
       return -1;
   }
   mark(st, "nn_phaseA");
-  const double* env_up = nullptr;
-  const double* env_lo = nullptr;
+  const float2* env = nullptr;
   if (use_lb) {
     // envelopes of the candidates; phase B tests lb_keogh per pair before its DP
     const int L = max_len;
-    if (denv.alloc(sizeof(double) * 2 * (size_t)L * ncand, st)) return -1;
-    double* up = denv.as<double>();
-    double* lo = up + (size_t)L * ncand;
+    if (denv.alloc(sizeof(float2) * (size_t)L * ncand, st)) return -1;
     if (launch_plain(k_envelope, dim3((unsigned)ncand), dim3(256), sizeof(double) * 5 * (size_t)L, st, dC,
-                     (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, up, lo))
+                     (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>()))
       return -1;
-    env_up = up;
-    env_lo = lo;
+    env = denv.as<float2>();
     mark(st, "envelope");
   }
   // phase B in two segments: the next-best ranks (where the survivors concentrate)
@@ -515,7 +511,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(),
                           seg_lo[sgi], seg_hi[sgi], K, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
-                          dcnt.as<int>() + 2 + 2 * sgi, (const int*)nullptr, env_up, env_lo))
+                          dcnt.as<int>() + 2 + 2 * sgi, env))
       return -1;
   }
   mark(st, "nn_phaseB");

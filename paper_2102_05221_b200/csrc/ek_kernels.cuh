@@ -275,8 +275,7 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
                                             int K, int win, int lmax, Params prm, int share,
                                             unsigned long long* cutbits, double* __restrict__ out,
                                             int* __restrict__ tend_out, int* __restrict__ counter,
-                                            const int* __restrict__ counts, const double* __restrict__ env_up,
-                                            const double* __restrict__ env_lo) {
+                                            const float2* __restrict__ env) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
   constexpr int PF = kChunk / 32;
@@ -288,6 +287,8 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
   const int span = rank_hi - rank_lo;
   const int rounds = (span + K - 1) / K;
   const long long nitems = (long long)rounds * nq;
+  // LB_Keogh pre-test (dtw/cdtw, equal lengths): env != nullptr
+  const bool use_lb = env != nullptr;
   int staged_q = -1, cb_len = -1;
   for (;;) {
     long long it = 0;
@@ -297,55 +298,54 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
     const int q = (int)(it % nq);
     const int r = (int)(it / nq);
     const int lq = qlen[q];
-    const int hi_q = counts ? min(rank_hi, counts[q]) : rank_hi;  // LB survivors per query
-    const int k_lo = rank_lo + r * K, k_hi = min(k_lo + K, hi_q);
-    if (k_lo >= k_hi) continue;
+    const int k_lo = rank_lo + r * K, k_hi = min(k_lo + K, rank_hi);
+    const int cnt = k_hi - k_lo;
+    // this item's candidates and their metadata, one per lane (K <= 32)
+    const int ord = lane < cnt ? order[(long long)q * ncand + k_lo + lane] : 0;
+    const int olen = clen[ord];
+    const long long ooff = coff[ord];
     if (q != staged_q) {
       __syncwarp();
       stage_series<KIND>(QB, Q + qoff[q], lq, PAD);
       staged_q = q;
     }
-    // this item's candidates, one per lane (K <= 32), and the first one's chunk
-    const int ord = (k_lo + lane < k_hi) ? order[(long long)q * ncand + k_lo + lane] : 0;
-    int c_next = __shfl_sync(FULL, ord, 0);
-    // LB_Keogh pre-test (dtw/cdtw, equal lengths; env_up != nullptr): prefetch the next
-    // candidate's first envelope chunk; otherwise its first data chunk
-    const bool use_lb = env_up != nullptr;
+    double cut = ld_cut(cutbits + q);
+    // prefetch: LB path keeps the first envelope batch of pairs i+1 and i+2 in two
+    // register sets (envA for even i, envB for odd i); otherwise the next pair's
+    // first data chunk
+    float2 envA[LB_BATCH], envB[LB_BATCH];
     double pf[PF];
-    double eu[LB_BATCH], el[LB_BATCH];
     if (use_lb) {
-      lb_load(env_up + (long long)c_next * lmax, env_lo + (long long)c_next * lmax, 0, lmax, eu, el);
+      lb_load(env + (long long)__shfl_sync(FULL, ord, 0) * lmax, 0, __shfl_sync(FULL, olen, 0), envA);
+      if (cnt > 1) lb_load(env + (long long)__shfl_sync(FULL, ord, 1) * lmax, 0, __shfl_sync(FULL, olen, 1), envB);
     } else {
-      const double* s = C + coff[c_next];
-      const int lc = clen[c_next];
+      const double* s = C + __shfl_sync(FULL, ooff, 0);
+      const int lc = __shfl_sync(FULL, olen, 0);
 #pragma unroll
       for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < lc) ? __ldg(s + u * 32 + lane) : 0.0;
     }
-    double cut = ld_cut(cutbits + q);
-    double pending = cut;  // cutoff refresh issued at the end of the previous pair
-    for (int k = k_lo; k < k_hi; ++k) {
-      cut = fmin(cut, pending);
-      const int c = c_next;
-      const int lc = clen[c];
-      const double* csrc = C + coff[c];
+    __syncwarp();
+    for (int i = 0; i < cnt; ++i) {
+      const int c = __shfl_sync(FULL, ord, i);
+      const int lc = __shfl_sync(FULL, olen, i);
+      const double* csrc = C + __shfl_sync(FULL, ooff, i);
       // orientation (kernels.py:168-171): query is s, candidate is t
       const bool q_rows = lq >= lc;
       const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
       const int w = win < 0 ? nl : win;
       bool evaluate = w >= nl - nc;
       if (use_lb) {
-        double eu0[LB_BATCH], el0[LB_BATCH];
-#pragma unroll
-        for (int b = 0; b < LB_BATCH; ++b) {
-          eu0[b] = eu[b];
-          el0[b] = el[b];
-        }
-        if (k + 1 < k_hi) {  // prefetch the next candidate's first envelope batch
-          c_next = __shfl_sync(FULL, ord, k + 1 - k_lo);
-          lb_load(env_up + (long long)c_next * lmax, env_lo + (long long)c_next * lmax, 0, lmax, eu, el);
-        }
-        evaluate = evaluate && warp_lb_pass<MODE>(QB, env_up + (long long)c * lmax, env_lo + (long long)c * lmax,
-                                                  lc, lb_threshold(cut), eu0, el0);
+        const int i2 = min(i + 2, cnt - 1);
+        const int c2 = __shfl_sync(FULL, ord, i2), l2 = __shfl_sync(FULL, olen, i2);
+        // first batch from the prefetched set, which is then refilled for pair i+2
+        auto first = [&](float2 (&e)[LB_BATCH]) {
+          const double t = lb_terms<MODE>(QB, 0, lc, e);
+          if (i + 2 < cnt) lb_load(env + (long long)c2 * lmax, 0, l2, e);
+          return t;
+        };
+        const double t0 = (i & 1) ? first(envB) : first(envA);
+        const double thr = lb_threshold(cut);
+        evaluate = evaluate && !(t0 > thr) && warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, thr, t0);
         if (evaluate) {  // survivor: stage its first chunk now
           __syncwarp();
 #pragma unroll
@@ -366,10 +366,9 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
           stage_pads<KIND>(CB, lc, PAD, first);
           cb_len = lc;
         }
-        if (k + 1 < k_hi) {  // prefetch the next candidate's first chunk
-          c_next = __shfl_sync(FULL, ord, k + 1 - k_lo);
-          const double* s = C + coff[c_next];
-          const int ln = clen[c_next];
+        if (i + 1 < cnt) {  // prefetch the next candidate's first chunk
+          const double* s = C + __shfl_sync(FULL, ooff, i + 1);
+          const int ln = __shfl_sync(FULL, olen, i + 1);
 #pragma unroll
           for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < ln) ? __ldg(s + u * 32 + lane) : 0.0;
         }
@@ -392,14 +391,13 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
           // values are >= 0 (or +inf), so IEEE bits order as unsigned integers
           atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
         }
-        if (share) cut = fmin(cut, cost);
+        if (share) cut = fmin(cut, fmin(cost, ld_cut(cutbits + q)));
       }
       const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) : 0;
       if (lane == 0) {
         out[(long long)q * ncand + c] = cost;
         tend_out[(long long)q * ncand + c] = cells;
       }
-      if (share) pending = ld_cut(cutbits + q);
     }
   }
 }

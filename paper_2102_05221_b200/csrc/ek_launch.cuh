@@ -10,7 +10,7 @@ using TriFn = void (*)(const double*, const long long*, const int*, int, int, in
                       unsigned long long*, int*);
 using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, int, int, int, int, Params, int, unsigned long long*,
-                      double*, int*, int*, const int*, const double*, const double*);
+                      double*, int*, int*, const float2*);
 using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, Params, unsigned long long*);
 

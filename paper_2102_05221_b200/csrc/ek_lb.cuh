@@ -8,10 +8,11 @@
 //
 // Soundness in floating point: every alignment path in the band matches each
 // query point i with some candidate point j, |i-j| <= w, so its cost is at
-// least sum_i dist(q_i, [L_i, U_i]).  The computed bound carries at most ~4n
-// ulps of relative error and the DP value at most ~2n ulps (n <= 2^13 terms of
-// non-negative sums), so a candidate is skipped only when
-// lb > cutoff * (1 + 2^-32), far above both error bounds.
+// least sum_i dist(q_i, [L_i, U_i]).  Envelopes are stored as floats rounded
+// outward (upper up, lower down), which only widens them.  The computed bound
+// carries at most ~4n ulps of relative error and the DP value at most ~2n ulps
+// (n <= 2^13 terms of non-negative sums), so a candidate is skipped only when
+// the bound exceeds cutoff * (1 + 2^-32), far above both error bounds.
 // (k_envelope, which builds the envelopes, lives in ek_misc.cu.)
 #pragma once
 #include "ek_common.cuh"
@@ -22,56 +23,51 @@ namespace ekb {
 // Warp-cooperative lb_keogh(q, env(c)) test with early exit.  Points are taken in
 // batches of LB_BATCH x 32 (lane = point within a 32-point chunk); the first batch
 // arrives prefetched, later batches are loaded together so their latency overlaps.
-// The test fails as soon as the running total exceeds thr.
 constexpr int LB_BATCH = 4;
 
 template <int MODE>
-__device__ __forceinline__ double lb_terms(const double* qs, int base, int L, const double (&u)[LB_BATCH],
-                                           const double (&l)[LB_BATCH]) {
+__device__ __forceinline__ double lb_terms(const double* qs, int base, int L, const float2 (&e)[LB_BATCH]) {
   const int lane = threadIdx.x & 31;
   double t = 0.0;
 #pragma unroll
   for (int b = 0; b < LB_BATCH; ++b) {
     const int k = base + b * 32 + lane;
-    if (k < L) {
-      const double qi = qs[k];
-      const double d = qi > u[b] ? qi - u[b] : (qi < l[b] ? l[b] - qi : 0.0);
-      t += MODE == 0 ? d * d : d;
-    }
+    const double qi = k < L ? qs[k] : 0.0;
+    // distance to [lower, upper] (upper >= lower), branch-free
+    double d = fmax(qi - (double)e[b].x, (double)e[b].y - qi);
+    d = fmax(d, 0.0);
+    t += MODE == 0 ? d * d : d;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
   return t;
 }
 
-__device__ __forceinline__ void lb_load(const double* __restrict__ up, const double* __restrict__ lo, int base, int L,
-                                        double (&u)[LB_BATCH], double (&l)[LB_BATCH]) {
+// out-of-range points load the neutral interval [-inf, +inf]
+__device__ __forceinline__ void lb_load(const float2* __restrict__ env, int base, int L, float2 (&e)[LB_BATCH]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int b = 0; b < LB_BATCH; ++b) {
     const int k = base + b * 32 + lane;
-    u[b] = k < L ? __ldg(up + k) : 0.0;
-    l[b] = k < L ? __ldg(lo + k) : 0.0;
+    e[b] = k < L ? __ldg(env + k) : make_float2(__int_as_float(0x7f800000), __int_as_float(0xff800000));
   }
 }
 
+// Continues the test past the prefetched first batch (running total `total`).
 // Returns true when the candidate must still be evaluated.
 template <int MODE>
-__device__ __forceinline__ bool warp_lb_pass(const double* qs, const double* __restrict__ up,
-                                             const double* __restrict__ lo, int L, double thr,
-                                             const double (&u0)[LB_BATCH], const double (&l0)[LB_BATCH]) {
-  double total = lb_terms<MODE>(qs, 0, L, u0, l0);
-  if (total > thr) return false;
+__device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __restrict__ env, int L, double thr,
+                                             double total) {
   for (int base = 32 * LB_BATCH; base < L; base += 32 * LB_BATCH) {
-    double u[LB_BATCH], l[LB_BATCH];
-    lb_load(up, lo, base, L, u, l);
-    total += lb_terms<MODE>(qs, base, L, u, l);
+    float2 e[LB_BATCH];
+    lb_load(env, base, L, e);
+    total += lb_terms<MODE>(qs, base, L, e);
     if (total > thr) return false;
   }
   return true;
 }
 
-// lb > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header)
+// bound > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header)
 __device__ __forceinline__ double lb_threshold(double cut) { return cut * (1.0 + 2.3283064365386963e-10); }
 
 }  // namespace ekb

@@ -136,12 +136,12 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const double* __restrict__ di
 }
 
 // Sliding max/min over [k-w, k+w] (build_envelope, lower_bounds.py:23-57) for every
-// candidate, row-major (env[c * L + k]) so a warp reads 32 consecutive points.  One block per candidate: doubling max/min tables in shared
+// candidate, row-major (env[c * L + k] = (upper, lower)) so a warp reads 32
+// consecutive points; stored as floats rounded outward (upper up, lower down).  One block per candidate: doubling max/min tables in shared
 // memory give max(x[s .. s+2w]) (clamped); windows cut by the left edge are scanned
 // directly; a window covering the whole series is the global max/min.
 __global__ void __launch_bounds__(256) k_envelope(const double* __restrict__ C, const long long* __restrict__ coff,
-                                                  int L, int ncand, int w, double* __restrict__ up,
-                                                  double* __restrict__ lo) {
+                                                  int L, int ncand, int w, float2* __restrict__ env) {
   extern __shared__ double sm[];
   double* x = sm;
   double* mx = sm + L;
@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(256) k_envelope(const double* __restrict__ C, 
         l = fmin(l, x[j]);
       }
     }
-    up[(long long)c * L + k] = u;
-    lo[(long long)c * L + k] = l;
+    // float with outward rounding: a wider envelope keeps lb_keogh a lower bound
+    env[(long long)c * L + k] = make_float2(__double2float_ru(u), __double2float_rd(l));
   }
 }
 

@@ -4,7 +4,7 @@
 
 namespace ekb {
 
-__global__ void k_envelope(const double* C, const long long* coff, int L, int ncand, int w, double* up, double* lo);
+__global__ void k_envelope(const double* C, const long long* coff, int L, int ncand, int w, float2* env);
 
 __global__ void k_rank_dist(const double* Q, const long long* qoff, const int* qlen, int nq, const double* C,
                             const long long* coff, const int* clen, int ncand, float* out);
