@@ -111,18 +111,19 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
 
 // Band cells an engine evaluated before it stopped at t_end (warp-parallel; every
 // lane returns the total): the diagonal engine evaluates each band cell with
-// i + j <= t_end, the stripe engine row i of lane l while l <= r0 + t_end - 1 - i.
+// i + j <= t_end; the stripe engine (two rows per step) evaluates row i of lane l
+// while r0 + 2(t_end-1-l) + 1 >= i.
 template <int ENG>
 __device__ __forceinline__ int warp_cells(int nl, int nc, int w, int tend, int r0) {
   const int lane = threadIdx.x & 31;
   constexpr bool DIAG = engine_is_diag(ENG);
   constexpr int S = engine_S(ENG);
-  const int imax = DIAG ? min(nl, tend - 1) : min(nl, r0 + tend - 1);
+  const int imax = DIAG ? min(nl, tend - 1) : min(nl, r0 + 2 * tend - 1);
   int c = 0;
   for (int i = 1 + lane; i <= imax; i += 32) {
     const int jlo = max(1, i - w);
     int jhi = min(nc, i + w);
-    jhi = DIAG ? min(jhi, tend - i) : min(jhi, (r0 + tend - i) * S);
+    jhi = DIAG ? min(jhi, tend - i) : min(jhi, ((r0 + 2 * tend - 1 - i) / 2 + 1) * S);
     c += max(0, jhi - jlo + 1);
   }
 #pragma unroll

@@ -69,54 +69,36 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
     if (lane != 0) dgpc = pcost<MODE>(cx(r0 - 2), ycol0);
   }
 
-  const int nsteps = nl - r0 + lf + 1;  // the last lane that matters finishes row nl
-  bool alive2 = false;                  // alive over the previous step
-  bool ea_flag = false;                 // EA: some row minimum exceeded the cutoff
+  // Two rows per step: lane l evaluates rows i0 = r0 + 2(t-l) and i1 = i0 + 1.  Row i1
+  // trails row i0 by one column inside the lane, so the two dependency chains
+  // interleave (the compiler schedules the fully unrolled straight-line code).
+  const int nsteps = lf + (nl - r0) / 2 + 1;  // lane lf reaches row nl in its last step
+  const bool last_is_i0 = ((nl - r0) & 1) == 0;
+  bool alive2 = false;   // alive over the previous step
+  bool ea_flag = false;  // EA: some row minimum exceeded the cutoff
   double nextcut = cut;
+  int cut_hi = hi_word(cut);
   int t = 0;
   bool dead = false;
-  double lastv = EKB_INF;  // value of the lane's last column for the current row
-  double lastpc = 0.0;
-  double rowmin_out = EKB_INF;
-  for (t = 0; t < nsteps; ++t) {
-    if constexpr (SHARED_CUT) {
-      if ((t & 31) == 0) nextcut = ld_cut(cutp);
-      if ((t & 31) == 24) cut = fmin(cut, nextcut);
-    }
-    const int i = r0 + t - lane;  // this lane's row
-    // receive the left neighbour's last column for row i (computed at step t-1)
-    double lb = __shfl_up_sync(FULL, lastv, 1);
-    double lbpc = TWE ? __shfl_up_sync(FULL, lastpc, 1) : 0.0;
-    double rmin = EA ? __shfl_up_sync(FULL, rowmin_out, 1) : EKB_INF;
-    const double x = cx(i - 1);
-    const RowD<KIND> rd = make_row<KIND, MODE>(x, xprev, prm);
-    xprev = x;
-    if (lane == 0) {
-      // border cell (i, 0)
-      if constexpr (BORDERED) {
-        if (i == 0) vb = 0.0;
-        else vb = dadd(vb, rd.ar);  // vb[i] = vb[i-1] + pc(l_i, g)
-        lb = (i <= w + 1) ? vb : EKB_INF;
-      } else {
-        lb = (i == 0) ? 0.0 : EKB_INF;
-      }
-      if constexpr (TWE) lbpc = pcost<MODE>(x, 0.0);  // pc(l_i, c_0 := 0) of the border cell
-      rmin = (i >= 1) ? lb : EKB_INF;                 // ea: the border cell joins the row minimum
-    }
-    const bool row_ok = (i >= r0) && (i <= nl);
-    bool alive = row_ok && lane == 0 && (lb <= cut);
-    // band of row i within this stripe: slots [a, b]
+  double last0 = EKB_INF, last1 = EKB_INF;  // this lane's last column for rows i0 / i1
+  double lastpc0 = 0.0, lastpc1 = 0.0;
+  double rmo0 = EKB_INF, rmo1 = EKB_INF;
+  double fin = EKB_INF;  // final cell when row nl is an i0 row
+  const int sf = (nc - 1) % S;
+
+  // one row over this lane's S columns; prev[] holds row i-1 on entry, row i on exit
+  auto row_pass = [&](int i, const RowD<KIND>& rd, double lft, double dgl, double dpc, double& rmin,
+                      double (&row)[S], bool& alive) {
     int a = 0, b = S - 1;
     if constexpr (BANDED) {
       const int hi = (i == 0) ? w + 1 : i + w;  // row 0 keeps hborder up to j = w+1
       a = i - w - jbase - 1;
       b = hi - jbase - 1;
     }
-    double dgl = dg, lft = lb, dpc = dgpc;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int j = jbase + 1 + s;
-      const double up = val[s];
+      const double up = row[s];
       DiagK<KIND> k{};  // off = 0.0: the stripe engine masks the band itself
       if constexpr (KIND == K_WDTW) k.w = tab[min(abs(i - j), tablen - 1)];
       if constexpr (TWE) k.tw = tab[min(abs(i - j), tablen - 1)];
@@ -132,19 +114,82 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
         pcr[s] = stt.pcp;  // pc(l_i, c_j) for the next row
         dpc = upc;
       }
-      val[s] = v;
+      row[s] = v;
       dgl = up;
       lft = v;
-      alive |= row_ok && (j <= nc) && (v <= cut);
+      // garbage cells (before the first row, past the last row or column) are +inf
+      // or only delay abandoning; the hi-word test is conservative (ek_diag.cuh)
+      alive |= hi_word(v) <= cut_hi;
       if constexpr (EA) rmin = (v < rmin) ? v : rmin;
     }
-    dg = lb;
-    dgpc = lbpc;
-    lastv = val[S - 1];
-    if constexpr (TWE) lastpc = pcr[S - 1];
+  };
+
+  for (t = 0; t < nsteps; ++t) {
+    if constexpr (SHARED_CUT) {
+      if ((t & 15) == 0) nextcut = ld_cut(cutp);
+      if ((t & 15) == 12) {
+        cut = fmin(cut, nextcut);
+        cut_hi = hi_word(cut);
+      }
+    }
+    const int i0 = r0 + 2 * (t - lane), i1 = i0 + 1;
+    // the left neighbour's last column for rows i0, i1 (computed at step t-1)
+    double lb0 = __shfl_up_sync(FULL, last0, 1);
+    double lb1 = __shfl_up_sync(FULL, last1, 1);
+    double lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1) : 0.0;
+    double lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1) : 0.0;
+    double rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1) : EKB_INF;
+    double rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1) : EKB_INF;
+    const double x0 = cx(i0 - 1), x1 = cx(i1 - 1);
+    const RowD<KIND> rd0 = make_row<KIND, MODE>(x0, xprev, prm);
+    const RowD<KIND> rd1 = make_row<KIND, MODE>(x1, x0, prm);
+    xprev = x1;
+    if (lane == 0) {
+      // border cells (i0, 0), (i1, 0)
+      if constexpr (BORDERED) {
+        vb = (i0 == 0) ? 0.0 : dadd(vb, rd0.ar);  // vb[i] = vb[i-1] + pc(l_i, g)
+        lb0 = (i0 <= w + 1) ? vb : EKB_INF;
+        vb = dadd(vb, rd1.ar);
+        lb1 = (i1 <= w + 1) ? vb : EKB_INF;
+      } else {
+        lb0 = (i0 == 0) ? 0.0 : EKB_INF;
+        lb1 = EKB_INF;
+      }
+      if constexpr (TWE) {
+        lbpc0 = pcost<MODE>(x0, 0.0);  // pc(l_i, c_0 := 0) of the border cell
+        lbpc1 = pcost<MODE>(x1, 0.0);
+      }
+      rm0 = (i0 >= 1) ? lb0 : EKB_INF;  // ea: the border cell joins the row minimum
+      rm1 = (i1 >= 1) ? lb1 : EKB_INF;
+    }
+    bool alive = lane == 0 && (hi_word(lb0) <= cut_hi || hi_word(lb1) <= cut_hi);
+    double row0[S];
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) row0[s2] = val[s2];
+    // row i0: diagonal input (i0-1, jbase) is the left neighbour's row i1 of step t-1
+    row_pass(i0, rd0, lb0, dg, dgpc, rm0, row0, alive);
+    if constexpr (TWE) lastpc0 = pcr[S - 1];
+    if (t == nsteps - 1 && last_is_i0) {
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2)
+        if (s2 == sf) fin = row0[s2];
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) val[s2] = row0[s2];
+    // row i1: diagonal input (i0, jbase) = lb0
+    row_pass(i1, rd1, lb1, lb0, lbpc0, rm1, val, alive);
+    if constexpr (TWE) lastpc1 = pcr[S - 1];
+    dg = lb1;
+    dgpc = lbpc1;
+    last0 = row0[S - 1];
+    last1 = val[S - 1];
     if constexpr (EA) {
-      rowmin_out = rmin;
-      if (lane == lf && row_ok && i >= 1 && rmin > cut) ea_flag = true;
+      rmo0 = rm0;
+      rmo1 = rm1;
+      if (lane == lf) {
+        if (i0 >= 1 && i0 <= nl && rm0 > cut) ea_flag = true;
+        if (i1 >= 1 && i1 <= nl && rm1 > cut) ea_flag = true;
+      }
     }
     if constexpr (!EA) {
       if (t & 1) {
@@ -152,7 +197,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
       }
       alive2 = alive;
     } else {
-      if ((t & 31) == 31 && __any_sync(FULL, ea_flag)) { dead = true; break; }
+      if ((t & 15) == 15 && __any_sync(FULL, ea_flag)) { dead = true; break; }
     }
   }
   (void)lane_on;
@@ -163,11 +208,11 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
     return res;
   }
   // cell (nl, nc) lives in lane lf, slot (nc-1) % S, computed at its last step
-  const int sf = (nc - 1) % S;
   double r = val[0];
 #pragma unroll
   for (int s = 1; s < S; ++s)
     if (s == sf) r = val[s];
+  if (last_is_i0) r = fin;
   r = __shfl_sync(FULL, r, lf);
   if constexpr (EA) {
     const bool flagged = __any_sync(FULL, ea_flag);
