@@ -712,7 +712,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     const long long ns = (long long)seeds.size();
     if (dseed.alloc(8 * ns, st) || dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
     CK(cudaMemcpyAsync(dseed.p, seeds.data(), 8 * ns, cudaMemcpyHostToDevice, st));
-    if (launch_persistent(fn, 32 * wpb, smem, st, ns, dq, (int)lq, dref, (long long)nref, (int)normalize,
+    if (launch_persistent(fn, 32 * wpb, smem, st, ns * 32, dq, (int)lq, dref, (long long)nref, (int)normalize,
                           (const long long*)dseed.as<long long>(), ns, win, plan, (int)share,
                           dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
       return -1;
