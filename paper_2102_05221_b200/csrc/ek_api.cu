@@ -704,22 +704,32 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   }
   CK(cudaMemcpyAsync(dcut.p, &cut0, 8, cudaMemcpyHostToDevice, st));
   mark(st, "seed_bounds");
+  // z-normalisation statistics of every window (thread per window)
+  DBuf dstats;
+  if (normalize) {
+    if (dstats.alloc(sizeof(double2) * (size_t)nwin, st)) return -1;
+    if (launch_plain(k_win_stats<0>, dim3((unsigned)((nwin + 255) / 256)), dim3(256), 0, st, dref, nwin, (int)lq, plan,
+                     dstats.as<double2>()))
+      return -1;
+  }
+  const double2* wst = normalize ? (const double2*)dstats.as<double2>() : nullptr;
+  mark(st, "win_stats");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
   const int wpb = 8;
-  const size_t smem = sizeof(double) * ((size_t)subseq_head((int)lq, nl_, eng) + wpb * (size_t)subseq_warp((int)lq, nl_));
+  const size_t smem = sizeof(double) * ((size_t)subseq_head((int)lq, nl_, eng) + wpb * (size_t)subseq_warp((int)lq, eng));
   if (!seeds.empty()) {
     DBuf dseed, dso, dst;
     const long long ns = (long long)seeds.size();
     if (dseed.alloc(8 * ns, st) || dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
     CK(cudaMemcpyAsync(dseed.p, seeds.data(), 8 * ns, cudaMemcpyHostToDevice, st));
-    if (launch_persistent(fn, 32 * wpb, smem, st, ns * 32, dq, (int)lq, dref, (long long)nref, (int)normalize,
+    if (launch_persistent(fn, 32 * wpb, smem, st, ns, dq, (int)lq, dref, (int)normalize, wst,
                           (const long long*)dseed.as<long long>(), ns, win, plan, (int)share,
                           dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
       return -1;
     CK(cudaStreamSynchronize(st));
   }
   mark(st, "subseq_phaseA");
-  if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, dq, (int)lq, dref, (long long)nref, (int)normalize,
+  if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, dq, (int)lq, dref, (int)normalize, wst,
                         (const long long*)nullptr, nwin, win, plan, (int)share, dcut.as<unsigned long long>(),
                         dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
     return -1;
