@@ -100,6 +100,13 @@ int ek_subseq_dev(const ek_spec* spec, int32_t variant, const double* d_query, i
                   const double* d_reference, int64_t n_ref, int32_t normalize, int64_t* best_off,
                   double* best_dist, int64_t* cells, int64_t* computed, int64_t* abandoned, void* stream);
 
+/* Distance profile: window_dist[o] = distance(spec, "base", query, window_o) for every
+ * stride-1 offset o (n_ref - lq + 1 values), each window z-normalised when normalize != 0.
+ * The per-offset loop of subsequence_search (search.py:189-213) without the running
+ * cutoff; the reference obtains the same numbers by calling engines.distance per window. */
+int ek_subseq_profile(const ek_spec* spec, const double* query, int64_t lq, const double* reference, int64_t n_ref,
+                      int32_t normalize, double* window_dist);
+
 /* Number of kernel launches the library issued since the last reset (bench accounting). */
 int64_t ek_launch_count(int32_t reset);
 

@@ -254,3 +254,24 @@ def subsequence(spec, variant, query, reference, normalize, chunk=None, threads=
         if o >= 0 and (d < best_d or (d == best_d and o < best_off)):
             best_off, best_d = o, d
     return best_off, best_d, int(cells.sum())
+
+
+def subsequence_profile(spec, query, reference, normalize, threads=None):
+    """Per-offset distance(spec, "base", query, window) of every window (the
+    search.py:189-213 loop with no running cutoff) -> float64 array."""
+    q = _f64(query)
+    ref = _f64(reference)
+    if normalize:
+        q = znormalize(q)
+    nwin = len(ref) - len(q) + 1
+    if nwin < 1:
+        raise ValueError("query longer than reference")
+    h = _SpecHolder(spec, "base", [len(q)])
+    bo = np.empty(nwin, dtype=np.int64)
+    bd = np.empty(nwin, dtype=np.float64)
+    cells = np.empty(nwin, dtype=np.int64)
+    rc = lib().eko_subseq(C.byref(h.s), _d(q), len(q), _d(ref), len(ref), int(bool(normalize)), 1,
+                          int(threads or default_threads()), _i(bo), _d(bd), _i(cells))
+    if rc:
+        raise RuntimeError(f"eko_subseq failed ({rc})")
+    return bd

@@ -651,7 +651,7 @@ int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int6
 
 static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* dq, int64_t lq, const double* dref,
                            int64_t nref, int32_t normalize, int64_t* best_off, double* best_dist, int64_t* cells,
-                           int64_t* computed, int64_t* abandoned, cudaStream_t st) {
+                           int64_t* computed, int64_t* abandoned, cudaStream_t st, double* profile = nullptr) {
   if (check_spec(spec)) return -1;
   if (spec->kind != K_DTW && spec->kind != K_CDTW) return fail("subsequence search supports dtw and cdtw only");
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
@@ -660,7 +660,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
   const int eng = choose_engine((int)lq, (int)lq, win < 0 ? (int)lq : win, false);
   if (eng < 0) return fail("query length %lld exceeds this build's engines", (long long)lq);
-  const bool share = variant == 1 || variant == 2;
+  const bool share = !profile && (variant == 1 || variant == 2);
   // numpy pairwise-sum plan for length lq
   std::vector<int2> leaves;
   std::vector<int> ops;
@@ -734,6 +734,9 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                         dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
     return -1;
   mark(st, "subseq_phaseB");
+  if (profile) {
+    CK(cudaMemcpyAsync(profile, dout.p, sizeof(double) * (size_t)nwin, cudaMemcpyDeviceToHost, st));
+  }
   // reduce
   const int nb = (int)std::min<long long>(1024, (nwin + 255) / 256);
   DBuf pd, pi, pc, pa, pcl;
@@ -794,6 +797,23 @@ int ek_subseq(const ek_spec* spec, int32_t variant, const double* query, int64_t
   CK(cudaMemcpyAsync(dr.p, reference, sizeof(double) * n_ref, cudaMemcpyHostToDevice, st));
   return subseq_dev_impl(spec, variant, dq.as<double>(), lq, dr.as<double>(), n_ref, normalize, best_off, best_dist,
                          cells, computed, abandoned, st);
+}
+
+int ek_subseq_profile(const ek_spec* spec, const double* query, int64_t lq, const double* reference, int64_t n_ref,
+                      int32_t normalize, double* window_dist) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  cudaStream_t st = g_ctx.stream;
+  if (lq < 1 || lq > n_ref) return fail("query length %lld exceeds reference length %lld", (long long)lq, (long long)n_ref);
+  if (!window_dist) return fail("window_dist must not be null");
+  DBuf dq, dr;
+  if (dq.alloc(sizeof(double) * lq, st) || dr.alloc(sizeof(double) * n_ref, st)) return -1;
+  CK(cudaMemcpyAsync(dq.p, query, sizeof(double) * lq, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dr.p, reference, sizeof(double) * n_ref, cudaMemcpyHostToDevice, st));
+  int64_t bo, c, cp, ab;
+  double bd;
+  return subseq_dev_impl(spec, 0, dq.as<double>(), lq, dr.as<double>(), n_ref, normalize, &bo, &bd, &c, &cp, &ab, st,
+                         window_dist);
 }
 
 }  // extern "C"

@@ -176,6 +176,30 @@ def subsequence_search(query, reference, cfg: SearchConfig):
     return int(off[0]), float(dist[0]), stats
 
 
+def subsequence_profile(query, reference, spec: DistanceSpec, normalize: bool = False, backend=None):
+    """Distance of ``query`` to every stride-1 window of ``reference`` (variant "base").
+
+    Entry ``o`` equals ``distance(spec, "base", query, reference[o:o+lq])`` with both
+    sides z-normalised when ``normalize`` -- the per-offset values subsequence_search
+    (search.py:189-213) compares, without its running cutoff.
+    """
+    if spec.kind not in ("dtw", "cdtw"):
+        raise SpecError("subsequence search supports dtw and cdtw only")
+    query = as_series(query)
+    reference = as_series(reference)
+    lq = len(query)
+    if lq > len(reference):
+        raise DimensionError(f"query length {lq} exceeds reference length {len(reference)}")
+    if normalize and lq < 2:
+        raise DegenerateInputError("z-normalization needs at least 2 points")
+    _backend.resolve(backend)
+    h = _lib.SpecHandle(spec)
+    out = np.empty(len(reference) - lq + 1, dtype=np.float64)
+    _lib.check(_lib.lib().ek_subseq_profile(h.ref, _lib.dptr(query), lq, _lib.dptr(reference), len(reference),
+                                            int(bool(normalize)), _lib.dptr(out)))
+    return out
+
+
 def pairwise(spec: DistanceSpec, X, variant: str = "pruned_only", backend=None):
     """Full symmetric matrix of ``distance(spec, variant, X[i], X[j])``, diagonal 0.0.
 

@@ -217,6 +217,24 @@ def test_subseq_vs_oracle_random(gpu, rng):
         assert got == want, (lq, n, w, norm)
 
 
+@pytest.mark.parametrize("lq,w,norm,mode", [(1, 0, False, "squared"), (7, 2, True, "squared"),
+                                            (129, 9, True, "squared"), (300, 31, True, "absolute"),
+                                            (64, None, True, "squared"), (200, 40, False, "absolute")])
+def test_subseq_profile_every_window(gpu, rng, lq, w, norm, mode):
+    """Every window's distance (not just the best) matches the oracle bit for bit;
+    the stream holds flat runs (all-zeros z-normalised windows) and spikes."""
+    ref = np.cumsum(rng.normal(0, 1, 3000))
+    ref[500:900] = 4.25          # flat run: std < 1e-12 windows
+    ref[1500:1520] *= 1e6        # large dynamic range
+    ref[2000:2300] = rng.normal(0, 1e-7, 300)
+    q = np.cumsum(rng.normal(0, 1, lq))
+    spec = gpu.DistanceSpec(kind="dtw" if w is None else "cdtw", window=w, cost_mode=mode)
+    got = gpu.subsequence_profile(q, ref, spec, normalize=norm)
+    want = eko.subsequence_profile(spec, q, ref, norm, threads=4)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want), int(np.flatnonzero(got != want)[0])
+
+
 @pytest.mark.parametrize("kind,window,mode", [("cdtw", 12, "squared"), ("dtw", None, "squared"),
                                               ("cdtw", 7, "absolute")])
 def test_nn_lb_filter_scale(gpu, kind, window, mode):
