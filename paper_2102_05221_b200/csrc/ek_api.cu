@@ -131,6 +131,15 @@ struct DBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// launch errors name the kernel (asynchronous faults surface at a later call)
+int launch_check(const void* fn) {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return 0;
+  const char* name = nullptr;
+  if (cudaFuncGetName(&name, fn) != cudaSuccess || !name) name = "?";
+  return fail("launch of %s failed: %s", name, cudaGetErrorString(e));
+}
+
 template <class Fn, class... Args>
 int launch_persistent(Fn fn, int block, size_t smem, cudaStream_t st, long long warp_units, Args... args) {
   if (!fn) return fail("no kernel instantiated for this configuration");
@@ -143,8 +152,7 @@ int launch_persistent(Fn fn, int block, size_t smem, cudaStream_t st, long long 
   long long grid = std::min<long long>((long long)g_ctx.nsm * per_sm, std::max<long long>(1, want));
   fn<<<(unsigned)grid, block, smem, st>>>(args...);
   ++g_launches;
-  CK(cudaGetLastError());
-  return 0;
+  return launch_check((const void*)fn);
 }
 
 template <class Fn, class... Args>
@@ -152,8 +160,7 @@ int launch_plain(Fn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Arg
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fn<<<grid, block, smem, st>>>(args...);
   ++g_launches;
-  CK(cudaGetLastError());
-  return 0;
+  return launch_check((const void*)fn);
 }
 
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
@@ -713,24 +720,41 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
       return -1;
   }
   const double2* wst = normalize ? (const double2*)dstats.as<double2>() : nullptr;
+  // the query, normalised once, and its LB_Keogh envelope (search.py:185-187)
+  DBuf dqn, denv, dzero;
+  if (dqn.alloc(sizeof(double) * (size_t)lq, st)) return -1;
+  if (launch_plain(k_subseq_query<0>, dim3(1), dim3(32), sizeof(double) * ((size_t)lq + nl_ + 16), st, dq, (int)lq,
+                   (int)normalize, plan, dqn.as<double>()))
+    return -1;
+  const bool use_lb = share && lq * 5 * sizeof(double) <= 200 * 1024;
+  const float2* env = nullptr;
+  if (use_lb) {
+    if (denv.alloc(sizeof(float2) * (size_t)lq, st) || dzero.alloc(8, st)) return -1;
+    CK(cudaMemsetAsync(dzero.p, 0, 8, st));
+    if (launch_plain(k_envelope, dim3(1), dim3(256), sizeof(double) * 5 * (size_t)lq, st,
+                     (const double*)dqn.as<double>(), (const long long*)dzero.as<long long>(), (int)lq, 1,
+                     win < 0 ? (int)lq : win, denv.as<float2>()))
+      return -1;
+    env = denv.as<float2>();
+  }
   mark(st, "win_stats");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
   const int wpb = 8;
-  const size_t smem = sizeof(double) * ((size_t)subseq_head((int)lq, nl_, eng) + wpb * (size_t)subseq_warp((int)lq, eng));
+  const size_t smem = sizeof(double) * ((size_t)subseq_head((int)lq, eng) + wpb * (size_t)subseq_warp((int)lq, eng));
   if (!seeds.empty()) {
     DBuf dseed, dso, dst;
     const long long ns = (long long)seeds.size();
     if (dseed.alloc(8 * ns, st) || dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
     CK(cudaMemcpyAsync(dseed.p, seeds.data(), 8 * ns, cudaMemcpyHostToDevice, st));
-    if (launch_persistent(fn, 32 * wpb, smem, st, ns, dq, (int)lq, dref, (int)normalize, wst,
-                          (const long long*)dseed.as<long long>(), ns, win, plan, (int)share,
+    if (launch_persistent(fn, 32 * wpb, smem, st, ns, (const double*)dqn.as<double>(), (int)lq, dref,
+                          (int)normalize, wst, env, (const long long*)dseed.as<long long>(), ns, win, (int)share,
                           dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
       return -1;
-    CK(cudaStreamSynchronize(st));
   }
   mark(st, "subseq_phaseA");
-  if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, dq, (int)lq, dref, (int)normalize, wst,
-                        (const long long*)nullptr, nwin, win, plan, (int)share, dcut.as<unsigned long long>(),
+  if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, (const double*)dqn.as<double>(), (int)lq, dref,
+                        (int)normalize, wst, env, (const long long*)nullptr, nwin, win, (int)share,
+                        dcut.as<unsigned long long>(),
                         dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
     return -1;
   mark(st, "subseq_phaseB");

@@ -15,6 +15,7 @@
 // stiffness nu*(|i-j|+|i-j|)).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <type_traits>
 

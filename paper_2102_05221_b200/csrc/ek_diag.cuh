@@ -44,10 +44,15 @@ struct DiagResult {
   int t_end;     // last anti-diagonal processed
 };
 
+// The shared cutoff as one warp-uniform value.  Lanes of a warp are not
+// guaranteed to execute a load together (independent thread scheduling), so a
+// per-lane load can observe two different values around another warp's atomicMin;
+// every decision taken on the cutoff must be the same in all 32 lanes, hence lane
+// 0's value is broadcast.  Call from converged code only.
 __device__ __forceinline__ double ld_cut(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return __longlong_as_double((long long)v);
+  unsigned long long v = 0;
+  if ((threadIdx.x & 31) == 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return __longlong_as_double((long long)__shfl_sync(0xffffffffu, v, 0));
 }
 
 __device__ __forceinline__ int hi_word(double v) { return __double2hiint(v); }
@@ -69,7 +74,15 @@ __host__ __device__ constexpr int diag_pad(int P) { return 16 * P + 8; }
 struct SmemSeries {
   const double* p;
   int n;
-  __device__ __forceinline__ double at(int k) const { return p[k]; }
+  __device__ __forceinline__ double at(int k) const {
+#ifdef EKB_BOUNDS
+    if (k < -EKB_BOUNDS || k >= n + EKB_BOUNDS) {
+      printf("SmemSeries OOB k=%d n=%d block=%d warp=%d\n", k, n, blockIdx.x, threadIdx.x >> 5);
+      __trap();
+    }
+#endif
+    return p[k];
+  }
 };
 
 // Runs f(integral_constant<S>) for S = S0 .. U-1 until one returns true.

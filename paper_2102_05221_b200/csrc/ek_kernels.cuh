@@ -303,8 +303,20 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
     const int cnt = k_hi - k_lo;
     // this item's candidates and their metadata, one per lane (K <= 32)
     const int ord = lane < cnt ? order[(long long)q * ncand + k_lo + lane] : 0;
+#ifdef EKB_BOUNDS
+    if (ord < 0 || ord >= ncand || q < 0 || q >= nq || k_lo < 0 || k_hi > ncand || cnt > 32) {
+      printf("k_nn bad item q=%d ord=%d k_lo=%d k_hi=%d cnt=%d it=%lld\n", q, ord, k_lo, k_hi, cnt, it);
+      __trap();
+    }
+#endif
     const int olen = clen[ord];
     const long long ooff = coff[ord];
+#ifdef EKB_BOUNDS
+    if (olen < 0 || olen > lmax || qlen[q] > lmax) {
+      printf("k_nn bad len olen=%d lq=%d lmax=%d\n", olen, qlen[q], lmax);
+      __trap();
+    }
+#endif
     if (q != staged_q) {
       __syncwarp();
       stage_series<KIND>(QB, Q + qoff[q], lq, PAD);
