@@ -721,7 +721,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   }
   const double2* wst = normalize ? (const double2*)dstats.as<double2>() : nullptr;
   // the query, normalised once, and its LB_Keogh envelope (search.py:185-187)
-  DBuf dqn, denv, dzero;
+  DBuf dqn, denv, dzero, dkeys, dlbo;
   if (dqn.alloc(sizeof(double) * (size_t)lq, st)) return -1;
   if (launch_plain(k_subseq_query<0>, dim3(1), dim3(32), sizeof(double) * ((size_t)lq + nl_ + 16), st, dq, (int)lq,
                    (int)normalize, plan, dqn.as<double>()))
@@ -736,6 +736,16 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                      win < 0 ? (int)lq : win, denv.as<float2>()))
       return -1;
     env = denv.as<float2>();
+    // LB test order: positions by decreasing envelope excess (k_rank_sort on one row)
+    if (dkeys.alloc(sizeof(float) * (size_t)lq, st) || dlbo.alloc(sizeof(int) * (size_t)lq, st)) return -1;
+    if (launch_plain(k_env_keys<0>, dim3((unsigned)((lq + 255) / 256)), dim3(256), 0, st, env, (int)lq,
+                     dkeys.as<float>()))
+      return -1;
+    int np2 = 1;
+    while (np2 < lq) np2 <<= 1;
+    if (launch_plain(k_rank_sort, dim3(1), dim3(1024), (size_t)np2 * 8, st, (const float*)dkeys.as<float>(), (int)lq,
+                     np2, dlbo.as<int>()))
+      return -1;
   }
   mark(st, "win_stats");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
@@ -747,13 +757,15 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     if (dseed.alloc(8 * ns, st) || dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
     CK(cudaMemcpyAsync(dseed.p, seeds.data(), 8 * ns, cudaMemcpyHostToDevice, st));
     if (launch_persistent(fn, 32 * wpb, smem, st, ns, (const double*)dqn.as<double>(), (int)lq, dref,
-                          (int)normalize, wst, env, (const long long*)dseed.as<long long>(), ns, win, (int)share,
+                          (int)normalize, wst, env, (const int*)dlbo.as<int>(), (const long long*)dseed.as<long long>(),
+                          ns, win, (int)share,
                           dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
       return -1;
   }
   mark(st, "subseq_phaseA");
   if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, (const double*)dqn.as<double>(), (int)lq, dref,
-                        (int)normalize, wst, env, (const long long*)nullptr, nwin, win, (int)share,
+                        (int)normalize, wst, env, (const int*)dlbo.as<int>(), (const long long*)nullptr, nwin, win,
+                        (int)share,
                         dcut.as<unsigned long long>(),
                         dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
     return -1;
