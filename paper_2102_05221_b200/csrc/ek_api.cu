@@ -675,11 +675,11 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   DBuf dleaves, dops, dcut, dout, dtend, dcnt;
   if (dleaves.alloc(sizeof(int2) * leaves.size(), st) || dops.alloc(sizeof(int) * ops.size(), st) ||
       dcut.alloc(8, st) || dout.alloc(sizeof(double) * (size_t)nwin, st) || dtend.alloc(sizeof(int) * (size_t)nwin, st) ||
-      dcnt.alloc(16, st))
+      dcnt.alloc(32, st))
     return -1;
   CK(cudaMemcpyAsync(dleaves.p, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dops.p, ops.data(), sizeof(int) * ops.size(), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(dcnt.p, 0, 16, st));
+  CK(cudaMemsetAsync(dcnt.p, 0, 32, st));
   NpPlan plan{dleaves.as<int2>(), (int)leaves.size(), dops.as<int>(), (int)ops.size()};
   mark_reset();
   mark(st, "start");
@@ -750,25 +750,41 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   mark(st, "win_stats");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
   const int wpb = 8;
-  const size_t smem = sizeof(double) * ((size_t)subseq_head((int)lq, eng) + wpb * (size_t)subseq_warp((int)lq, eng));
+  const size_t smem = sizeof(double) * ((size_t)subseq_qslot((int)lq, eng) + wpb * (size_t)subseq_warp((int)lq, eng));
+  const double* qn_ = dqn.as<double>();
   if (!seeds.empty()) {
     DBuf dseed, dso, dst;
     const long long ns = (long long)seeds.size();
     if (dseed.alloc(8 * ns, st) || dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
     CK(cudaMemcpyAsync(dseed.p, seeds.data(), 8 * ns, cudaMemcpyHostToDevice, st));
-    if (launch_persistent(fn, 32 * wpb, smem, st, ns, (const double*)dqn.as<double>(), (int)lq, dref,
-                          (int)normalize, wst, env, (const int*)dlbo.as<int>(), (const long long*)dseed.as<long long>(),
-                          ns, win, (int)share,
+    if (launch_persistent(fn, 32 * wpb, smem, st, ns, qn_, (int)lq, dref, (int)normalize, wst,
+                          (const long long*)dseed.as<long long>(), ns, (const int*)nullptr, 0, win, (int)share,
                           dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
       return -1;
   }
   mark(st, "subseq_phaseA");
-  if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, (const double*)dqn.as<double>(), (int)lq, dref,
-                        (int)normalize, wst, env, (const int*)dlbo.as<int>(), (const long long*)nullptr, nwin, win,
-                        (int)share,
-                        dcut.as<unsigned long long>(),
-                        dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
-    return -1;
+  if (env) {
+    // phase B1: LB_Keogh test of every window (lane per window); B2: DP of the survivors
+    DBuf dsurv, dns;
+    if (dsurv.alloc(sizeof(long long) * (size_t)nwin, st) || dns.alloc(16, st)) return -1;
+    CK(cudaMemsetAsync(dns.p, 0, 16, st));
+    if (launch_persistent(get_subseq_lb(spec->cost_mode), 256, sizeof(double) * (size_t)subseq_lb_smem((int)lq), st,
+                          (nwin + 31) / 32, dref, (int)lq, (int)normalize, wst, env, (const int*)dlbo.as<int>(), nwin,
+                          (const unsigned long long*)dcut.as<unsigned long long>(), dout.as<double>(),
+                          dtend.as<int>(), dsurv.as<long long>(), dns.as<int>(), dcnt.as<int>() + 2))
+      return -1;
+    mark(st, "subseq_lb");
+    if (launch_persistent(fn, 32 * wpb, smem, st, nwin, qn_, (int)lq, dref, (int)normalize, wst,
+                          (const long long*)dsurv.as<long long>(), nwin, (const int*)dns.as<int>(), 1, win,
+                          (int)share, dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
+                          dcnt.as<int>() + 4))
+      return -1;
+  } else {
+    if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, qn_, (int)lq, dref, (int)normalize, wst,
+                          (const long long*)nullptr, nwin, (const int*)nullptr, 0, win, (int)share,
+                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
+      return -1;
+  }
   mark(st, "subseq_phaseB");
   if (profile) {
     CK(cudaMemcpyAsync(profile, dout.p, sizeof(double) * (size_t)nwin, cudaMemcpyDeviceToHost, st));

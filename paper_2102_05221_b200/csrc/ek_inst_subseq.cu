@@ -22,4 +22,6 @@ SubseqFn get_subseq(int mode, int eng) {
 
 SubseqUBFn get_subseq_ub(int mode) { return mode == 0 ? k_subseq_ub<0> : k_subseq_ub<1>; }
 
+SubseqLBFn get_subseq_lb(int mode) { return mode == 0 ? k_subseq_lb<0> : k_subseq_lb<1>; }
+
 }  // namespace ekb
