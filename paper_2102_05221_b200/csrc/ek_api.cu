@@ -684,48 +684,54 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   mark_reset();
   mark(st, "start");
   const int nl_ = plan.nleaves;
-  unsigned long long cut0 = 0x7ff0000000000000ULL;
-  std::vector<long long> seeds;
-  if (share) {
-    // sampled exact diagonal bounds; the best few windows run first (phase A)
-    const long long nsamp = std::min<long long>(nwin, 4096);
-    const long long stride = std::max<long long>(1, nwin / nsamp);
-    DBuf dub;
-    if (dub.alloc(sizeof(double) * nsamp, st)) return -1;
-    const size_t smem = sizeof(double) * ((size_t)lq + nl_ + 16 + 4 * ((size_t)lq + nl_ + 16));
-    if (launch_plain(get_subseq_ub(spec->cost_mode), dim3((unsigned)std::min<long long>(1024, (nsamp + 3) / 4)),
-                     dim3(128), smem, st, dq, (int)lq, dref, nwin, stride, (int)normalize, plan, dub.as<double>(),
-                     nsamp))
-      return -1;
-    std::vector<double> ub(nsamp);
-    CK(cudaMemcpyAsync(ub.data(), dub.p, sizeof(double) * nsamp, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::vector<long long> idx(nsamp);
-    for (long long k = 0; k < nsamp; ++k) idx[k] = k;
-    std::sort(idx.begin(), idx.end(), [&](long long a, long long b) { return ub[a] < ub[b] || (ub[a] == ub[b] && a < b); });
-    double best = ub[idx[0]];
-    if (best < INFINITY) {
-      std::memcpy(&cut0, &best, 8);
-      for (long long k = 0; k < std::min<long long>(16, nsamp); ++k) seeds.push_back(idx[k] * stride);
-    }
-  }
-  CK(cudaMemcpyAsync(dcut.p, &cut0, 8, cudaMemcpyHostToDevice, st));
-  mark(st, "seed_bounds");
   // z-normalisation statistics of every window (thread per window)
   DBuf dstats;
   if (normalize) {
     if (dstats.alloc(sizeof(double2) * (size_t)nwin, st)) return -1;
-    if (launch_plain(k_win_stats<0>, dim3((unsigned)((nwin + 255) / 256)), dim3(256), 0, st, dref, nwin, (int)lq, plan,
-                     dstats.as<double2>()))
+    const size_t ssm = sizeof(double) * (size_t)win_stats_smem((int)lq);
+    if (ssm <= 200 * 1024) {
+      if (launch_plain(k_win_stats4<0>, dim3((unsigned)((nwin + kStatsWin - 1) / kStatsWin)), dim3(256), ssm, st, dref,
+                       nwin, (int)lq, plan, dstats.as<double2>()))
+        return -1;
+    } else if (launch_plain(k_win_stats<0>, dim3((unsigned)((nwin + 255) / 256)), dim3(256), 0, st, dref, nwin,
+                            (int)lq, plan, dstats.as<double2>())) {
       return -1;
+    }
   }
   const double2* wst = normalize ? (const double2*)dstats.as<double2>() : nullptr;
-  // the query, normalised once, and its LB_Keogh envelope (search.py:185-187)
+  // the query, normalised once (search.py:181-182)
   DBuf dqn, denv, dzero, dkeys, dlbo;
   if (dqn.alloc(sizeof(double) * (size_t)lq, st)) return -1;
   if (launch_plain(k_subseq_query<0>, dim3(1), dim3(32), sizeof(double) * ((size_t)lq + nl_ + 16), st, dq, (int)lq,
                    (int)normalize, plan, dqn.as<double>()))
     return -1;
+  if (launch_plain(k_fill_u64, dim3(1), dim3(32), 0, st, dcut.as<unsigned long long>(), 1LL, 0x7ff0000000000000ULL))
+    return -1;
+  mark(st, "win_stats");
+  // cutoff seed: exact diagonal bounds of sampled windows; the best few run first (phase A)
+  DBuf dseed, dukeys, dsord;
+  long long ns = 0;
+  if (share) {
+    const long long nsamp = std::min<long long>(nwin, 4096);
+    const long long stride = std::max<long long>(1, nwin / nsamp);
+    if (dukeys.alloc(sizeof(float) * nsamp, st) || dsord.alloc(sizeof(int) * nsamp, st)) return -1;
+    if (launch_plain(get_subseq_ub(spec->cost_mode), dim3((unsigned)((nsamp + 3) / 4)), dim3(128), 0, st,
+                     (const double*)dqn.as<double>(), (int)lq, dref, stride, (int)normalize, wst, nsamp,
+                     dukeys.as<float>(), dcut.as<unsigned long long>()))
+      return -1;
+    int np2 = 1;
+    while (np2 < nsamp) np2 <<= 1;
+    if (launch_plain(k_rank_sort, dim3(1), dim3(1024), (size_t)np2 * 8, st, (const float*)dukeys.as<float>(),
+                     (int)nsamp, np2, dsord.as<int>()))
+      return -1;
+    ns = std::min<long long>(16, nsamp);
+    if (dseed.alloc(sizeof(long long) * ns, st)) return -1;
+    if (launch_plain(k_seed_list<0>, dim3(1), dim3(32), 0, st, (const int*)dsord.as<int>(), (int)ns, stride,
+                     dseed.as<long long>()))
+      return -1;
+  }
+  mark(st, "seed_bounds");
+  // LB_Keogh envelope of the query (search.py:185-187) and the test order
   const bool use_lb = share && lq * 5 * sizeof(double) <= 200 * 1024;
   const float2* env = nullptr;
   if (use_lb) {
@@ -736,7 +742,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                      win < 0 ? (int)lq : win, denv.as<float2>()))
       return -1;
     env = denv.as<float2>();
-    // LB test order: positions by decreasing envelope excess (k_rank_sort on one row)
+    // positions by decreasing envelope excess (k_rank_sort on one row)
     if (dkeys.alloc(sizeof(float) * (size_t)lq, st) || dlbo.alloc(sizeof(int) * (size_t)lq, st)) return -1;
     if (launch_plain(k_env_keys<0>, dim3((unsigned)((lq + 255) / 256)), dim3(256), 0, st, env, (int)lq,
                      dkeys.as<float>()))
@@ -747,16 +753,14 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                      np2, dlbo.as<int>()))
       return -1;
   }
-  mark(st, "win_stats");
+  mark(st, "envelope");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
   const int wpb = 8;
   const size_t smem = sizeof(double) * ((size_t)subseq_qslot((int)lq, eng) + wpb * (size_t)subseq_warp((int)lq, eng));
   const double* qn_ = dqn.as<double>();
-  if (!seeds.empty()) {
-    DBuf dseed, dso, dst;
-    const long long ns = (long long)seeds.size();
-    if (dseed.alloc(8 * ns, st) || dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
-    CK(cudaMemcpyAsync(dseed.p, seeds.data(), 8 * ns, cudaMemcpyHostToDevice, st));
+  if (ns > 0) {
+    DBuf dso, dst;
+    if (dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
     if (launch_persistent(fn, 32 * wpb, smem, st, ns, qn_, (int)lq, dref, (int)normalize, wst,
                           (const long long*)dseed.as<long long>(), ns, (const int*)nullptr, 0, win, (int)share,
                           dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
