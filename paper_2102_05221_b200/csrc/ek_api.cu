@@ -236,6 +236,16 @@ NNFn pick_nn(int kind, int mode, int eng) {
   }
   return nullptr;
 }
+NNFixFn pick_nn_fix(int kind, int mode, int eng) {
+  switch (kind_tag(kind)) {
+    case K_DTW: return get_nn_fix<K_DTW>(mode, eng);
+    case K_WDTW: return get_nn_fix<K_WDTW>(mode, eng);
+    case K_ERP: return get_nn_fix<K_ERP>(mode, eng);
+    case K_MSM: return get_nn_fix<K_MSM>(mode, eng);
+    case K_TWE: return get_nn_fix<K_TWE>(mode, eng);
+  }
+  return nullptr;
+}
 UBFn pick_ub(int kind, int mode) {
   switch (kind_tag(kind)) {
     case K_DTW: return get_ub<K_DTW>(mode);
@@ -425,6 +435,17 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
   return 0;
 }
 
+// guarded engine for wide bands (EKB_GUARD=0/8/16 overrides, for tuning)
+static int guard_engine_impl() {
+  const char* e = getenv("EKB_GUARD");
+  const int g = e ? atoi(e) : 8;
+  return g == 16 ? E_GDIAG16 : g == 8 ? E_GDIAG8 : -1;
+}
+static int guard_engine() {
+  static const int g = guard_engine_impl();
+  return g;
+}
+
 static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, const int64_t* dqoff,
                        const int32_t* dqlen, int64_t nq, const double* dC, const int64_t* dcoff, const int32_t* dclen,
                        int64_t ncand, int32_t max_len, int32_t dense, int64_t* d_idx, double* d_dist,
@@ -448,9 +469,18 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   DBuf dord, dkeys, dout, dtend, dcut, dcnt, denv;
   if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dout.alloc(sizeof(double) * (size_t)npairs, st) ||
       dtend.alloc(sizeof(int) * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
-      dcnt.alloc(sizeof(int) * 4 * 2, st))
+      dcnt.alloc(sizeof(int) * 16, st))
     return -1;
-  CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 8, st));
+  CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 16, st));
+  int* const ovf_count = dcnt.as<int>() + 8;  // guarded-band overflows (phase B) and their redo counter
+  // phase B engine: with a cutoff, wide bands run as a guarded P=8 band (EAPruned's pruned
+  // columns skipped wholesale; overflows are redone by k_nn_fix).  ERP keeps its window
+  // semantics in the borders, so it never narrows.
+  int engB = eng;
+  if (share && kind_tag(spec->kind) != K_ERP && (!engine_is_diag(eng) || eng == E_DIAG16) && guard_engine() >= 0)
+    engB = guard_engine();
+  DBuf dovf;
+  if (engB != eng && dovf.alloc(sizeof(int2) * (size_t)npairs, st)) return -1;
   // 1. candidate order: approximate Euclidean ranking (scheduling only)
   const bool rank = share && ncand <= 16384 && ncand > 1;
   if (rank) {
@@ -491,7 +521,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
                           (const int*)dord.as<int>(), 0, ka, 1, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>(),
-                          (const float2*)nullptr))
+                          (const float2*)nullptr, dovf.as<int2>(), ovf_count))
       return -1;
   }
   mark(st, "nn_phaseA");
@@ -510,18 +540,28 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // one pair per item for load balance, the rest in items of 8
   const int kb1 = (int)std::min<int64_t>(ncand, ka + 64);
   const int seg_lo[2] = {ka, kb1}, seg_hi[2] = {kb1, (int)ncand}, seg_k[2] = {1, 8};
+  const NNFn fnB = pick_nn(spec->kind, spec->cost_mode, engB);
+  const size_t smemB = pair_smem(max_len, engB, wpb);
   for (int sgi = 0; sgi < 2; ++sgi) {
     if (seg_lo[sgi] >= seg_hi[sgi]) continue;
     const int K = seg_k[sgi];
     const long long items = (long long)nq * ((seg_hi[sgi] - seg_lo[sgi] + K - 1) / K);
-    if (launch_persistent(fn, 32 * wpb, smem, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
+    if (launch_persistent(fnB, 32 * wpb, smemB, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
                           (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(),
                           seg_lo[sgi], seg_hi[sgi], K, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
-                          dcnt.as<int>() + 2 + 2 * sgi, env))
+                          dcnt.as<int>() + 2 + 2 * sgi, env, dovf.as<int2>(), ovf_count))
       return -1;
   }
   mark(st, "nn_phaseB");
+  if (engB != eng) {  // redo guarded-band overflows with the full-band engine
+    if (launch_persistent(pick_nn_fix(spec->kind, spec->cost_mode, eng), 32 * wpb, smem, st, npairs, dQ,
+                          (const long long*)dqoff, (const int*)dqlen, dC, (const long long*)dcoff, (const int*)dclen,
+                          (int)ncand, (const int2*)dovf.as<int2>(), (const int*)ovf_count, win, (int)max_len, ph.prm,
+                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), ovf_count + 1))
+      return -1;
+    mark(st, "nn_fix");
+  }
   // 4. lexicographic (distance, index) minimum + accounting
   if (launch_plain(k_nn_reduce, dim3((unsigned)nq), dim3(256), 0, st, (const double*)dout.as<double>(),
                    (const int*)dtend.as<int>(), (const int*)dqlen, (int)nq, (const int*)dclen, (int)ncand, win,

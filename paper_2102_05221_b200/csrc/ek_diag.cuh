@@ -42,6 +42,7 @@ constexpr unsigned FULL = 0xffffffffu;
 struct DiagResult {
   double cost;   // exact, or +inf when abandoned / above cutoff
   int t_end;     // last anti-diagonal processed
+  bool ovf;      // guarded band: a cell <= cutoff reached a guard lane (cost meaningless)
 };
 
 // The shared cutoff as one warp-uniform value.  Lanes of a warp are not
@@ -98,9 +99,19 @@ __device__ __forceinline__ bool unrolled_steps(F& f) {
 
 // X: lines accessor (nl >= nc), Y: cols accessor.  w: effective window
 // (w >= nl - nc, checked by the caller).
+//
+// guard != 0 (a lane mask) runs the band [-w, w] as a stand-in for a wider true band:
+// cells outside it count as +inf.  That is exact under the keep-if-<=-cutoff contract
+// as long as no cell <= cutoff ever appears in a guard lane (the lanes holding the
+// band's narrowed edges).  A path of cost <= cutoff has all its prefixes <= cutoff
+// (costs are >= 0) and moves one diagonal at a time, so before it could leave the
+// band it would put a live cell, computed exactly, in a guard lane; the cutoff only
+// decreases, so a path <= the final cutoff is live at every check.  On that event the
+// pair stops with ovf set and the caller redoes it with a full-band engine.
 template <int KIND, int MODE, int P, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
 __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
-                                const unsigned long long* cutp, const Params& prm, Loader& ld) {
+                                const unsigned long long* cutp, const Params& prm, Loader& ld,
+                                unsigned guard = 0u) {
   static_assert(P % 2 == 0 && P >= 2, "P must be even");
   constexpr int H = P / 2;
   constexpr bool BORDERED = (KIND == K_ERP);
@@ -152,6 +163,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   const int Tf = nl + nc;
   int cut_hi = hi_word(cut);
   bool dead = false;
+  bool ovf = false;
 
   // One double step.  With ROT the register windows are rings whose rotation
   // (rx for xw, ry for yw) is a compile-time function of the unrolled step S,
@@ -206,8 +218,13 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
     if (t + 1 >= Tf) return true;
-    if (!__any_sync(FULL, alive)) {
+    const unsigned live = __ballot_sync(FULL, alive);
+    if (!live) {
       dead = true;
+      return true;
+    }
+    if (live & guard) {
+      ovf = true;
       return true;
     }
     // ---- slide the register windows by one element ----
@@ -258,8 +275,9 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   }
 
   DiagResult res;
-  res.t_end = dead ? t + 1 : Tf;  // last anti-diagonal evaluated
-  if (dead) {
+  res.t_end = (dead || ovf) ? t + 1 : Tf;  // last anti-diagonal evaluated
+  res.ovf = ovf;
+  if (dead || ovf) {
     res.cost = EKB_INF;
     return res;
   }

@@ -21,17 +21,24 @@
 namespace ekb {
 
 // Engine codes: 0..2 diagonal P=4/8/16; 3..5 stripe S=4/8/16 (unbanded);
-// 6 stripe S=16 banded; 7 stripe S=16 banded with row abandoning ("ea").
+// 6 stripe S=16 banded; 7 stripe S=16 banded with row abandoning ("ea");
+// 8..9 guarded diagonal P=8/16: a band narrower than the pair's own, valid as long as
+// no cell <= cutoff reaches the band's edge lanes (else the pair is redone; see
+// diag_pair's GUARD) -- EAPruned's pruned columns, skipped wholesale.
 enum Engine : int {
   E_DIAG4 = 0, E_DIAG8 = 1, E_DIAG16 = 2,
   E_STR4 = 3, E_STR8 = 4, E_STR16 = 5,
   E_STRB16 = 6,
   E_STR16_EA = 7,
-  E_COUNT = 8
+  E_GDIAG8 = 8, E_GDIAG16 = 9,
+  E_COUNT = 10
 };
 
-__host__ __device__ constexpr int engine_is_diag(int e) { return e <= E_DIAG16; }
-__host__ __device__ constexpr int engine_P(int e) { return e == E_DIAG4 ? 4 : e == E_DIAG8 ? 8 : 16; }
+__host__ __device__ constexpr int engine_is_diag(int e) { return e <= E_DIAG16 || e >= E_GDIAG8; }
+__host__ __device__ constexpr int engine_guarded(int e) { return e >= E_GDIAG8; }
+__host__ __device__ constexpr int engine_P(int e) {
+  return e == E_DIAG4 ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
+}
 __host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e == E_STR8 ? 8 : 16; }
 // elements an engine may read beyond either end of a staged series
 __host__ __device__ constexpr int engine_pad(int e) {
@@ -91,11 +98,45 @@ __device__ __forceinline__ void stage_table(double* tab, int len, const Params& 
   }
 }
 
+// The band an engine actually runs: guarded engines narrow it to what 32 lanes of P
+// slots hold (the widest w with diag_slots_needed <= 32P).
+template <int ENG>
+__device__ __forceinline__ int engine_band(int nl, int nc, int w) {
+  if constexpr (engine_guarded(ENG)) {
+    constexpr int P = engine_P(ENG);
+    int wg = min(w, 16 * P - 2);
+    while (wg > 0 && diag_slots_needed(nl, nc, wg) > 32 * P) --wg;
+    return wg;
+  } else {
+    return w;
+  }
+}
+
 template <int KIND, int MODE, int ENG, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
 __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
                                            const unsigned long long* cutp, const double* tab, int tablen,
                                            const Params& prm, Loader& ld, double& cost, int& tend) {
-  if constexpr (engine_is_diag(ENG)) {
+  if constexpr (engine_guarded(ENG)) {
+    // the widest band that fits 32 lanes of P slots; guard the sides it narrows
+    constexpr int P = engine_P(ENG);
+    const int wg = engine_band<ENG>(nl, nc, w);
+    if (wg < nl - nc) {  // the final cell would fall outside: redo with the full engine
+      cost = __longlong_as_double(0x7ff8000000000000LL);
+      tend = -1;
+      return;
+    }
+    const int dlo_t = max(-w, 1 - nc), dhi_t = min(w, nl - 1);
+    const int dlo_g = max(-wg, 1 - nc), dhi_g = min(wg, nl - 1);
+    const int dbase = (dlo_g - 1) & ~1;
+    const unsigned guard = (dlo_g > dlo_t ? 1u : 0u) | (dhi_g < dhi_t ? 1u << ((dhi_g - dbase) / P) : 0u);
+    DiagResult r = diag_pair<KIND, MODE, P, SHARED_CUT>(X, nl, Y, nc, wg, cut, cutp, prm, ld, guard);
+    cost = r.cost;
+    tend = r.t_end;
+    if (r.ovf) {
+      cost = __longlong_as_double(0x7ff8000000000000LL);
+      tend = -1;
+    }
+  } else if constexpr (engine_is_diag(ENG)) {
     DiagResult r = diag_pair<KIND, MODE, engine_P(ENG), SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
     cost = r.cost;
     tend = r.t_end;
@@ -276,7 +317,8 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
                                             int K, int win, int lmax, Params prm, int share,
                                             unsigned long long* cutbits, double* __restrict__ out,
                                             int* __restrict__ tend_out, int* __restrict__ counter,
-                                            const float2* __restrict__ env) {
+                                            const float2* __restrict__ env, int2* __restrict__ ovf_list,
+                                            int* __restrict__ ovf_count) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
   constexpr int PF = kChunk / 32;
@@ -406,11 +448,66 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
         }
         if (share) cut = fmin(cut, fmin(cost, ld_cut(cutbits + q)));
       }
-      const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) : 0;
+      const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, engine_band<ENG>(nl, nc, w), tend, KIND == K_ERP ? 0 : 1) : 0;
       if (lane == 0) {
+        if (tend < 0) {  // guarded band overflowed: the pair is redone by k_nn_fix
+          ovf_list[atomicAdd(ovf_count, 1)] = make_int2(q, c);
+          cost = EKB_INF;
+        }
         out[(long long)q * ncand + c] = cost;
         tend_out[(long long)q * ncand + c] = cells;
       }
+    }
+  }
+}
+
+// Redo of the pairs a guarded band gave up on (k_nn's ovf_list, *ovf_count of them)
+// with a full-band engine and the query's shared cutoff.
+template <int KIND, int MODE, int ENG>
+__global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, const long long* __restrict__ qoff,
+                                                const int* __restrict__ qlen, const double* __restrict__ C,
+                                                const long long* __restrict__ coff, const int* __restrict__ clen,
+                                                int ncand, const int2* __restrict__ list,
+                                                const int* __restrict__ count, int win, int lmax, Params prm,
+                                                unsigned long long* cutbits, double* __restrict__ out,
+                                                int* __restrict__ tend_out, int* __restrict__ counter) {
+  extern __shared__ double smem[];
+  constexpr int PAD = engine_pad(ENG);
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* X = smem + wib * warp_stride(lmax, ENG) + PAD;
+  double* Y = X + series_slot(lmax, PAD);
+  double* tab = Y - PAD + series_slot(lmax, PAD);
+  const int n = *count;
+  NoLoader ld;
+  for (;;) {
+    int e = 0;
+    if (lane == 0) e = atomicAdd(counter, 1);
+    e = __shfl_sync(FULL, e, 0);
+    if (e >= n) break;
+    const int2 pc = list[e];
+    const int q = pc.x, c = pc.y;
+    const int lq = qlen[q], lc = clen[c];
+    const bool q_rows = lq >= lc;  // orientation (kernels.py:168-171)
+    const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
+    const int w = win < 0 ? nl : win;
+    const Params pp = pair_params(prm, nl);
+    __syncwarp();
+    stage_series<KIND>(X, q_rows ? Q + qoff[q] : C + coff[c], nl, PAD);
+    stage_series<KIND>(Y, q_rows ? C + coff[c] : Q + qoff[q], nc, PAD);
+    const int tablen = max(nl, nc) + 1;
+    if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
+    __syncwarp();
+    const double cut = ld_cut(cutbits + q);
+    double cost;
+    int tend;
+    run_engine<KIND, MODE, ENG, true>(SmemSeries{X, nl}, nl, SmemSeries{Y, nc}, nc, w, cut, cutbits + q, tab, tablen,
+                                      pp, ld, cost, tend);
+    const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) : 0;
+    if (lane == 0) {
+      if (cost < EKB_INF) atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
+      out[(long long)q * ncand + c] = cost;
+      tend_out[(long long)q * ncand + c] = cells;
     }
   }
 }

@@ -10,7 +10,9 @@ using TriFn = void (*)(const double*, const long long*, const int*, int, int, in
                       unsigned long long*, int*);
 using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, int, int, int, int, Params, int, unsigned long long*,
-                      double*, int*, int*, const float2*);
+                      double*, int*, int*, const float2*, int2*, int*);
+using NNFixFn = void (*)(const double*, const long long*, const int*, const double*, const long long*, const int*,
+                         int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*);
 using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, Params, unsigned long long*);
 
@@ -113,6 +115,28 @@ NNFn get_nn(int mode, int eng) {
   switch (mode * 16 + eng) {
     EKB_ENG_CASES(0, k_nn)
     EKB_ENG_CASES(1, k_nn)
+    case 0 * 16 + E_GDIAG8: return k_nn<KIND, 0, E_GDIAG8>;
+    case 1 * 16 + E_GDIAG8: return k_nn<KIND, 1, E_GDIAG8>;
+    case 0 * 16 + E_GDIAG16: return k_nn<KIND, 0, E_GDIAG16>;
+    case 1 * 16 + E_GDIAG16: return k_nn<KIND, 1, E_GDIAG16>;
+  }
+  return nullptr;
+}
+
+// full-band engines that redo guarded-band overflows
+template <int KIND>
+NNFixFn get_nn_fix(int mode, int eng) {
+  switch (mode * 16 + eng) {
+    case 0 * 16 + E_STR4: return k_nn_fix<KIND, 0, E_STR4>;
+    case 1 * 16 + E_STR4: return k_nn_fix<KIND, 1, E_STR4>;
+    case 0 * 16 + E_STR8: return k_nn_fix<KIND, 0, E_STR8>;
+    case 1 * 16 + E_STR8: return k_nn_fix<KIND, 1, E_STR8>;
+    case 0 * 16 + E_STR16: return k_nn_fix<KIND, 0, E_STR16>;
+    case 1 * 16 + E_STR16: return k_nn_fix<KIND, 1, E_STR16>;
+    case 0 * 16 + E_DIAG16: return k_nn_fix<KIND, 0, E_DIAG16>;
+    case 1 * 16 + E_DIAG16: return k_nn_fix<KIND, 1, E_DIAG16>;
+    case 0 * 16 + E_STRB16: return k_nn_fix<KIND, 0, E_STRB16>;
+    case 1 * 16 + E_STRB16: return k_nn_fix<KIND, 1, E_STRB16>;
   }
   return nullptr;
 }
@@ -126,6 +150,7 @@ UBFn get_ub(int mode) {
   template PairsFn get_pairs<K>(int, int);       \
   template TriFn get_triangle<K>(int, int);      \
   template NNFn get_nn<K>(int, int);             \
+  template NNFixFn get_nn_fix<K>(int, int);      \
   template UBFn get_ub<K>(int);
 
 }  // namespace ekb

@@ -252,3 +252,34 @@ def test_nn_lb_filter_scale(gpu, kind, window, mode):
     assert np.array_equal(dist, r["nn_distance"])
     assert idx[5] == 300 and dist[5] == 0.0
     assert np.all(comp + ab == len(C))
+
+
+@pytest.mark.parametrize("kind", ["msm", "twe", "dtw", "wdtw"])
+def test_nn_guarded_band(gpu, kind):
+    """Unconstrained series longer than a P=8 band: phase B runs the guarded band
+    (ek_kernels.cuh E_GDIAG8) and must return the oracle's answer exactly."""
+    from paper_2102_05221_b200 import datagen
+
+    C, cl, protos = datagen.warped_prototypes(300, 400, 6, 0.2, 91)
+    Q, ql, _ = datagen.warped_prototypes(8, 400, 6, 0.2, 92, protos=protos)
+    params = {"msm": dict(msm_c=1.0), "twe": dict(twe_nu=0.001, twe_lambda=1.0), "dtw": {}, "wdtw": dict(wdtw_g=0.05)}
+    spec = gpu.DistanceSpec(kind=kind, **params[kind])
+    for variant in ("eapruned", "ea"):
+        idx, dist = gpu.nn_batch(spec, variant, Q, C)[:2]
+        r = eko.nn(spec, variant, Q, C, threads=4)
+        assert np.array_equal(idx, r["nn_index"]), (kind, variant)
+        assert np.array_equal(dist, r["nn_distance"]), (kind, variant)
+
+
+@pytest.mark.parametrize("kind", ["msm", "dtw"])
+def test_nn_guard_overflow_redo(gpu, rng, kind):
+    """Near-constant series keep every cell under the cutoff, so the guarded band
+    overflows and k_nn_fix redoes the pairs: still the oracle's answer."""
+    C = rng.normal(0.0, 1e-3, size=(40, 300))
+    Q = rng.normal(0.0, 1e-3, size=(3, 300))
+    C[7] = Q[1]
+    spec = gpu.DistanceSpec(kind=kind, msm_c=1.0) if kind == "msm" else gpu.DistanceSpec(kind=kind)
+    idx, dist = gpu.nn_batch(spec, "eapruned", Q, C)[:2]
+    r = eko.nn(spec, "eapruned", Q, C, threads=4)
+    assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"])
+    assert idx[1] == 7 and dist[1] == 0.0
