@@ -39,6 +39,10 @@ namespace ekb {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef EKB_ROT_MAX_H
+#define EKB_ROT_MAX_H 2  // register windows rotate at compile time up to H = P/2 = 2 (U = 6 unrolled steps)
+#endif
+
 struct DiagResult {
   double cost;   // exact, or +inf when abandoned / above cutoff
   int t_end;     // last anti-diagonal processed
@@ -108,7 +112,7 @@ __device__ __forceinline__ bool unrolled_steps(F& f) {
 // band it would put a live cell, computed exactly, in a guard lane; the cutoff only
 // decreases, so a path <= the final cutoff is live at every check.  On that event the
 // pair stops with ovf set and the caller redoes it with a full-band engine.
-template <int KIND, int MODE, int P, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
+template <int KIND, int MODE, int P, bool SHARED_CUT, bool GUARD = false, class XAcc, class YAcc, class Loader>
 __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
                                 const unsigned long long* cutp, const Params& prm, Loader& ld,
                                 unsigned guard = 0u) {
@@ -168,7 +172,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   // One double step.  With ROT the register windows are rings whose rotation
   // (rx for xw, ry for yw) is a compile-time function of the unrolled step S,
   // so sliding costs no register moves; otherwise the windows shift in place.
-  constexpr bool ROT = (H <= 2);
+  constexpr bool ROT = (H <= EKB_ROT_MAX_H);
   constexpr int U = ROT ? H * (H + 1) : 1;
   auto dstep = [&](auto S_) -> bool {
     constexpr int S = decltype(S_)::value;
@@ -218,13 +222,18 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
     if (t + 1 >= Tf) return true;
-    const unsigned live = __ballot_sync(FULL, alive);
-    if (!live) {
+    if constexpr (GUARD) {
+      const unsigned live = __ballot_sync(FULL, alive);
+      if (!live) {
+        dead = true;
+        return true;
+      }
+      if (live & guard) {
+        ovf = true;
+        return true;
+      }
+    } else if (!__any_sync(FULL, alive)) {
       dead = true;
-      return true;
-    }
-    if (live & guard) {
-      ovf = true;
       return true;
     }
     // ---- slide the register windows by one element ----

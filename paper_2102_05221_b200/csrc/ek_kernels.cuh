@@ -129,7 +129,7 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
     const int dlo_g = max(-wg, 1 - nc), dhi_g = min(wg, nl - 1);
     const int dbase = (dlo_g - 1) & ~1;
     const unsigned guard = (dlo_g > dlo_t ? 1u : 0u) | (dhi_g < dhi_t ? 1u << ((dhi_g - dbase) / P) : 0u);
-    DiagResult r = diag_pair<KIND, MODE, P, SHARED_CUT>(X, nl, Y, nc, wg, cut, cutp, prm, ld, guard);
+    DiagResult r = diag_pair<KIND, MODE, P, SHARED_CUT, true>(X, nl, Y, nc, wg, cut, cutp, prm, ld, guard);
     cost = r.cost;
     tend = r.t_end;
     if (r.ovf) {
