@@ -477,7 +477,9 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // columns skipped wholesale; overflows are redone by k_nn_fix).  ERP keeps its window
   // semantics in the borders, so it never narrows.
   int engB = eng;
-  if (share && kind_tag(spec->kind) != K_ERP && (!engine_is_diag(eng) || eng == E_DIAG16) && guard_engine() >= 0)
+  // (only when the band is well beyond what the guarded lanes hold)
+  if (share && kind_tag(spec->kind) != K_ERP && (!engine_is_diag(eng) || eng == E_DIAG16) && guard_engine() >= 0 &&
+      diag_slots_needed(max_len, max_len, wmax) > 384)
     engB = guard_engine();
   DBuf dovf;
   if (engB != eng && dovf.alloc(sizeof(int2) * (size_t)npairs, st)) return -1;
@@ -485,15 +487,22 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   const bool rank = share && ncand <= 16384 && ncand > 1;
   if (rank) {
     if (dkeys.alloc(sizeof(float) * (size_t)npairs, st)) return -1;
-    if (launch_plain(k_rank_dist, dim3((unsigned)((ncand + 31) / 32), (unsigned)((nq + 31) / 32)), dim3(256), 0, st,
-                     dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC, (const long long*)dcoff,
-                     (const int*)dclen, (int)ncand, dkeys.as<float>()))
+    // FP32 Euclidean distance between piecewise aggregates (segments of 4 points)
+    const int R = 4, D = (max_len + R - 1) / R;
+    DBuf dqp, dcp;
+    if (dqp.alloc(sizeof(float) * (size_t)nq * D, st) || dcp.alloc(sizeof(float) * (size_t)ncand * D, st)) return -1;
+    auto blocks = [](long long n) { return dim3((unsigned)std::min<long long>(2048, (n + 255) / 256)); };
+    if (launch_plain(k_paa, blocks((long long)nq * D), dim3(256), 0, st, dQ, (const long long*)dqoff,
+                     (const int*)dqlen, (int)nq, R, D, dqp.as<float>()) ||
+        launch_plain(k_paa, blocks((long long)ncand * D), dim3(256), 0, st, dC, (const long long*)dcoff,
+                     (const int*)dclen, (int)ncand, R, D, dcp.as<float>()))
       return -1;
-    int np2 = 1;
-    while (np2 < ncand) np2 <<= 1;
-    if (launch_plain(k_rank_sort, dim3((unsigned)nq), dim3(1024), (size_t)np2 * 8, st, (const float*)dkeys.as<float>(),
-                     (int)ncand, np2, dord.as<int>()))
+    if (launch_plain(k_rank_paa, dim3((unsigned)((ncand + 63) / 64), (unsigned)((nq + 63) / 64)), dim3(256), 0, st,
+                     (const float*)dqp.as<float>(), (int)nq, (const float*)dcp.as<float>(), (int)ncand, D,
+                     dkeys.as<float>()))
       return -1;
+    CK(rank_radix((const float*)dkeys.as<float>(), (int)nq, (int)ncand, dord.as<int>(), st));
+    ++g_launches;
   } else {
     if (launch_plain(k_identity_order, dim3(1024), dim3(256), 0, st, (int)nq, (int)ncand, dord.as<int>())) return -1;
   }

@@ -2,6 +2,7 @@
 // (a scheduling heuristic only -- it never decides a result), the per-query
 // lexicographic (distance, index) reduction, and computed-cell accounting.
 #include "ek_misc.cuh"
+#include <cub/block/block_radix_sort.cuh>
 
 namespace ekb {
 
@@ -43,6 +44,114 @@ __global__ void __launch_bounds__(256) k_rank_dist(const double* __restrict__ Q,
     const int q = q0 + ty + 8 * u, c = c0 + tx;
     if (q < nq && c < ncand) out[(long long)q * ncand + c] = acc[u];
   }
+}
+
+// Piecewise aggregate approximation for the ranking: dst[s * D + k] = sum of series s
+// over points [kR, kR + R) (zero past its end), in FP32.  Ranking only.
+__global__ void k_paa(const double* __restrict__ src, const long long* __restrict__ off,
+                      const int* __restrict__ len, int n, int R, int D, float* __restrict__ dst) {
+  const long long total = (long long)n * D;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(e / D), k = (int)(e % D);
+    const int L = len[s];
+    const double* x = src + off[s];
+    float acc = 0.f;
+    for (int r = 0; r < R; ++r) {
+      const int i = k * R + r;
+      if (i < L) acc += (float)x[i];
+    }
+    dst[e] = acc;
+  }
+}
+
+// Squared Euclidean distance between PAA rows (FP32), 64x64 (query, candidate) tile per
+// block, 4x4 per thread, D in chunks of 16 through shared memory.  Ranking only.
+__global__ void __launch_bounds__(256) k_rank_paa(const float* __restrict__ Qp, int nq, const float* __restrict__ Cp,
+                                                  int ncand, int D, float* __restrict__ out) {
+  __shared__ float qs[16][65];
+  __shared__ float cs[16][65];
+  const int q0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int kb = 0; kb < D; kb += 16) {
+    for (int e = threadIdx.x; e < 64 * 16; e += 256) {
+      const int r = e >> 4, k = e & 15;
+      const int q = q0 + r, c = c0 + r, kk = kb + k;
+      qs[k][r] = (q < nq && kk < D) ? Qp[(long long)q * D + kk] : 0.f;
+      cs[k][r] = (c < ncand && kk < D) ? Cp[(long long)c * D + kk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = qs[k][ty + 16 * u];
+        b[u] = cs[k][tx + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const float d = a[u] - b[v];
+          acc[u][v] = fmaf(d, d, acc[u][v]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int q = q0 + ty + 16 * u, c = c0 + tx + 16 * v;
+      if (q < nq && c < ncand) out[(long long)q * ncand + c] = acc[u][v];
+    }
+}
+
+// Per query: stable block radix sort of (key, candidate) -> ranked candidate order
+// (ties keep index order).  THREADS x ITEMS >= ncand; padding sorts last.
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) k_rank_radix(const float* __restrict__ keys, int ncand,
+                                                        int* __restrict__ order) {
+  using Sort = cub::BlockRadixSort<float, THREADS, ITEMS, int>;
+  extern __shared__ __align__(16) unsigned char rank_sm[];
+  auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(rank_sm);
+  const int q = blockIdx.x;
+  const float* row = keys + (long long)q * ncand;
+  float k[ITEMS];
+  int v[ITEMS];
+#pragma unroll
+  for (int u = 0; u < ITEMS; ++u) {
+    const int i = threadIdx.x * ITEMS + u;  // blocked arrangement
+    const float key = i < ncand ? row[i] : __int_as_float(0x7f800000);
+    k[u] = key != key ? __int_as_float(0x7f800000) : key;  // NaN ranks last
+    v[u] = i;
+  }
+  Sort(tmp).Sort(k, v);
+#pragma unroll
+  for (int u = 0; u < ITEMS; ++u) {
+    const int i = threadIdx.x * ITEMS + u;
+    if (i < ncand) order[(long long)q * ncand + i] = v[u];
+  }
+}
+// launched from this unit (a template kernel's host stub must live with its definition)
+cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st) {
+  if (ncand <= 128 * 8) {
+    using Sort = cub::BlockRadixSort<float, 128, 8, int>;
+    k_rank_radix<128, 8><<<nq, 128, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order);
+  } else if (ncand <= 256 * 16) {
+    using Sort = cub::BlockRadixSort<float, 256, 16, int>;
+    k_rank_radix<256, 16><<<nq, 256, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order);
+  } else {
+    using Sort = cub::BlockRadixSort<float, 1024, 16, int>;
+    const size_t sm = sizeof(typename Sort::TempStorage);
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_rank_radix<1024, 16>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_rank_radix<1024, 16><<<nq, 1024, sm, st>>>(keys, ncand, order);
+  }
+  return cudaGetLastError();
 }
 
 // Per query: bitonic sort of (key, candidate) in shared memory -> ranked candidate order.
