@@ -471,11 +471,15 @@ def run_ours(args):
     }
     if "e2e" in head:
         line["e2e"] = head["e2e"]
-    prof = os.path.join(REPO, "profiles", f"ncu_{args.config}.json")
-    if os.path.exists(prof):
+    # dram bytes per launch of the dominant kernel from the committed `ncu --set full` summary
+    import glob
+
+    profs = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_ncu_{args.config}_*.json")))
+    if profs:
         try:
-            line["roofline"]["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:
+            line["roofline"]["traffic"] = json.load(open(profs[-1])).get("dram_bytes_per_launch")
+            line["roofline"]["traffic_source"] = os.path.relpath(profs[-1], REPO)
+        except (OSError, ValueError):
             pass
     if not args.no_cpu_baseline:
         cb = cpu_baseline_nn(args.config) if args.config in ("c1", "c2", "c4m", "c4t") else \
