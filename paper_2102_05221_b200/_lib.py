@@ -80,6 +80,8 @@ def lib():
 def check(rc: int) -> None:
     if rc != 0:
         msg = lib().ek_last_error().decode("utf-8", "replace")
+        if msg == "time series values must all be finite":  # the library's input validation (as_series)
+            raise ValueError(msg)
         raise RuntimeError(f"elastik_b200: {msg}")
 
 

@@ -163,6 +163,35 @@ int launch_plain(Fn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Arg
   return launch_check((const void*)fn);
 }
 
+// Input validation of the host entry points (as_series, series.py:19-28): flag any
+// non-finite value of the uploaded series.
+__global__ void k_check_finite(const double* __restrict__ p, long long n, int* __restrict__ bad) {
+  int b = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b |= !isfinite(p[i]);
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+// queue a finiteness check of n doubles at p, accumulating into *bad (device int)
+int check_finite(const double* p, long long n, int* bad, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const unsigned blocks = (unsigned)std::min<long long>(1184, (n + 255) / 256);
+  return launch_plain(k_check_finite, dim3(blocks), dim3(256), 0, st, p, n, bad);
+}
+const char* const kNonFinite = "time series values must all be finite";
+
+// check two uploaded buffers and wait for the verdict (host entry points only)
+int inputs_finite(const double* a, long long na, const double* b, long long nb, cudaStream_t st) {
+  DBuf dbad;
+  if (dbad.alloc(sizeof(int), st)) return -1;
+  CK(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
+  if (check_finite(a, na, dbad.as<int>(), st) || check_finite(b, nb, dbad.as<int>(), st)) return -1;
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return bad ? fail("%s", kNonFinite) : 0;
+}
+
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = v;
@@ -611,7 +640,7 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   DBuf dq, dqo, dql, dc, dco, dcl, dout;
   if (dq.alloc(sizeof(double) * q_total, st) || dqo.alloc(8 * n_queries, st) || dql.alloc(4 * n_queries, st) ||
       dc.alloc(sizeof(double) * c_total, st) || dco.alloc(8 * std::max<int64_t>(1, n_cands), st) ||
-      dcl.alloc(4 * std::max<int64_t>(1, n_cands), st) || dout.alloc(8 * 5 * n_queries, st))
+      dcl.alloc(4 * std::max<int64_t>(1, n_cands), st) || dout.alloc(8 * (5 * n_queries + 1), st))
     return -1;
   CK(cudaMemcpyAsync(dq.p, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dqo.p, q_off, 8 * n_queries, cudaMemcpyHostToDevice, st));
@@ -622,16 +651,23 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
     CK(cudaMemcpyAsync(dcl.p, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
   }
   int64_t* o = dout.as<int64_t>();
+  int* bad = (int*)(o + 5 * n_queries);  // validation flag rides with the results
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  if (check_finite(dq.as<double>(), q_total, bad, st) || check_finite(dc.as<double>(), c_total, bad, st)) return -1;
   if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
                   dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, dense, o, (double*)(o + n_queries), o + 2 * n_queries,
                   o + 3 * n_queries, o + 4 * n_queries, st))
     return -1;
-  CK(cudaMemcpyAsync(nn_idx, o, 8 * n_queries, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(nn_dist, o + n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(cells, o + 2 * n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(computed, o + 3 * n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(abandoned, o + 4 * n_queries, 8 * n_queries, cudaMemcpyDeviceToHost, st));
+  // one copy back: five result arrays and the validation flag
+  std::vector<int64_t> h(5 * n_queries + 1);
+  CK(cudaMemcpyAsync(h.data(), o, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (*(const int*)(h.data() + 5 * n_queries)) return fail("%s", kNonFinite);
+  std::memcpy(nn_idx, h.data(), 8 * n_queries);
+  std::memcpy(nn_dist, h.data() + n_queries, 8 * n_queries);
+  std::memcpy(cells, h.data() + 2 * n_queries, 8 * n_queries);
+  std::memcpy(computed, h.data() + 3 * n_queries, 8 * n_queries);
+  std::memcpy(abandoned, h.data() + 4 * n_queries, 8 * n_queries);
   return 0;
 }
 
@@ -697,6 +733,14 @@ int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int6
   CK(cudaMemcpyAsync(ds.p, series, sizeof(double) * total, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(doff.p, off, 8 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dlen.p, l32.data(), 4 * n, cudaMemcpyHostToDevice, st));
+  DBuf dbad;
+  if (dbad.alloc(sizeof(int), st)) return -1;
+  CK(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
+  if (check_finite(ds.as<double>(), total, dbad.as<int>(), st)) return -1;
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad) return fail("%s", kNonFinite);
   if (pairwise_dev_impl(spec, variant, ds.as<double>(), doff.as<int64_t>(), dlen.as<int32_t>(), n, mx, dD.as<double>(),
                         cells, st))
     return -1;
@@ -900,6 +944,7 @@ int ek_subseq(const ek_spec* spec, int32_t variant, const double* query, int64_t
   if (dq.alloc(sizeof(double) * lq, st) || dr.alloc(sizeof(double) * n_ref, st)) return -1;
   CK(cudaMemcpyAsync(dq.p, query, sizeof(double) * lq, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dr.p, reference, sizeof(double) * n_ref, cudaMemcpyHostToDevice, st));
+  if (inputs_finite(dq.as<double>(), lq, dr.as<double>(), n_ref, st)) return -1;
   return subseq_dev_impl(spec, variant, dq.as<double>(), lq, dr.as<double>(), n_ref, normalize, best_off, best_dist,
                          cells, computed, abandoned, st);
 }
@@ -915,6 +960,7 @@ int ek_subseq_profile(const ek_spec* spec, const double* query, int64_t lq, cons
   if (dq.alloc(sizeof(double) * lq, st) || dr.alloc(sizeof(double) * n_ref, st)) return -1;
   CK(cudaMemcpyAsync(dq.p, query, sizeof(double) * lq, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dr.p, reference, sizeof(double) * n_ref, cudaMemcpyHostToDevice, st));
+  if (inputs_finite(dq.as<double>(), lq, dr.as<double>(), n_ref, st)) return -1;
   int64_t bo, c, cp, ab;
   double bd;
   return subseq_dev_impl(spec, 0, dq.as<double>(), lq, dr.as<double>(), n_ref, normalize, &bo, &bd, &c, &cp, &ab, st,

@@ -85,15 +85,15 @@ class SearchRecord:
 def _pack(series):
     """Series collection -> (flat float64, offsets, lengths).  A 2-D C-contiguous float64
     array (equal lengths) is used in place -- no copy, so a pinned host array stays
-    pinned for the library's host-to-device copy; anything else goes through as_series
-    per series (the reference's validation) and is concatenated."""
+    pinned for the library's host-to-device copy, and the library checks finiteness on
+    the device; anything else goes through as_series per series (the reference's
+    validation) and is concatenated."""
     if isinstance(series, np.ndarray) and series.ndim == 2 and series.dtype == np.float64 \
             and series.flags.c_contiguous:
         n, length = series.shape
         if n and length < 1:
             raise ValueError("time series must contain at least one value")
-        if n and not np.isfinite(series).all():
-            raise ValueError("time series values must all be finite")
+        # finiteness is checked by the library on the uploaded copy (ValueError, same message)
         return series.reshape(-1), np.arange(n, dtype=np.int64) * length, np.full(n, length, dtype=np.int64)
     return _lib.ragged([as_series(x) for x in series])
 

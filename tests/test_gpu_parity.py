@@ -283,3 +283,28 @@ def test_nn_guard_overflow_redo(gpu, rng, kind):
     r = eko.nn(spec, "eapruned", Q, C, threads=4)
     assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"])
     assert idx[1] == 7 and dist[1] == 0.0
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_inputs_raise(gpu, rng, bad):
+    """as_series' contract (series.py:19-28) for the dense in-place path, where the
+    library checks the uploaded copy: ValueError with the reference's message."""
+    Q = rng.normal(size=(3, 40))
+    C = rng.normal(size=(9, 40))
+    C[4, 17] = bad
+    spec = gpu.DistanceSpec(kind="cdtw", window=4)
+    with pytest.raises(ValueError, match="must all be finite"):
+        gpu.nn_batch(spec, "eapruned", Q, C)
+    with pytest.raises(ValueError, match="must all be finite"):
+        gpu.pairwise(spec, C)
+    Qb = Q.copy()
+    Qb[1, 3] = bad
+    with pytest.raises(ValueError, match="must all be finite"):
+        gpu.nn_batch(spec, "eapruned", Qb, C[:4])
+    ref = rng.normal(size=200)
+    ref[50] = bad
+    with pytest.raises(ValueError, match="must all be finite"):
+        gpu.subsequence_search(Q[0], ref, gpu.SearchConfig(spec=spec))
+    # the library stays usable afterwards
+    idx = gpu.nn_batch(spec, "eapruned", Q, C[:4])[0]
+    assert idx.shape == (3,)
