@@ -394,13 +394,13 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
         const int c2 = __shfl_sync(FULL, ord, i2), l2 = __shfl_sync(FULL, olen, i2);
         // first batch from the prefetched set, which is then refilled for pair i+2
         auto first = [&](float2 (&e)[LB_BATCH]) {
-          const double t = lb_terms<MODE>(QB, 0, lc, e);
+          const float t = lb_terms<MODE>(QB, 0, lc, e);
           if (i + 2 < cnt) lb_load(env + (long long)c2 * lmax, 0, l2, e);
           return t;
         };
-        const double t0 = (i & 1) ? first(envB) : first(envA);
+        const float t0 = (i & 1) ? first(envB) : first(envA);
         const double thr = lb_threshold(cut);
-        evaluate = evaluate && !(t0 > thr) && warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, thr, t0);
+        evaluate = evaluate && !((double)t0 > thr) && warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, thr, t0);
         if (evaluate) {  // survivor: stage its first chunk now
           __syncwarp();
 #pragma unroll

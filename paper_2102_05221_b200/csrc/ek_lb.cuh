@@ -9,10 +9,11 @@
 // Soundness in floating point: every alignment path in the band matches each
 // query point i with some candidate point j, |i-j| <= w, so its cost is at
 // least sum_i dist(q_i, [L_i, U_i]).  Envelopes are stored as floats rounded
-// outward (upper up, lower down), which only widens them.  The computed bound
-// carries at most ~4n ulps of relative error and the DP value at most ~2n ulps
-// (n <= 2^13 terms of non-negative sums), so a candidate is skipped only when
-// the bound exceeds cutoff * (1 + 2^-32), far above both error bounds.
+// outward (upper up, lower down), which only widens them, and the per-pair bound
+// is summed in FP32 rounding toward -inf (lb_terms), so it never exceeds the exact
+// bound.  The DP value carries at most ~2n ulps of relative error (n <= 2^13 terms
+// of non-negative sums), so a candidate is skipped only when the bound exceeds
+// cutoff * (1 + 2^-32), far above that error.
 // (k_envelope, which builds the envelopes, lives in ek_misc.cu.)
 #pragma once
 #include "ek_common.cuh"
@@ -25,21 +26,26 @@ namespace ekb {
 // arrives prefetched, later batches are loaded together so their latency overlaps.
 constexpr int LB_BATCH = 4;
 
+// One batch of LB_Keogh terms in FP32 with every operation rounded toward -inf, so
+// the sum is a guaranteed lower bound of the exact bound: q is widened to
+// [RD(q), RU(q)], the distances to the (outward-rounded) envelope are rounded down,
+// squared and summed rounding down.  The warp total (xor butterfly, so every lane holds
+// the same value) is exact-or-below; lb_threshold's margin covers the DP's rounding.
 template <int MODE>
-__device__ __forceinline__ double lb_terms(const double* qs, int base, int L, const float2 (&e)[LB_BATCH]) {
+__device__ __forceinline__ float lb_terms(const double* qs, int base, int L, const float2 (&e)[LB_BATCH]) {
   const int lane = threadIdx.x & 31;
-  double t = 0.0;
+  float t = 0.f;
 #pragma unroll
   for (int b = 0; b < LB_BATCH; ++b) {
     const int k = base + b * 32 + lane;
     const double qi = k < L ? qs[k] : 0.0;
-    // distance to [lower, upper] (upper >= lower), branch-free
-    double d = fmax(qi - (double)e[b].x, (double)e[b].y - qi);
-    d = fmax(d, 0.0);
-    t += MODE == 0 ? d * d : d;
+    const float qlo = __double2float_rd(qi), qhi = __double2float_ru(qi);
+    // distance to [lower, upper] (upper >= lower), branch-free; neutral interval -> 0
+    const float d = fmaxf(fmaxf(__fsub_rd(qlo, e[b].x), __fsub_rd(e[b].y, qhi)), 0.f);
+    t = __fadd_rd(t, MODE == 0 ? __fmul_rd(d, d) : d);
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+  for (int o = 16; o; o >>= 1) t = __fadd_rd(t, __shfl_xor_sync(FULL, t, o));
   return t;
 }
 
@@ -57,12 +63,12 @@ __device__ __forceinline__ void lb_load(const float2* __restrict__ env, int base
 // Returns true when the candidate must still be evaluated.
 template <int MODE>
 __device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __restrict__ env, int L, double thr,
-                                             double total) {
+                                             float total) {
   for (int base = 32 * LB_BATCH; base < L; base += 32 * LB_BATCH) {
     float2 e[LB_BATCH];
     lb_load(env, base, L, e);
-    total += lb_terms<MODE>(qs, base, L, e);
-    if (total > thr) return false;
+    total = __fadd_rd(total, lb_terms<MODE>(qs, base, L, e));
+    if ((double)total > thr) return false;
   }
   return true;
 }
