@@ -576,6 +576,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   }
   // phase B in two segments: the next-best ranks (where the survivors concentrate)
   // one pair per item for load balance, the rest in items of 8
+  // (64 / 8 measured best on C2 against 32..128 / 4..32: tools/tune_seg.sh history)
   const int kb1 = (int)std::min<int64_t>(ncand, ka + 64);
   const int seg_lo[2] = {ka, kb1}, seg_hi[2] = {kb1, (int)ncand}, seg_k[2] = {1, 8};
   const NNFn fnB = pick_nn(spec->kind, spec->cost_mode, engB);
