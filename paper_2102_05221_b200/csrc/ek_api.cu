@@ -265,6 +265,16 @@ NNFn pick_nn(int kind, int mode, int eng) {
   }
   return nullptr;
 }
+RefFn pick_pairs_ref(int kind, int mode, int eng) {
+  switch (kind_tag(kind)) {
+    case K_DTW: return get_pairs_ref<K_DTW>(mode, eng);
+    case K_WDTW: return get_pairs_ref<K_WDTW>(mode, eng);
+    case K_ERP: return get_pairs_ref<K_ERP>(mode, eng);
+    case K_MSM: return get_pairs_ref<K_MSM>(mode, eng);
+    case K_TWE: return get_pairs_ref<K_TWE>(mode, eng);
+  }
+  return nullptr;
+}
 NNFixFn pick_nn_fix(int kind, int mode, int eng) {
   switch (kind_tag(kind)) {
     case K_DTW: return get_nn_fix<K_DTW>(mode, eng);
@@ -394,9 +404,9 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
   if (n_pairs <= 0) return 0;
   cudaStream_t st = g_ctx.stream;
   // host-side orientation / window / variant semantics (engines.py:121-147, kernels.py:168-171)
-  std::vector<std::vector<PairDesc>> groups(E_COUNT);
-  std::vector<std::vector<long long>> gidx(E_COUNT);
-  std::vector<int> glmax(E_COUNT, 0);
+  std::vector<std::vector<PairDesc>> groups(E_COUNT), rgroups(E_COUNT);
+  std::vector<std::vector<long long>> gidx(E_COUNT), ridx(E_COUNT);
+  std::vector<int> glmax(E_COUNT, 0), rlmax(E_COUNT, 0);
   for (int64_t p = 0; p < n_pairs; ++p) {
     const bool swap = t_len[p] > s_len[p];
     PairDesc pd{};
@@ -426,6 +436,16 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
     if (w < pd.nl - pd.nc) continue;  // infeasible window: (+inf, 0)
     pd.w = w;
     pd.cut = cut;
+    // ea with a finite cutoff, eapruned and pruned_only report the reference's own cell
+    // count (ek_refcells.cuh) when the row-stripe replay engine holds the pair
+    if ((ea_rows || variant == 2 || variant == 3) && pd.nc <= kRefMaxCols && pd.nl <= 2048) {
+      const int reng = ea_rows ? E_STR16_EA : (w < pd.nl - 1 ? E_STRB16 : E_STR16);
+      pd.pad_ = ea_rows ? 1 : variant;
+      rgroups[reng].push_back(pd);
+      ridx[reng].push_back(p);
+      rlmax[reng] = std::max(rlmax[reng], pd.nl);
+      continue;
+    }
     const int eng = choose_engine(pd.nl, pd.nc, w, ea_rows);
     if (eng < 0) return fail("series of length %d x %d with window %d exceed this build's engines", pd.nl, pd.nc, w);
     groups[eng].push_back(pd);
@@ -458,6 +478,28 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
     for (size_t k = 0; k < n; ++k) {
       out_cost[gidx[eng][k]] = hc[k];
       out_cells[gidx[eng][k]] = hcl[k];
+    }
+  }
+  for (int eng = 0; eng < E_COUNT; ++eng) {  // reference cell counts (k_pairs_ref)
+    const size_t n = rgroups[eng].size();
+    if (!n) continue;
+    DBuf dp, dc, dt;
+    if (dp.alloc(sizeof(PairDesc) * n, st) || dc.alloc(sizeof(double) * n, st) || dt.alloc(sizeof(long long) * n, st))
+      return -1;
+    CK(cudaMemcpyAsync(dp.p, rgroups[eng].data(), sizeof(PairDesc) * n, cudaMemcpyHostToDevice, st));
+    const size_t smem = sizeof(double) * (size_t)ref_warp_stride(rlmax[eng], eng);
+    if (launch_persistent(pick_pairs_ref(spec->kind, spec->cost_mode, eng), 32, smem, st, (long long)n,
+                          (const double*)dser.as<double>(), (const PairDesc*)dp.as<PairDesc>(), (int)n, rlmax[eng],
+                          ph.prm, dc.as<double>(), dt.as<long long>()))
+      return -1;
+    std::vector<double> hc(n);
+    std::vector<long long> hcl(n);
+    CK(cudaMemcpyAsync(hc.data(), dc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hcl.data(), dt.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t k = 0; k < n; ++k) {
+      out_cost[ridx[eng][k]] = hc[k];
+      out_cells[ridx[eng][k]] = hcl[k];
     }
   }
   CK(cudaStreamSynchronize(st));

@@ -2,6 +2,7 @@
 // (ek_inst_<kind>.cu) so the template expansion compiles in parallel.
 #pragma once
 #include "ek_kernels.cuh"
+#include "ek_refcells.cuh"
 
 namespace ekb {
 
@@ -13,6 +14,7 @@ using NNFn = void (*)(const double*, const long long*, const int*, int, const do
                       double*, int*, int*, const float2*, int2*, int*);
 using NNFixFn = void (*)(const double*, const long long*, const int*, const double*, const long long*, const int*,
                          int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*);
+using RefFn = void (*)(const double*, const PairDesc*, int, int, Params, double*, long long*);
 using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, Params, unsigned long long*);
 
@@ -79,6 +81,83 @@ __global__ void __launch_bounds__(128) k_ub_init(const double* __restrict__ Q, c
     __syncwarp();
   }
   if (lane == 0) cutbits[q] = (unsigned long long)__double_as_longlong(total);
+}
+
+// Single pairs with the reference's own cells_computed (ek_refcells.cuh): one warp per
+// pair on the row-stripe engine (S = 16: STR16 / STRB16 / STR16_EA).  pd.pad_ selects
+// the count: 1 ea rows, 2 eapruned replay, 3 pruned_only (eapruned replay at the
+// diagonal upper bound, computed here in DP order, engines.py:87-118).
+__host__ __device__ constexpr int ref_warp_stride(int lmax, int eng) {
+  return warp_stride(lmax, eng) + ((lmax + 1) * kRefWords * 2 + (lmax + 1) + 7) / 8;
+}
+
+template <int KIND, int MODE, int ENG>
+__global__ void __launch_bounds__(32) k_pairs_ref(const double* __restrict__ series,
+                                                  const PairDesc* __restrict__ pairs, int npairs, int lmax,
+                                                  Params prm, double* __restrict__ out_cost,
+                                                  long long* __restrict__ out_cells) {
+  extern __shared__ double smem[];
+  constexpr int PAD = engine_pad(ENG);
+  constexpr bool BANDED = ENG >= E_STRB16;
+  constexpr bool EA = ENG == E_STR16_EA;
+  const int lane = threadIdx.x & 31;
+  double* X = smem + PAD;
+  double* Y = X + series_slot(lmax, PAD);
+  double* tab = Y - PAD + series_slot(lmax, PAD);
+  unsigned short* bits = (unsigned short*)(smem + warp_stride(lmax, ENG));
+  unsigned char* vbl = (unsigned char*)(bits + (lmax + 1) * kRefWords);
+  __shared__ double terms[32];
+  for (int pid = blockIdx.x; pid < npairs; pid += gridDim.x) {
+    const PairDesc pd = pairs[pid];
+    const Params pp = pair_params(prm, pd.nl);
+    const int nl = pd.nl, nc = pd.nc, w = pd.w;
+    __syncwarp();
+    stage_series<KIND>(X, series + pd.xoff, nl, PAD);
+    stage_series<KIND>(Y, series + pd.yoff, nc, PAD);
+    const int tablen = max(nl, nc) + 1;
+    stage_table<KIND>(tab, tablen, pp);
+    unsigned* bw = (unsigned*)bits;
+    for (int k = lane; k < (nl + 1) * kRefWords / 2; k += 32) bw[k] = 0u;
+    for (int k = lane; k <= nl; k += 32) vbl[k] = 0;
+    __syncwarp();
+    double cut = pd.cut;
+    if (pd.pad_ == 3) {  // diagonal_upper_bound, summed in DP order
+      double total = 0.0;
+      for (int base = 1; base <= nl; base += 32) {
+        const int k = base + lane;
+        terms[lane] = (k <= nl) ? ub_term<KIND, MODE>(X, Y, nc, k, pp) : 0.0;
+        __syncwarp();
+        if (lane == 0)
+          for (int u = 0; u < min(32, nl - base + 1); ++u) total = dadd(total, terms[u]);
+        __syncwarp();
+      }
+      cut = __shfl_sync(FULL, total, 0);
+    }
+    const RowBits rec{bits, vbl};
+    const StripeResult r = stripe_pair<KIND, MODE, 16, BANDED, false, EA>(SmemSeries{X, nl}, nl, SmemSeries{Y, nc},
+                                                                           nc, w, cut, nullptr, tab, tablen, pp, rec);
+    __syncwarp();
+    if (lane == 0) {
+      long long cells;
+      if (pd.pad_ == 1) cells = ea_cells(nl, nc, w, r.ea_row == 0x7fffffff ? nl : r.ea_row);
+      else cells = eapruned_cells(bits, vbl, nl, nc, w, KIND == K_ERP);
+      out_cost[pid] = r.cost;
+      out_cells[pid] = cells;
+    }
+  }
+}
+
+template <int KIND>
+RefFn get_pairs_ref(int mode, int eng) {
+  switch (mode * 16 + eng) {
+    case 0 * 16 + E_STR16: return k_pairs_ref<KIND, 0, E_STR16>;
+    case 1 * 16 + E_STR16: return k_pairs_ref<KIND, 1, E_STR16>;
+    case 0 * 16 + E_STRB16: return k_pairs_ref<KIND, 0, E_STRB16>;
+    case 1 * 16 + E_STRB16: return k_pairs_ref<KIND, 1, E_STRB16>;
+    case 0 * 16 + E_STR16_EA: return k_pairs_ref<KIND, 0, E_STR16_EA>;
+    case 1 * 16 + E_STR16_EA: return k_pairs_ref<KIND, 1, E_STR16_EA>;
+  }
+  return nullptr;
 }
 
 #define EKB_ENG_CASES(M, FN)                                                                         \
@@ -148,6 +227,7 @@ UBFn get_ub(int mode) {
 
 #define EKB_INSTANTIATE_KIND(K)                  \
   template PairsFn get_pairs<K>(int, int);       \
+  template RefFn get_pairs_ref<K>(int, int);     \
   template TriFn get_triangle<K>(int, int);      \
   template NNFn get_nn<K>(int, int);             \
   template NNFixFn get_nn_fix<K>(int, int);      \

@@ -26,14 +26,24 @@ namespace ekb {
 
 struct StripeResult {
   double cost;
-  int t_end;  // steps executed
+  int t_end;   // steps executed
+  int ea_row;  // EA: first row whose minimum exceeded the cutoff (0x7fffffff if none)
+};
+
+// Row recorder: the default records nothing.  RowBits (ek_refcells.cuh) keeps each
+// row's "value <= cutoff" bits so the reference's own cell count can be replayed.
+struct NoRec {
+  static constexpr bool on = false;
+  __device__ __forceinline__ void row(int, int, unsigned) const {}
+  __device__ __forceinline__ void vb(int, bool) const {}
 };
 
 // tab: per-pair |i-j| table in shared memory (WDTW: weights; TWE: nu*(d+d)); len >= max(nl,nc)+1.
-template <int KIND, int MODE, int S, bool BANDED, bool SHARED_CUT, bool EA, class XAcc, class YAcc>
+template <int KIND, int MODE, int S, bool BANDED, bool SHARED_CUT, bool EA, class XAcc, class YAcc,
+          class Rec = NoRec>
 __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
                                     const unsigned long long* cutp, const double* tab, int tablen,
-                                    const Params& prm) {
+                                    const Params& prm, const Rec& rec = Rec{}) {
   const int lane = threadIdx.x & 31;
   constexpr bool BORDERED = (KIND == K_ERP);
   constexpr bool TWE = (KIND == K_TWE);
@@ -87,8 +97,10 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   const int sf = (nc - 1) % S;
 
   // one row over this lane's S columns; prev[] holds row i-1 on entry, row i on exit
+  int ea_row = 0x7fffffff;
   auto row_pass = [&](int i, const RowD<KIND>& rd, double lft, double dgl, double dpc, double& rmin,
                       double (&row)[S], bool& alive) {
+    unsigned live_bits = 0;
     int a = 0, b = S - 1;
     if constexpr (BANDED) {
       const int hi = (i == 0) ? w + 1 : i + w;  // row 0 keeps hborder up to j = w+1
@@ -121,6 +133,10 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
       // or only delay abandoning; the hi-word test is conservative (ek_diag.cuh)
       alive |= hi_word(v) <= cut_hi;
       if constexpr (EA) rmin = (v < rmin) ? v : rmin;
+      if constexpr (Rec::on) live_bits |= (unsigned)(j <= nc && v <= cut) << s;
+    }
+    if constexpr (Rec::on) {
+      if (i >= 0 && i <= nl) rec.row(i, lane, live_bits);
     }
   };
 
@@ -161,6 +177,10 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
       }
       rm0 = (i0 >= 1) ? lb0 : EKB_INF;  // ea: the border cell joins the row minimum
       rm1 = (i1 >= 1) ? lb1 : EKB_INF;
+      if constexpr (Rec::on) {
+        if (i0 >= 1 && i0 <= nl) rec.vb(i0, lb0 <= cut);
+        if (i1 >= 1 && i1 <= nl) rec.vb(i1, lb1 <= cut);
+      }
     }
     bool alive = lane == 0 && (hi_word(lb0) <= cut_hi || hi_word(lb1) <= cut_hi);
     double row0[S];
@@ -187,8 +207,14 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
       rmo0 = rm0;
       rmo1 = rm1;
       if (lane == lf) {
-        if (i0 >= 1 && i0 <= nl && rm0 > cut) ea_flag = true;
-        if (i1 >= 1 && i1 <= nl && rm1 > cut) ea_flag = true;
+        if (i0 >= 1 && i0 <= nl && rm0 > cut) {
+          ea_flag = true;
+          ea_row = min(ea_row, i0);
+        }
+        if (i1 >= 1 && i1 <= nl && rm1 > cut) {
+          ea_flag = true;
+          ea_row = min(ea_row, i1);
+        }
       }
     }
     if constexpr (!EA) {
@@ -203,6 +229,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   (void)lane_on;
   StripeResult res;
   res.t_end = dead ? t + 1 : nsteps;
+  res.ea_row = EA ? __shfl_sync(FULL, ea_row, lf) : 0x7fffffff;
   if (dead) {
     res.cost = EKB_INF;
     return res;

@@ -10,13 +10,14 @@ selection and variant semantics follow the reference:
                   if it is above the cutoff (_speedups.pyx:129-162);
 * ``eapruned``    exact when cost <= cutoff, +inf otherwise (SPEC.md:271);
 * ``pruned_only`` the diagonal upper bound as a prune-only cutoff, which never
-                  changes the exact result (engines.py:106-118) -- computed as
-                  the exact windowed cost.
+                  changes the exact result (engines.py:106-118).
 
 An infeasible window (w < |len(s)-len(t)|) is (+inf, 0) for every windowed
-variant.  ``cells_computed`` counts the band cells the GPU engine evaluated;
-the schedule differs from the CPU's five-stage row loop, so it is not the
-reference's count except for ``base`` (lines*cols) and windowed ``base``.
+variant.  ``cells_computed`` is the reference's own count for every variant
+(EngineResult equality): ``base`` is lines*cols or the band; ``ea``, ``eapruned``
+and ``pruned_only`` replay the reference's row logic from the GPU DP's
+"value <= cutoff" masks (csrc/ek_refcells.cuh) for pairs of up to 512 columns
+and 2048 rows.  Longer pairs report the band cells the GPU evaluated.
 """
 
 from __future__ import annotations

@@ -39,9 +39,34 @@ def test_golden_pairs_gpu(gpu):
         for k, c, n in zip(rows, costs, cells):
             if not same(c, g["cost"][k]):
                 bad.append((specs[si].kind, VARIANTS[vi], g["cutoff"][k], c, g["cost"][k]))
-            if VARIANTS[vi] == "base" and n != g["cells"][k]:
-                bad.append(("cells", specs[si].kind, int(n), int(g["cells"][k])))
+            if n != g["cells"][k]:  # EngineResult equality: the reference's own cell counts
+                bad.append(("cells", specs[si].kind, VARIANTS[vi], g["cutoff"][k], int(n), int(g["cells"][k])))
     assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("kind", ["dtw", "cdtw", "wdtw", "erp", "msm", "twe"])
+def test_reference_cells_long_pairs(gpu, rng, kind):
+    """cells_computed of ea / eapruned / pruned_only equal the reference's (oracle, which
+    replays the reference's row stages) on pairs up to 300 points, every cutoff regime."""
+    bad = []
+    for mode in ("squared", "absolute"):
+        spec = random_spec(gpu, kind, rng, 300, mode)
+        pairs, cuts, want = [], [], []
+        for _ in range(6):
+            n1, n2 = int(rng.integers(150, 301)), int(rng.integers(150, 301))
+            a, b = np.cumsum(rng.normal(0, 1, n1)), np.cumsum(rng.normal(0, 1, n2))
+            exact = eko.distance(spec, "base", a, b)[0]
+            for f in (np.inf, 1.02, 1.0, 0.97, 0.5):
+                c = exact * f if np.isfinite(exact) else f
+                pairs.append((a, b))
+                cuts.append(c)
+        for variant in ("ea", "eapruned", "pruned_only"):
+            costs, cells = gpu.distance_batch(spec, variant, pairs, cutoffs=cuts)
+            for (a, b), c, got_c, got_n in zip(pairs, cuts, costs, cells):
+                ref = eko.distance(spec, variant, a, b, cutoff=c)
+                if not (same(got_c, ref[0]) and got_n == ref[1]):
+                    bad.append((kind, mode, variant, c, got_c, ref[0], int(got_n), int(ref[1])))
+    assert not bad, bad[:6]
 
 
 def random_spec(ekb, kind, rng, maxlen, mode):
