@@ -537,7 +537,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
   const long long npairs = (long long)nq * ncand;
-  DBuf dord, dkeys, dout, dtend, dcut, dcnt, denv;
+  DBuf dord, dkeys, dout, dtend, dcut, dcnt, denv, denvq;
   if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dout.alloc(sizeof(double) * (size_t)npairs, st) ||
       dtend.alloc(sizeof(int) * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
       dcnt.alloc(sizeof(int) * 16, st))
@@ -601,7 +601,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
                           (const int*)dord.as<int>(), 0, ka, 1, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>(),
-                          (const float2*)nullptr, dovf.as<int2>(), ovf_count))
+                          (const float2*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count))
       return -1;
   }
   mark(st, "nn_phaseA");
@@ -614,6 +614,11 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                      (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>()))
       return -1;
     env = denv.as<float2>();
+    // query envelopes for the reverse bound of the survivors (lb_keogh2's second order)
+    if (denvq.alloc(sizeof(float2) * (size_t)L * nq, st)) return -1;
+    if (launch_plain(k_envelope, dim3((unsigned)nq), dim3(256), sizeof(double) * 5 * (size_t)L, st, dQ,
+                     (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>()))
+      return -1;
     mark(st, "envelope");
   }
   // phase B in two segments: the next-best ranks (where the survivors concentrate)
@@ -631,7 +636,8 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(),
                           seg_lo[sgi], seg_hi[sgi], K, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
-                          dcnt.as<int>() + 2 + 2 * sgi, env, dovf.as<int2>(), ovf_count))
+                          dcnt.as<int>() + 2 + 2 * sgi, env, (const float2*)denvq.as<float2>(), dovf.as<int2>(),
+                          ovf_count))
       return -1;
   }
   mark(st, "nn_phaseB");

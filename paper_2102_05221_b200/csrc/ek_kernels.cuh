@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
                                             int K, int win, int lmax, Params prm, int share,
                                             unsigned long long* cutbits, double* __restrict__ out,
                                             int* __restrict__ tend_out, int* __restrict__ counter,
-                                            const float2* __restrict__ env, int2* __restrict__ ovf_list,
-                                            int* __restrict__ ovf_count) {
+                                            const float2* __restrict__ env, const float2* __restrict__ envq,
+                                            int2* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
   constexpr int PF = kChunk / 32;
@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
       const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
       const int w = win < 0 ? nl : win;
       bool evaluate = w >= nl - nc;
+      int staged = min(kChunk, lc);  // candidate elements already in CB
       if (use_lb) {
         const int i2 = min(i + 2, cnt - 1);
         const int c2 = __shfl_sync(FULL, ord, i2), l2 = __shfl_sync(FULL, olen, i2);
@@ -401,15 +402,13 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
         const float t0 = (i & 1) ? first(envB) : first(envA);
         const double thr = lb_threshold(cut);
         evaluate = evaluate && !((double)t0 > thr) && warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, thr, t0);
-        if (evaluate) {  // survivor: stage its first chunk now
+        if (evaluate) {  // survivor: stage the whole candidate, then the reverse bound
           __syncwarp();
-#pragma unroll
-          for (int u = 0; u < PF; ++u)
-            if (u * 32 + lane < lc) CB[u * 32 + lane] = __ldg(csrc + u * 32 + lane);
-          if (lc != cb_len) {
-            stage_pads<KIND>(CB, lc, PAD, 0.0);
-            cb_len = lc;
-          }
+          stage_series<KIND>(CB, csrc, lc, PAD);
+          cb_len = lc;
+          staged = lc;
+          __syncwarp();
+          evaluate = warp_lb_reverse<MODE>(CB, envq + (long long)q * lmax, lc, thr);
         }
       } else {
         __syncwarp();
@@ -432,7 +431,7 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
       int tend = 0;
       if (evaluate) {
         const Params pp = pair_params(prm, nl);
-        LazyCand ld{CB, csrc, lc, min(kChunk, lc), !q_rows};
+        LazyCand ld{CB, csrc, lc, staged, !q_rows};
         const int tablen = max(nl, nc) + 1;
         if constexpr (!engine_is_diag(ENG)) {
           ld.load_to(lc);  // the stripe engine reads all columns up front

@@ -73,6 +73,22 @@ __device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __r
   return true;
 }
 
+// The reverse bound LB_Keogh(candidate, envelope(query)) (lb_keogh2's second order,
+// lower_bounds.py:87-98) over a candidate staged in shared memory; the query
+// envelope comes from global memory.  true when the pair must still be evaluated.
+template <int MODE>
+__device__ __forceinline__ bool warp_lb_reverse(const double* cs, const float2* __restrict__ envq, int L,
+                                                double thr) {
+  float total = 0.f;
+  for (int base = 0; base < L; base += 32 * LB_BATCH) {
+    float2 e[LB_BATCH];
+    lb_load(envq, base, L, e);
+    total = __fadd_rd(total, lb_terms<MODE>(cs, base, L, e));
+    if ((double)total > thr) return false;
+  }
+  return true;
+}
+
 // bound > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header)
 __device__ __forceinline__ double lb_threshold(double cut) { return cut * (1.0 + 2.3283064365386963e-10); }
 
