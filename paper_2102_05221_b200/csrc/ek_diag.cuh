@@ -174,13 +174,17 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   // so sliding costs no register moves; otherwise the windows shift in place.
   constexpr bool ROT = (H <= EKB_ROT_MAX_H);
   constexpr int U = ROT ? H * (H + 1) : 1;
+  // liveness accumulates over two double steps and is voted on every second one:
+  // four consecutive dead anti-diagonals still cut every path, and the warp vote
+  // (and the guard test: a path needs >= P/2 double steps to cross a P-diagonal guard
+  // lane) runs half as often
+  bool alive = false;
   auto dstep = [&](auto S_) -> bool {
     constexpr int S = decltype(S_)::value;
     constexpr int rx = ROT ? S % (H + 1) : 0;
     constexpr int ry = ROT ? (H - S % H) % H : 0;
     auto XW = [&](int k) -> RowD<KIND>& { return xw[(k + rx) % (H + 1)]; };
     auto YW = [&](int m) -> ColD<KIND>& { return yw[(m + ry) % H]; };
-    bool alive = false;
     // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
     double tin = __shfl_up_sync(FULL, val[P - 1], 1);
     if constexpr (BORDERED) {
@@ -222,19 +226,23 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
     if (t + 1 >= Tf) return true;
-    if constexpr (GUARD) {
-      const unsigned live = __ballot_sync(FULL, alive);
-      if (!live) {
+    const bool vote = ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1;
+    if (vote) {
+      if constexpr (GUARD) {
+        const unsigned live = __ballot_sync(FULL, alive);
+        if (!live) {
+          dead = true;
+          return true;
+        }
+        if (live & guard) {
+          ovf = true;
+          return true;
+        }
+      } else if (!__any_sync(FULL, alive)) {
         dead = true;
         return true;
       }
-      if (live & guard) {
-        ovf = true;
-        return true;
-      }
-    } else if (!__any_sync(FULL, alive)) {
-      dead = true;
-      return true;
+      alive = false;
     }
     // ---- slide the register windows by one element ----
     t += 2;
