@@ -395,20 +395,22 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
         const int c2 = __shfl_sync(FULL, ord, i2), l2 = __shfl_sync(FULL, olen, i2);
         // first batch from the prefetched set, which is then refilled for pair i+2
         auto first = [&](float2 (&e)[LB_BATCH]) {
-          const float t = lb_terms<MODE>(QB, 0, lc, e);
+          const float t = lb_lane_terms<MODE>(QB, 0, lc, e);
           if (i + 2 < cnt) lb_load(env + (long long)c2 * lmax, 0, l2, e);
           return t;
         };
         const float t0 = (i & 1) ? first(envB) : first(envA);
-        const double thr = lb_threshold(cut);
-        evaluate = evaluate && !((double)t0 > thr) && warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, thr, t0);
+        const LBScale sc = lb_scale(lb_threshold(cut));
+        const unsigned tot0 = lb_reduce(t0, sc);
+        evaluate = evaluate && !sc.all && tot0 <= sc.T &&
+                   warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, sc, tot0);
         if (evaluate) {  // survivor: stage the whole candidate, then the reverse bound
           __syncwarp();
           stage_series<KIND>(CB, csrc, lc, PAD);
           cb_len = lc;
           staged = lc;
           __syncwarp();
-          evaluate = warp_lb_reverse<MODE>(CB, envq + (long long)q * lmax, lc, thr);
+          evaluate = warp_lb_reverse<MODE>(CB, envq + (long long)q * lmax, lc, sc);
         }
       } else {
         __syncwarp();

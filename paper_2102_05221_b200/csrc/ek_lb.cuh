@@ -10,7 +10,7 @@
 // query point i with some candidate point j, |i-j| <= w, so its cost is at
 // least sum_i dist(q_i, [L_i, U_i]).  Envelopes are stored as floats rounded
 // outward (upper up, lower down), which only widens them, and the per-pair bound
-// is summed in FP32 rounding toward -inf (lb_terms), so it never exceeds the exact
+// is summed in FP32 rounding toward -inf (lb_lane_terms, totals in fixed point: lb_reduce), so it never exceeds the exact
 // bound.  The DP value carries at most ~2n ulps of relative error (n <= 2^13 terms
 // of non-negative sums), so a candidate is skipped only when the bound exceeds
 // cutoff * (1 + 2^-32), far above that error.
@@ -29,10 +29,9 @@ constexpr int LB_BATCH = 4;
 // One batch of LB_Keogh terms in FP32 with every operation rounded toward -inf, so
 // the sum is a guaranteed lower bound of the exact bound: q is widened to
 // [RD(q), RU(q)], the distances to the (outward-rounded) envelope are rounded down,
-// squared and summed rounding down.  The warp total (xor butterfly, so every lane holds
-// the same value) is exact-or-below; lb_threshold's margin covers the DP's rounding.
+// squared and summed rounding down.  Returns this lane's partial sum.
 template <int MODE>
-__device__ __forceinline__ float lb_terms(const double* qs, int base, int L, const float2 (&e)[LB_BATCH]) {
+__device__ __forceinline__ float lb_lane_terms(const double* qs, int base, int L, const float2 (&e)[LB_BATCH]) {
   const int lane = threadIdx.x & 31;
   float t = 0.f;
 #pragma unroll
@@ -44,9 +43,39 @@ __device__ __forceinline__ float lb_terms(const double* qs, int base, int L, con
     const float d = fmaxf(fmaxf(__fsub_rd(qlo, e[b].x), __fsub_rd(e[b].y, qhi)), 0.f);
     t = __fadd_rd(t, MODE == 0 ? __fmul_rd(d, d) : d);
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) t = __fadd_rd(t, __shfl_xor_sync(FULL, t, o));
   return t;
+}
+
+// Warp totals in fixed point: each lane's partial is scaled by a power of two s and
+// truncated (clamped at 2^26, so 32 lanes cannot overflow), then one integer
+// __reduce_add_sync replaces the five-step float butterfly.  s puts the threshold in
+// [2^20, 2^21): T = ceil(RU(thr) * s) exactly, every other step rounds down, so a total
+// above T proves the exact bound exceeds thr; truncation only weakens the bound.
+struct LBScale {
+  float s;     // multiplier (0: never prune)
+  unsigned T;  // scaled threshold
+  bool all;    // thr < 0: every pair is pruned (nothing is <= a negative cutoff)
+};
+__device__ __forceinline__ LBScale lb_scale(double thr) {
+  LBScale r;
+  r.all = thr < 0.0;
+  const float tf = __double2float_ru(thr);
+  const int ex = ((__float_as_int(tf) >> 23) & 0xff) - 127;  // tf in [2^ex, 2^(ex+1)) for normal tf
+  if (!(thr >= 0.0) || !(tf < __int_as_float(0x7f800000))) {
+    r.s = 0.f;  // +inf / NaN threshold: never prune
+    r.T = 0xffffffffu;
+  } else if (tf < 0x1p-100f) {  // (near) zero threshold: any term above 2^-100 prunes
+    r.s = 0x1p100f;
+    r.T = 0u;
+  } else {
+    r.s = __int_as_float((147 - ex) << 23);  // 2^(20 - ex)
+    r.T = __float2uint_ru(tf * r.s);         // exact product, in [2^20, 2^21)
+  }
+  return r;
+}
+__device__ __forceinline__ unsigned lb_reduce(float t, const LBScale& sc) {
+  const unsigned q = __float2uint_rd(fminf(__fmul_rd(t, sc.s), 67108864.0f));  // 2^26
+  return __reduce_add_sync(FULL, q);
 }
 
 // out-of-range points load the neutral interval [-inf, +inf]
@@ -59,16 +88,16 @@ __device__ __forceinline__ void lb_load(const float2* __restrict__ env, int base
   }
 }
 
-// Continues the test past the prefetched first batch (running total `total`).
+// Continues the test past the prefetched first batch (running scaled total `total`).
 // Returns true when the candidate must still be evaluated.
 template <int MODE>
-__device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __restrict__ env, int L, double thr,
-                                             float total) {
+__device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __restrict__ env, int L,
+                                             const LBScale& sc, unsigned total) {
   for (int base = 32 * LB_BATCH; base < L; base += 32 * LB_BATCH) {
     float2 e[LB_BATCH];
     lb_load(env, base, L, e);
-    total = __fadd_rd(total, lb_terms<MODE>(qs, base, L, e));
-    if ((double)total > thr) return false;
+    total += lb_reduce(lb_lane_terms<MODE>(qs, base, L, e), sc);
+    if (total > sc.T) return false;
   }
   return true;
 }
@@ -78,13 +107,13 @@ __device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __r
 // envelope comes from global memory.  true when the pair must still be evaluated.
 template <int MODE>
 __device__ __forceinline__ bool warp_lb_reverse(const double* cs, const float2* __restrict__ envq, int L,
-                                                double thr) {
-  float total = 0.f;
+                                                const LBScale& sc) {
+  unsigned total = 0;
   for (int base = 0; base < L; base += 32 * LB_BATCH) {
     float2 e[LB_BATCH];
     lb_load(envq, base, L, e);
-    total = __fadd_rd(total, lb_terms<MODE>(cs, base, L, e));
-    if ((double)total > thr) return false;
+    total += lb_reduce(lb_lane_terms<MODE>(cs, base, L, e), sc);
+    if (total > sc.T) return false;
   }
   return true;
 }
