@@ -599,7 +599,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   if (ka > 0) {
     if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
-                          (const int*)dord.as<int>(), 0, ka, 1, win, (int)max_len, ph.prm, (int)share,
+                          (const int*)dord.as<int>(), 0, ka, ka, 1, 1, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>(),
                           (const float2*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count))
       return -1;
@@ -621,23 +621,29 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       return -1;
     mark(st, "envelope");
   }
-  // phase B in two segments: the next-best ranks (where the survivors concentrate)
-  // one pair per item for load balance, the rest in items of 8
-  // (64 / 8 measured best on C2 against 32..128 / 4..32: tools/tune_seg.sh history)
+  // phase B, one launch of two segments: the next-best 64 ranks (where the survivors
+  // concentrate) one pair per item for load balance, the rest in items of 8
+  // (64 / 8 measured best on C2 against 32..128 / 4..32)
   const int kb1 = (int)std::min<int64_t>(ncand, ka + 64);
-  const int seg_lo[2] = {ka, kb1}, seg_hi[2] = {kb1, (int)ncand}, seg_k[2] = {1, 8};
   const NNFn fnB = pick_nn(spec->kind, spec->cost_mode, engB);
   const size_t smemB = pair_smem(max_len, engB, wpb);
-  for (int sgi = 0; sgi < 2; ++sgi) {
-    if (seg_lo[sgi] >= seg_hi[sgi]) continue;
-    const int K = seg_k[sgi];
-    const long long items = (long long)nq * ((seg_hi[sgi] - seg_lo[sgi] + K - 1) / K);
+  // With the LB pre-test most pairs are cheap and the first segment's tail of long DPs
+  // would idle the GPU, so both segments share one launch.  Without it (MSM, TWE, ...)
+  // every pair runs the DP and the second segment waits for the first one's cutoffs.
+  // (a single launch needs k_nn's TWO_SEG, i.e. the dtw kernels)
+  const bool one_launch = use_lb && kind_tag(spec->kind) == K_DTW;
+  const int seg_lo[2] = {ka, kb1}, seg_mid[2] = {kb1, (int)ncand};
+  for (int sgi = 0; sgi < (one_launch ? 1 : 2); ++sgi) {
+    const int lo = one_launch ? ka : seg_lo[sgi], mid = one_launch ? kb1 : seg_mid[sgi];
+    const int hi = one_launch ? (int)ncand : mid;
+    const int K1 = (one_launch || sgi == 0) ? 1 : 8;
+    if (lo >= hi) continue;
+    const long long items = (long long)nq * ((mid - lo + K1 - 1) / K1 + (hi - mid + 7) / 8);
     if (launch_persistent(fnB, 32 * wpb, smemB, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
-                          (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(),
-                          seg_lo[sgi], seg_hi[sgi], K, win, (int)max_len, ph.prm, (int)share,
-                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
-                          dcnt.as<int>() + 2 + 2 * sgi, env, (const float2*)denvq.as<float2>(), dovf.as<int2>(),
-                          ovf_count))
+                          (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), lo, mid,
+                          hi, K1, 8, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
+                          dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2 + 2 * sgi, env,
+                          (const float2*)denvq.as<float2>(), dovf.as<int2>(), ovf_count))
       return -1;
   }
   mark(st, "nn_phaseB");

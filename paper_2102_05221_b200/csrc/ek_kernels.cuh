@@ -313,8 +313,8 @@ template <int KIND, int MODE, int ENG>
 __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const long long* __restrict__ qoff,
                                             const int* __restrict__ qlen, int nq, const double* __restrict__ C,
                                             const long long* __restrict__ coff, const int* __restrict__ clen,
-                                            int ncand, const int* __restrict__ order, int rank_lo, int rank_hi,
-                                            int K, int win, int lmax, Params prm, int share,
+                                            int ncand, const int* __restrict__ order, int rank_lo, int rank_mid,
+                                            int rank_hi, int K1, int K2, int win, int lmax, Params prm, int share,
                                             unsigned long long* cutbits, double* __restrict__ out,
                                             int* __restrict__ tend_out, int* __restrict__ counter,
                                             const float2* __restrict__ env, const float2* __restrict__ envq,
@@ -327,9 +327,14 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
   double* QB = smem + wib * warp_stride(lmax, ENG) + PAD;
   double* CB = QB + series_slot(lmax, PAD);
   double* tab = CB - PAD + series_slot(lmax, PAD);
-  const int span = rank_hi - rank_lo;
-  const int rounds = (span + K - 1) / K;
-  const long long nitems = (long long)rounds * nq;
+  // two segments in one launch: ranks [rank_lo, rank_mid) in items of K1, then
+  // [rank_mid, rank_hi) in items of K2, each round-major over the queries, so warps
+  // that finish the first segment's tail start on the second at once.  Only the
+  // dtw/cdtw LB path uses a second segment; the other kinds keep the one-segment item
+  // logic (rank_mid == rank_hi), whose code they are register-tuned on.
+  constexpr bool TWO_SEG = (KIND == K_DTW);
+  const long long items1 = (long long)((rank_mid - rank_lo + K1 - 1) / K1) * nq;
+  const long long nitems = TWO_SEG ? items1 + (long long)((rank_hi - rank_mid + K2 - 1) / K2) * nq : items1;
   // LB_Keogh pre-test (dtw/cdtw, equal lengths): env != nullptr
   const bool use_lb = env != nullptr;
   int staged_q = -1, cb_len = -1;
@@ -338,10 +343,14 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
     if (lane == 0) it = (long long)atomicAdd((unsigned long long*)counter, 1ULL);
     it = __shfl_sync(FULL, it, 0);
     if (it >= nitems) break;
-    const int q = (int)(it % nq);
-    const int r = (int)(it / nq);
+    const bool first_seg = !TWO_SEG || it < items1;
+    const long long is = first_seg ? it : it - items1;
+    const int q = (int)(is % nq);
+    const int r = (int)(is / nq);
     const int lq = qlen[q];
-    const int k_lo = rank_lo + r * K, k_hi = min(k_lo + K, rank_hi);
+    const int K = first_seg ? K1 : K2;
+    const int k_lo = (first_seg ? rank_lo : rank_mid) + r * K;
+    const int k_hi = min(k_lo + K, first_seg ? rank_mid : rank_hi);
     const int cnt = k_hi - k_lo;
     // this item's candidates and their metadata, one per lane (K <= 32)
     const int ord = lane < cnt ? order[(long long)q * ncand + k_lo + lane] : 0;

@@ -10,7 +10,7 @@ using PairsFn = void (*)(const double*, const PairDesc*, int, int, Params, doubl
 using TriFn = void (*)(const double*, const long long*, const int*, int, int, int, Params, double*,
                       unsigned long long*, int*);
 using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
-                      const int*, int, const int*, int, int, int, int, int, Params, int, unsigned long long*,
+                      const int*, int, const int*, int, int, int, int, int, int, int, Params, int, unsigned long long*,
                       double*, int*, int*, const float2*, const float2*, int2*, int*);
 using NNFixFn = void (*)(const double*, const long long*, const int*, const double*, const long long*, const int*,
                          int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*);
