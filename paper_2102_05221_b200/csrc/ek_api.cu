@@ -72,6 +72,8 @@ struct Ctx {
   int dev = 0;
   int nsm = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // independent work forked off the calling stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 Ctx g_ctx;
 std::mutex g_mu;
@@ -105,6 +107,9 @@ int ensure_ctx() {
   if (pr.major < 10) return fail("device %d is sm_%d%d; this library is built for sm_100a", g_ctx.dev, pr.major, pr.minor);
   g_ctx.nsm = pr.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&g_ctx.side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&g_ctx.ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&g_ctx.ev_join, cudaEventDisableTiming));
   // keep stream-ordered allocations cached between calls (no re-mapping per call)
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, g_ctx.dev));
@@ -554,6 +559,23 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     engB = guard_engine();
   DBuf dovf;
   if (engB != eng && dovf.alloc(sizeof(int2) * (size_t)npairs, st)) return -1;
+  // 0. LB envelopes on a side stream, overlapping the ranking and phase A: candidates'
+  //    for lb_keogh(query, env(candidate)), queries' for the survivors' reverse bound
+  const float2* env = nullptr;
+  if (use_lb) {
+    const int L = max_len;
+    if (denv.alloc(sizeof(float2) * (size_t)L * ncand, st) || denvq.alloc(sizeof(float2) * (size_t)L * nq, st))
+      return -1;
+    CK(cudaEventRecord(g_ctx.ev_fork, st));
+    CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_fork, 0));
+    if (launch_plain(k_envelope, dim3((unsigned)ncand), dim3(256), sizeof(double) * 5 * (size_t)L, g_ctx.side, dC,
+                     (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>()) ||
+        launch_plain(k_envelope, dim3((unsigned)nq), dim3(256), sizeof(double) * 5 * (size_t)L, g_ctx.side, dQ,
+                     (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>()))
+      return -1;
+    CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
+    env = denv.as<float2>();
+  }
   // 1. candidate order: approximate Euclidean ranking (scheduling only)
   const bool rank = share && ncand <= 16384 && ncand > 1;
   if (rank) {
@@ -605,22 +627,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       return -1;
   }
   mark(st, "nn_phaseA");
-  const float2* env = nullptr;
-  if (use_lb) {
-    // envelopes of the candidates; phase B tests lb_keogh per pair before its DP
-    const int L = max_len;
-    if (denv.alloc(sizeof(float2) * (size_t)L * ncand, st)) return -1;
-    if (launch_plain(k_envelope, dim3((unsigned)ncand), dim3(256), sizeof(double) * 5 * (size_t)L, st, dC,
-                     (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>()))
-      return -1;
-    env = denv.as<float2>();
-    // query envelopes for the reverse bound of the survivors (lb_keogh2's second order)
-    if (denvq.alloc(sizeof(float2) * (size_t)L * nq, st)) return -1;
-    if (launch_plain(k_envelope, dim3((unsigned)nq), dim3(256), sizeof(double) * 5 * (size_t)L, st, dQ,
-                     (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>()))
-      return -1;
-    mark(st, "envelope");
-  }
+  if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the envelopes (side stream)
   // phase B, one launch of two segments: the next-best 64 ranks (where the survivors
   // concentrate) one pair per item for load balance, the rest in items of 8
   // (64 / 8 measured best on C2 against 32..128 / 4..32)
