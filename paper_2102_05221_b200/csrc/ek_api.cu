@@ -302,9 +302,10 @@ UBFn pick_ub(int kind, int mode) {
 }
 
 // Engine for a (lines, cols, window) shape; -1 if unsupported.
-int choose_engine(int nl, int nc, int w, bool ea_rows) {
+int choose_engine(int nl, int nc, int w, bool ea_rows, bool allow_p2 = false) {
   if (ea_rows) return nc <= 512 ? E_STR16_EA : -1;
   const int slots = diag_slots_needed(nl, nc, w);
+  if (allow_p2 && slots <= 64) return E_DIAG2;
   if (slots <= 128) return E_DIAG4;
   if (slots <= 256) return E_DIAG8;
   const bool banded = w < nl - 1;
@@ -745,7 +746,7 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
     return 0;
   }
   const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
-  const int eng = choose_engine(max_len, max_len, win < 0 ? max_len : win, false);
+  const int eng = choose_engine(max_len, max_len, win < 0 ? max_len : win, false, true);
   if (eng < 0) return fail("series length %d exceeds this build's engines", max_len);
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;

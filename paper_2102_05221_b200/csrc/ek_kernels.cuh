@@ -31,13 +31,14 @@ enum Engine : int {
   E_STRB16 = 6,
   E_STR16_EA = 7,
   E_GDIAG8 = 8, E_GDIAG16 = 9,
-  E_COUNT = 10
+  E_DIAG2 = 10,  // narrow bands (<= 64 slots) in the all-pairs kernel: twice the lanes of P=4
+  E_COUNT = 11
 };
 
 __host__ __device__ constexpr int engine_is_diag(int e) { return e <= E_DIAG16 || e >= E_GDIAG8; }
-__host__ __device__ constexpr int engine_guarded(int e) { return e >= E_GDIAG8; }
+__host__ __device__ constexpr int engine_guarded(int e) { return e == E_GDIAG8 || e == E_GDIAG16; }
 __host__ __device__ constexpr int engine_P(int e) {
-  return e == E_DIAG4 ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
+  return e == E_DIAG2 ? 2 : e == E_DIAG4 ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
 }
 __host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e == E_STR8 ? 8 : 16; }
 // elements an engine may read beyond either end of a staged series

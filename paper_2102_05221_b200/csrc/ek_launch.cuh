@@ -185,6 +185,8 @@ TriFn get_triangle(int mode, int eng) {
   switch (mode * 16 + eng) {
     EKB_ENG_CASES(0, k_triangle)
     EKB_ENG_CASES(1, k_triangle)
+    case 0 * 16 + E_DIAG2: return k_triangle<KIND, 0, E_DIAG2>;
+    case 1 * 16 + E_DIAG2: return k_triangle<KIND, 1, E_DIAG2>;
   }
   return nullptr;
 }
