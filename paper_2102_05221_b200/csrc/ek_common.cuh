@@ -61,6 +61,9 @@ EKB_DI double pcost(double a, double b) {
   return fabs(d);
 }
 
+// IEEE sign bit (0 / 1) of a double
+EKB_DI int sign_bit(double v) { return (int)((unsigned)__double2hiint(v) >> 31); }
+
 // ---- row / column data ----
 template <int KIND> struct RowD { double x; };
 template <int KIND> struct ColD { double y; };
@@ -68,8 +71,8 @@ template <> struct RowD<K_ERP> { double x, ar; };
 template <> struct ColD<K_ERP> { double y, ac; };
 template <> struct RowD<K_TWE> { double x, ar; };
 template <> struct ColD<K_TWE> { double y, ac; };
-template <> struct RowD<K_MSM> { double x, dr; int f; };  // f bit0: xprev<=x, bit1: xprev>=x
-template <> struct ColD<K_MSM> { double y, dc; int f; };  // f bit0: y<=yprev, bit1: y>=yprev
+template <> struct RowD<K_MSM> { double x, dr; int s; };  // s: sign bit of x - xprev
+template <> struct ColD<K_MSM> { double y, dc; int s; };  // s: sign bit of y - yprev
 
 // x = l[i-1], xp = l[i-2] (pad: MSM uses l[0] at index -1, TWE a phantom 0.0)
 template <int KIND, int MODE>
@@ -79,8 +82,9 @@ EKB_DI RowD<KIND> make_row(double x, double xp, const Params& p) {
   if constexpr (KIND == K_ERP) r.ar = pcost<MODE>(x, p.gap);                 // alt_row: pc(l_i, g)
   if constexpr (KIND == K_TWE) r.ar = dadd(dadd(pcost<MODE>(x, xp), p.nu), p.lam);  // (pc(l_i,l_{i-1})+nu)+lam
   if constexpr (KIND == K_MSM) {
-    r.dr = fabs(dsub(x, xp));  // fabs(np - x) in msm_cost(l_i, l_{i-1}, c_j)
-    r.f = (xp <= x ? 1 : 0) | (xp >= x ? 2 : 0);
+    const double d = dsub(x, xp);
+    r.dr = fabs(d);  // fabs(np - x) in msm_cost(l_i, l_{i-1}, c_j)
+    r.s = sign_bit(d);
   }
   return r;
 }
@@ -92,8 +96,9 @@ EKB_DI ColD<KIND> make_col(double y, double yp, const Params& p) {
   if constexpr (KIND == K_ERP) c.ac = pcost<MODE>(p.gap, y);                 // alt_col: pc(g, c_j)
   if constexpr (KIND == K_TWE) c.ac = dadd(dadd(pcost<MODE>(y, yp), p.nu), p.lam);
   if constexpr (KIND == K_MSM) {
-    c.dc = fabs(dsub(y, yp));  // fabs(np - y) in msm_cost(c_j, l_i, c_{j-1})
-    c.f = (y <= yp ? 1 : 0) | (y >= yp ? 2 : 0);
+    const double d = dsub(y, yp);
+    c.dc = fabs(d);  // fabs(np - y) in msm_cost(c_j, l_i, c_{j-1})
+    c.s = sign_bit(d);
   }
   return c;
 }
@@ -123,6 +128,13 @@ EKB_DI DiagK<KIND> make_diag(int d, const Params& p, bool in_band = true) {
 
 // MSM split/merge alternative (kernels.py:95-105; _speedups.pyx:41-47), given the
 // shared |l_i - c_j| and the between-test already decided.
+//
+// Between-tests from sign bits: with e = l_i - c_j and dr = l_i - l_{i-1},
+// "l_{i-1} <= l_i <= c_j or l_{i-1} >= l_i >= c_j" holds iff e and dr do not have the
+// same strict sign, and the column test (l_i <= c_j <= c_{j-1} or ...) iff e and
+// dc = c_j - c_{j-1} do.  Reading "strict sign" as the IEEE sign bit only misclassifies
+// a zero (e or dr / dc == +0: an exact difference is never -0), and then both outcomes
+// give the same value: c, or c + min(|d|, 0) = c + 0 = c.
 EKB_DI double msm_alt(bool between, double c, double dother, double de) {
   double m = (dother < de) ? dother : de;  // "d1 if d1 < d2 else d2" (value-identical)
   return between ? c : dadd(c, m);
@@ -156,9 +168,9 @@ EKB_DI double cell(double D, double T, double L, const RowD<KIND>& r, const ColD
   } else {  // MSM: canonical |l_i - c_j| regardless of cost mode
     double e = dsub(r.x, c.y);
     double de = fabs(e);
-    bool le = e <= 0.0, ge = e >= 0.0;  // l_i <= c_j, l_i >= c_j
-    bool brow = ((r.f & 1) && le) || ((r.f & 2) && ge);  // l_{i-1}<=l_i<=c_j or l_{i-1}>=l_i>=c_j
-    bool bcol = (le && (c.f & 1)) || (ge && (c.f & 2));  // l_i<=c_j<=c_{j-1} or l_i>=c_j>=c_{j-1}
+    const int se = sign_bit(e);
+    bool brow = se != r.s;  // l_{i-1}<=l_i<=c_j or l_{i-1}>=l_i>=c_j (see msm_alt)
+    bool bcol = se == c.s;  // l_i<=c_j<=c_{j-1} or l_i>=c_j>=c_{j-1}
     double ar = msm_alt(brow, p.msm_c, r.dr, de);
     double ac = msm_alt(bcol, p.msm_c, c.dc, de);
     double v = dadd(D, de);

@@ -42,8 +42,7 @@ __device__ __forceinline__ double ub_term(const double* X, const double* Y, int 
   else if constexpr (KIND == K_ERP || KIND == K_TWE) return r.ar;
   else if constexpr (KIND == K_MSM) {
     const double e = dsub(r.x, y);
-    const bool brow = ((r.f & 1) && e <= 0.0) || ((r.f & 2) && e >= 0.0);
-    return msm_alt(brow, pp.msm_c, r.dr, fabs(e));
+    return msm_alt(sign_bit(e) != r.s, pp.msm_c, r.dr, fabs(e));
   } else return pcost<MODE>(r.x, y);
 }
 
