@@ -333,3 +333,59 @@ def test_nonfinite_inputs_raise(gpu, rng, bad):
     # the library stays usable afterwards
     idx = gpu.nn_batch(spec, "eapruned", Q, C[:4])[0]
     assert idx.shape == (3,)
+
+
+def _workload_rows(wl, nq, seed_shift=0):
+    from paper_2102_05221_b200 import datagen
+
+    C, cl, protos = datagen.warped_prototypes(wl.n_candidates, wl.length, wl.classes, wl.sigma, wl.seed)
+    Q, ql, _ = datagen.warped_prototypes(nq, wl.length, wl.classes, wl.sigma, wl.seed + 1 + seed_shift,
+                                         protos=protos)
+    return Q, C
+
+
+@pytest.mark.parametrize("which", ["c2", "c4m", "c4t"])
+def test_benchmark_shapes_vs_oracle(gpu, which):
+    """The BASELINE configurations at full candidate count and length, on a query subset
+    the oracle finishes in seconds: nn indices and distances identical."""
+    from paper_2102_05221_b200 import datagen
+
+    wl = datagen.C2 if which == "c2" else datagen.C4
+    nq = 32 if which == "c2" else 8
+    Q, C = _workload_rows(wl, nq)
+    spec = {"c2": gpu.DistanceSpec(kind="cdtw", window=51),
+            "c4m": gpu.DistanceSpec(kind="msm", msm_c=1.0),
+            "c4t": gpu.DistanceSpec(kind="twe", twe_nu=0.001, twe_lambda=1.0)}[which]
+    idx, dist = gpu.nn_batch(spec, "eapruned", Q, C)[:2]
+    r = eko.nn(spec, "eapruned", Q, C, threads=16)
+    assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"])
+
+
+def test_c2_full_size_properties(gpu, rng):
+    """Full C2 size (256 x 4096 x 512): results are invariant under any candidate order
+    (indices map back through the permutation) and equal to base-variant distances."""
+    from paper_2102_05221_b200 import datagen
+
+    Q, _, C, _ = datagen.C2.make()
+    spec = gpu.DistanceSpec(kind="cdtw", window=51)
+    idx, dist = gpu.nn_batch(spec, "eapruned", Q, C)[:2]
+    perm = rng.permutation(len(C))
+    idx_p, dist_p = gpu.nn_batch(spec, "eapruned", Q, np.ascontiguousarray(C[perm]))[:2]
+    assert np.array_equal(dist, dist_p)
+    assert np.array_equal(perm[idx_p], idx)  # no exact ties in this data
+    # every reported distance is the exact (base) distance of that pair
+    pairs = [(Q[k], C[idx[k]]) for k in range(0, len(Q), 16)]
+    base, _ = gpu.distance_batch(spec, "base", pairs)
+    assert np.array_equal(base, dist[::16])
+
+
+def test_subseq_long_stream_vs_oracle(gpu):
+    """C5 shape (query 1024, w=51, z-normalised) on a 2^15-point stream: best window and
+    distance identical to the oracle; the planted copy is found at distance ~0."""
+    from paper_2102_05221_b200 import datagen
+
+    stream, q = datagen.subsequence_workload(stream_len=1 << 15, query_len=1024, seed=4242)
+    spec = gpu.DistanceSpec(kind="cdtw", window=51)
+    got = gpu.subsequence_search(q, stream, gpu.SearchConfig(spec=spec, variant="eapruned", normalize=True))[:2]
+    want = eko.subsequence(spec, "eapruned", q, stream, True, chunk=2048, threads=16)[:2]
+    assert got == want
