@@ -70,3 +70,81 @@ def test_two_rank_query_shards_match_serial():
     ref = eko.nn(DistanceSpec(kind="cdtw", window=5), "eapruned", Qs, C, threads=2)
     assert np.array_equal(np.concatenate([g[1] for g in gathered]), ref["nn_index"])
     assert np.array_equal(np.concatenate([g[2] for g in gathered]), ref["nn_distance"])
+
+
+def _oracle_hooks():
+    """CPU stand-ins with the signatures of nn_batch / subsequence_search / distance_batch."""
+    from oracle import eko
+    from paper_2102_05221_b200.search import SearchStats
+
+    def nn(spec, variant, Q, C):
+        r = eko.nn(spec, variant, Q, C, threads=1)
+        return r["nn_index"], r["nn_distance"], r["cells"], r["computed"], r["abandoned"]
+
+    def subseq(q, ref, cfg):
+        off, d, cells = eko.subsequence(cfg.spec, cfg.variant, q, ref, cfg.normalize, threads=1)
+        return off, d, SearchStats(cells=cells)
+
+    def pairs(spec, variant, prs):
+        out = [eko.distance(spec, variant, a, b) for a, b in prs]
+        return np.array([o[0] for o in out]), np.array([o[1] for o in out], dtype=np.int64)
+
+    return nn, subseq, pairs
+
+
+def _sharded_worker(rank, world, port, out):
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2102_05221_b200 import DistanceSpec, SearchConfig, datagen, distributed
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nn, subseq, pairs = _oracle_hooks()
+    C, _, protos = datagen.warped_prototypes(40, 40, 4, 0.1, 21)
+    Q, _, _ = datagen.warped_prototypes(7, 40, 4, 0.1, 22, protos=protos)
+    spec = DistanceSpec(kind="cdtw", window=4)
+    res_nn = distributed.nn_batch_sharded(spec, "eapruned", Q, C, compute=nn)
+    rng = np.random.default_rng(5)
+    stream = np.cumsum(rng.normal(0, 1, 700))
+    q = stream[311:351].copy()
+    cfg = SearchConfig(spec=spec, variant="eapruned", normalize=True)
+    res_ss = distributed.subsequence_search_sharded(q, stream, cfg, compute=subseq)
+    X = [np.cumsum(rng.normal(0, 1, 25)) for _ in range(9)]
+    res_pw = distributed.pairwise_sharded(DistanceSpec(kind="erp", window=5, erp_gap=0.0), X, compute=pairs)
+    if rank == 0:
+        out.put((res_nn, res_ss[:2], res_pw))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_sharded_entry_points_match_single_process():
+    """distributed.{nn_batch,subsequence_search,pairwise}_sharded over 2 gloo ranks give the
+    single-process answers (the stream split keeps its L-1 halo and the tie rule)."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res_nn, res_ss, res_pw = out.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import eko
+    from paper_2102_05221_b200 import DistanceSpec, datagen, distributed
+
+    C, _, protos = datagen.warped_prototypes(40, 40, 4, 0.1, 21)
+    Q, _, _ = datagen.warped_prototypes(7, 40, 4, 0.1, 22, protos=protos)
+    spec = DistanceSpec(kind="cdtw", window=4)
+    ref = eko.nn(spec, "eapruned", Q, C, threads=2)
+    assert np.array_equal(res_nn[0], ref["nn_index"]) and np.array_equal(res_nn[1], ref["nn_distance"])
+    rng = np.random.default_rng(5)
+    stream = np.cumsum(rng.normal(0, 1, 700))
+    q = stream[311:351].copy()
+    off, d, _ = eko.subsequence(spec, "eapruned", q, stream, True)
+    assert tuple(res_ss) == (off, d) and off == 311
+    X = [np.cumsum(rng.normal(0, 1, 25)) for _ in range(9)]
+    D = eko.pairwise(DistanceSpec(kind="erp", window=5, erp_gap=0.0), X)[0]
+    assert np.array_equal(res_pw[0], D)
+    assert [distributed.shard_range(7, r, 3) for r in range(3)] == [(0, 3), (3, 5), (5, 7)]
