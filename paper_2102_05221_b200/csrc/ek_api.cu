@@ -303,7 +303,7 @@ UBFn pick_ub(int kind, int mode) {
 
 // Engine for a (lines, cols, window) shape; -1 if unsupported.
 int choose_engine(int nl, int nc, int w, bool ea_rows, bool allow_p2 = false) {
-  if (ea_rows) return nc <= 512 ? E_STR16_EA : -1;
+  if (ea_rows) return nc <= 512 ? E_STR16_EA : E_STRIP16_EA;
   const int slots = diag_slots_needed(nl, nc, w);
   if (allow_p2 && slots <= 64) return E_DIAG2;
   if (slots <= 128) return E_DIAG4;
@@ -316,7 +316,7 @@ int choose_engine(int nl, int nc, int w, bool ea_rows, bool allow_p2 = false) {
   }
   if (slots <= 512) return E_DIAG16;
   if (nc <= 512) return E_STRB16;
-  return -1;
+  return banded ? E_STRIPB16 : E_STRIP16;  // long series: 512-column strips
 }
 int eng_S(int e) { return engine_S(e); }
 
@@ -358,6 +358,29 @@ struct ParamHolder {
 };
 
 size_t pair_smem(int lmax, int eng, int wpb) { return sizeof(double) * (size_t)wpb * warp_stride(lmax, eng); }
+
+// warps per block: up to `want`, as many as the per-warp shared memory allows
+int pick_wpb(int lmax, int eng, int want, int extra_per_warp = 0) {
+  int wpb = want;
+  while (wpb > 1 && (size_t)wpb * (sizeof(double) * (size_t)(warp_stride(lmax, eng) + extra_per_warp)) > 220 * 1024)
+    --wpb;
+  return wpb;
+}
+
+// per-warp boundary columns of the strip engines (Params.strip_buf), sized for every
+// warp the persistent launch of `fn` can have resident
+template <class Fn>
+int strip_scratch(Fn fn, int eng, int block, size_t smem, int lmax, Params& prm, DBuf& buf, cudaStream_t st) {
+  if (!engine_is_strip(eng)) return 0;
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+  const long long warps = (long long)std::max(1, per_sm) * g_ctx.nsm * (block / 32);
+  prm.strip_stride = lmax + 1;
+  if (buf.alloc(sizeof(double) * 3 * (size_t)prm.strip_stride * (size_t)warps, st)) return -1;
+  prm.strip_buf = buf.as<double>();
+  return 0;
+}
 
 // numpy pairwise-sum plan (see ek_subseq.cuh)
 void np_plan_rec(int start, int n, std::vector<int2>& leaves, std::vector<int>& ops) {
@@ -470,11 +493,14 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
     if (dp.alloc(sizeof(PairDesc) * n, st) || dc.alloc(sizeof(double) * n, st) || dt.alloc(sizeof(int) * n, st))
       return -1;
     CK(cudaMemcpyAsync(dp.p, groups[eng].data(), sizeof(PairDesc) * n, cudaMemcpyHostToDevice, st));
-    const int wpb = 4;
+    const int wpb = pick_wpb(glmax[eng], eng, 4);
     const size_t smem = pair_smem(glmax[eng], eng, wpb);
-    if (launch_persistent(pick_pairs(spec->kind, spec->cost_mode, eng), 32 * wpb, smem, st, (long long)n,
-                          (const double*)dser.as<double>(), (const PairDesc*)dp.as<PairDesc>(), (int)n,
-                          glmax[eng], ph.prm, dc.as<double>(), dt.as<int>()))
+    const PairsFn pf = pick_pairs(spec->kind, spec->cost_mode, eng);
+    Params prm = ph.prm;
+    DBuf dstrip;
+    if (strip_scratch(pf, eng, 32 * wpb, smem, glmax[eng], prm, dstrip, st)) return -1;
+    if (launch_persistent(pf, 32 * wpb, smem, st, (long long)n, (const double*)dser.as<double>(),
+                          (const PairDesc*)dp.as<PairDesc>(), (int)n, glmax[eng], prm, dc.as<double>(), dt.as<int>()))
       return -1;
     std::vector<double> hc(n);
     std::vector<int> hcl(n);
@@ -616,8 +642,10 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   mark(st, "seed_cutoff");
   // 3. phase A: the top-ranked few per query; phase B: everything else
   const NNFn fn = pick_nn(spec->kind, spec->cost_mode, eng);
-  const int wpb = 4;
+  const int wpb = pick_wpb(max_len, eng, 4);
   const size_t smem = pair_smem(max_len, eng, wpb);
+  DBuf dstrip;
+  if (strip_scratch(fn, eng, 32 * wpb, smem, max_len, ph.prm, dstrip, st)) return -1;
   const int ka = share ? (int)std::min<int64_t>(4, ncand) : 0;
   if (ka > 0) {
     if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
@@ -656,10 +684,14 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   }
   mark(st, "nn_phaseB");
   if (engB != eng) {  // redo guarded-band overflows with the full-band engine
-    if (launch_persistent(pick_nn_fix(spec->kind, spec->cost_mode, eng), 32 * wpb, smem, st, npairs, dQ,
-                          (const long long*)dqoff, (const int*)dqlen, dC, (const long long*)dcoff, (const int*)dclen,
-                          (int)ncand, (const int2*)dovf.as<int2>(), (const int*)ovf_count, win, (int)max_len, ph.prm,
-                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), ovf_count + 1))
+    const NNFixFn ff = pick_nn_fix(spec->kind, spec->cost_mode, eng);
+    Params fprm = ph.prm;
+    DBuf dstrip2;
+    if (strip_scratch(ff, eng, 32 * wpb, smem, max_len, fprm, dstrip2, st)) return -1;
+    if (launch_persistent(ff, 32 * wpb, smem, st, npairs, dQ, (const long long*)dqoff, (const int*)dqlen, dC,
+                          (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int2*)dovf.as<int2>(),
+                          (const int*)ovf_count, win, (int)max_len, fprm, dcut.as<unsigned long long>(),
+                          dout.as<double>(), dtend.as<int>(), ovf_count + 1))
       return -1;
     mark(st, "nn_fix");
   }
@@ -757,8 +789,11 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
   if (dcnt.alloc(8, st) || dtot.alloc(8, st)) return -1;
   CK(cudaMemsetAsync(dcnt.p, 0, 8, st));
   CK(cudaMemsetAsync(dtot.p, 0, 8, st));
-  const int wpb = 4;
-  if (launch_persistent(pick_tri(spec->kind, spec->cost_mode, eng), 32 * wpb, pair_smem(max_len, eng, wpb), st, np,
+  const int wpb = pick_wpb(max_len, eng, 4);
+  const TriFn tf = pick_tri(spec->kind, spec->cost_mode, eng);
+  DBuf dstrip;
+  if (strip_scratch(tf, eng, 32 * wpb, pair_smem(max_len, eng, wpb), max_len, ph.prm, dstrip, st)) return -1;
+  if (launch_persistent(tf, 32 * wpb, pair_smem(max_len, eng, wpb), st, np,
                         d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, ph.prm, d_D,
                         dtot.as<unsigned long long>(), dcnt.as<int>()))
     return -1;

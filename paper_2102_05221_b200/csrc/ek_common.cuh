@@ -36,6 +36,10 @@ struct Params {
   const long long* wt_off;
   const double* wt;  // per pair: the table for this pair's longest length
   int wt_len;        // entries available in wt
+  // long-series strip engines: per-warp boundary columns (2 x strip_stride doubles per
+  // warp, indexed by the global warp id)
+  double* strip_buf;
+  int strip_stride;
 };
 
 // Params for one pair whose longest series has length m.

@@ -32,10 +32,18 @@ enum Engine : int {
   E_STR16_EA = 7,
   E_GDIAG8 = 8, E_GDIAG16 = 9,
   E_DIAG2 = 10,  // narrow bands (<= 64 slots) in the all-pairs kernel: twice the lanes of P=4
-  E_COUNT = 11
+  E_STRIP16 = 11, E_STRIPB16 = 12,  // long series: 512-column strips (unbanded / banded)
+  E_STRIP16_EA = 13,                // long series, ea rows (full computation + row minima)
+  E_COUNT = 14
 };
+__host__ __device__ constexpr int engine_is_strip(int e) {
+  return e == E_STRIP16 || e == E_STRIPB16 || e == E_STRIP16_EA;
+}
+constexpr int kStripDone = 0x40000000;  // strip engines' t_end for a completed pair
 
-__host__ __device__ constexpr int engine_is_diag(int e) { return e <= E_DIAG16 || e >= E_GDIAG8; }
+__host__ __device__ constexpr int engine_is_diag(int e) {
+  return e <= E_DIAG16 || e == E_GDIAG8 || e == E_GDIAG16 || e == E_DIAG2;
+}
 __host__ __device__ constexpr int engine_guarded(int e) { return e == E_GDIAG8 || e == E_GDIAG16; }
 __host__ __device__ constexpr int engine_P(int e) {
   return e == E_DIAG2 ? 2 : e == E_DIAG4 ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
@@ -141,8 +149,14 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
     DiagResult r = diag_pair<KIND, MODE, engine_P(ENG), SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
     cost = r.cost;
     tend = r.t_end;
+  } else if constexpr (engine_is_strip(ENG)) {
+    double* sb = prm.strip_buf + (size_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 3 * prm.strip_stride;
+    StripeResult r = strip_pair<KIND, MODE, ENG != E_STRIP16, SHARED_CUT, ENG == E_STRIP16_EA>(
+        X, nl, Y, nc, w, cut, cutp, tab, tablen, prm, sb, sb + prm.strip_stride, sb + 2 * prm.strip_stride);
+    cost = r.cost;
+    tend = (r.cost < EKB_INF) ? kStripDone : r.t_end;  // warp_cells: the band, or steps x 1024 cells
   } else {
-    constexpr bool BANDED = ENG >= E_STRB16;
+    constexpr bool BANDED = ENG == E_STRB16 || ENG == E_STR16_EA;
     constexpr bool EA = ENG == E_STR16_EA;
     StripeResult r = stripe_pair<KIND, MODE, engine_S(ENG), BANDED, SHARED_CUT, EA>(X, nl, Y, nc, w, cut, cutp,
                                                                                      tab, tablen, prm);
@@ -160,6 +174,13 @@ __device__ __forceinline__ int warp_cells(int nl, int nc, int w, int tend, int r
   const int lane = threadIdx.x & 31;
   constexpr bool DIAG = engine_is_diag(ENG);
   constexpr int S = engine_S(ENG);
+  if constexpr (engine_is_strip(ENG)) {  // whole band when completed, else ~1024 cells per step
+    int c = 0;
+    for (int i = 1 + lane; i <= nl; i += 32) c += max(0, min(nc, i + w) - max(1, i - w) + 1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    return tend >= kStripDone ? c : min(c, tend * 1024);
+  }
   const int imax = DIAG ? min(nl, tend - 1) : min(nl, r0 + 2 * tend - 1);
   int c = 0;
   for (int i = 1 + lane; i <= imax; i += 32) {

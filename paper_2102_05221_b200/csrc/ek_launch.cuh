@@ -166,7 +166,9 @@ RefFn get_pairs_ref(int mode, int eng) {
   case (M)*16 + E_STR4: return FN<KIND, M, E_STR4>;                                                 \
   case (M)*16 + E_STR8: return FN<KIND, M, E_STR8>;                                                 \
   case (M)*16 + E_STR16: return FN<KIND, M, E_STR16>;                                               \
-  case (M)*16 + E_STRB16: return FN<KIND, M, E_STRB16>;
+  case (M)*16 + E_STRB16: return FN<KIND, M, E_STRB16>;                                             \
+  case (M)*16 + E_STRIP16: return FN<KIND, M, E_STRIP16>;                                           \
+  case (M)*16 + E_STRIPB16: return FN<KIND, M, E_STRIPB16>;
 
 template <int KIND>
 PairsFn get_pairs(int mode, int eng) {
@@ -175,6 +177,8 @@ PairsFn get_pairs(int mode, int eng) {
     EKB_ENG_CASES(1, k_pairs)
     case 0 * 16 + E_STR16_EA: return k_pairs<KIND, 0, E_STR16_EA>;
     case 1 * 16 + E_STR16_EA: return k_pairs<KIND, 1, E_STR16_EA>;
+    case 0 * 16 + E_STRIP16_EA: return k_pairs<KIND, 0, E_STRIP16_EA>;
+    case 1 * 16 + E_STRIP16_EA: return k_pairs<KIND, 1, E_STRIP16_EA>;
   }
   return nullptr;
 }
@@ -217,6 +221,10 @@ NNFixFn get_nn_fix(int mode, int eng) {
     case 1 * 16 + E_DIAG16: return k_nn_fix<KIND, 1, E_DIAG16>;
     case 0 * 16 + E_STRB16: return k_nn_fix<KIND, 0, E_STRB16>;
     case 1 * 16 + E_STRB16: return k_nn_fix<KIND, 1, E_STRB16>;
+    case 0 * 16 + E_STRIP16: return k_nn_fix<KIND, 0, E_STRIP16>;
+    case 1 * 16 + E_STRIP16: return k_nn_fix<KIND, 1, E_STRIP16>;
+    case 0 * 16 + E_STRIPB16: return k_nn_fix<KIND, 0, E_STRIPB16>;
+    case 1 * 16 + E_STRIPB16: return k_nn_fix<KIND, 1, E_STRIPB16>;
   }
   return nullptr;
 }

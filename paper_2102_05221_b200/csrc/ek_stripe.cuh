@@ -252,3 +252,235 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
 }
 
 }  // namespace ekb
+
+namespace ekb {
+
+// Long series (more than 32 x 16 columns): the row-stripe engine over vertical strips of
+// 512 columns, one after another.  Strip k reads its left boundary column (column 512k,
+// rows 0..nl) from `bin` and writes its own last column to `bout` for strip k + 1; the
+// two buffers (nl + 1 doubles each, per warp) swap between strips.  Inside strip 0 the
+// two-dead-steps cut is valid as in stripe_pair; later strips can be re-entered from
+// their left boundary, so they only stop the pair when a whole boundary column is dead
+// (every path crosses every column).  The same cells, borders and band masks as
+// stripe_pair, so values are bit-identical.  EA (`ea` with a finite cutoff): a row's
+// minimum spans every strip, so nothing is abandoned; each strip folds its row minima
+// (border cell included, _speedups.pyx:147-160) into `rmin` and the result is +inf if
+// any row minimum exceeds the cutoff, else the exact cost.
+template <int KIND, int MODE, bool BANDED, bool SHARED_CUT, bool EA, class XAcc, class YAcc>
+__device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
+                                   const unsigned long long* cutp, const double* tab, int tablen,
+                                   const Params& prm, double* bin, double* bout, double* rmin) {
+  constexpr int S = 16;
+  constexpr int STRIP = 32 * S;
+  const int lane = threadIdx.x & 31;
+  constexpr bool BORDERED = (KIND == K_ERP);
+  constexpr bool TWE = (KIND == K_TWE);
+  const int r0 = BORDERED ? 0 : 1;
+  const int nstrips = (nc + STRIP - 1) / STRIP;
+  auto cy = [&](int k) { return Y.at(min(max(k, -1), nc)); };
+  auto cx = [&](int k) { return X.at(k); };
+  double nextcut = cut;
+  int cut_hi = hi_word(cut);
+  int steps_done = 0;
+  double result = EKB_INF;
+  bool dead = false;
+  if constexpr (EA) {
+    for (int i = lane; i <= nl; i += 32) rmin[i] = EKB_INF;
+    __syncwarp();
+  }
+
+  for (int sk = 0; sk < nstrips && !dead; ++sk) {
+    const int jbase = sk * STRIP + lane * S;
+    const bool last_strip = sk == nstrips - 1;
+    const int lf = last_strip ? (nc - 1 - sk * STRIP) / S : 31;
+    const int sf = (nc - 1) % S;
+    ColD<KIND> cols[S];
+    double val[S];
+    double pcr[TWE ? S : 1];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int j = jbase + 1 + s;
+      cols[s] = make_col<KIND, MODE>(cy(j - 1), cy(j - 2), prm);
+      val[s] = EKB_INF;
+      if constexpr (TWE) pcr[s] = pcost<MODE>(cx(r0 - 2), cols[s].y);
+    }
+    double dg = EKB_INF, dgpc = 0.0;
+    double xprev = cx(r0 - 2);
+    double vb = 0.0;
+    const double ycol0 = cy(jbase - 1);
+    if (lane == 0 && sk == 0) dg = BORDERED ? EKB_INF : 0.0;
+    if constexpr (TWE) dgpc = pcost<MODE>(cx(r0 - 2), ycol0);
+    const int nsteps = lf + (nl - r0) / 2 + 1;
+    const bool last_is_i0 = ((nl - r0) & 1) == 0;
+    bool alive2 = false;
+    double last0 = EKB_INF, last1 = EKB_INF, lastpc0 = 0.0, lastpc1 = 0.0;
+    double rmo0 = EKB_INF, rmo1 = EKB_INF;
+    double fin = EKB_INF;
+
+    auto row_pass = [&](int i, const RowD<KIND>& rd, double lft, double dgl, double dpc, double (&row)[S],
+                        bool& alive, double& rm) {
+      int a = 0, b = S - 1;
+      if constexpr (BANDED) {
+        const int hi = (i == 0) ? w + 1 : i + w;
+        a = i - w - jbase - 1;
+        b = hi - jbase - 1;
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int j = jbase + 1 + s;
+        const double up = row[s];
+        DiagK<KIND> k{};
+        if constexpr (KIND == K_WDTW) k.w = tab[min(abs(i - j), tablen - 1)];
+        if constexpr (TWE) k.tw = tab[min(abs(i - j), tablen - 1)];
+        SlotS<KIND> stt;
+        double upc = 0.0;
+        if constexpr (TWE) {
+          stt.pcp = dpc;
+          upc = pcr[s];
+        }
+        double v = cell<KIND, MODE, false>(dgl, up, lft, rd, cols[s], k, stt, prm);
+        if constexpr (BANDED) v = (s >= a && s <= b) ? v : EKB_INF;
+        if constexpr (TWE) {
+          pcr[s] = stt.pcp;
+          dpc = upc;
+        }
+        row[s] = v;
+        dgl = up;
+        lft = v;
+        alive |= hi_word(v) <= cut_hi;
+        if constexpr (EA) rm = (v < rm) ? v : rm;
+      }
+    };
+
+    int t = 0;
+    for (t = 0; t < nsteps; ++t) {
+      if constexpr (SHARED_CUT) {
+        if ((t & 15) == 0) nextcut = ld_cut(cutp);
+        if ((t & 15) == 12) {
+          cut = fmin(cut, nextcut);
+          cut_hi = hi_word(cut);
+        }
+      }
+      const int i0 = r0 + 2 * (t - lane), i1 = i0 + 1;
+      double lb0 = __shfl_up_sync(FULL, last0, 1);
+      double lb1 = __shfl_up_sync(FULL, last1, 1);
+      double lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1) : 0.0;
+      double lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1) : 0.0;
+      double rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1) : EKB_INF;
+      double rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1) : EKB_INF;
+      const double x0 = cx(i0 - 1), x1 = cx(i1 - 1);
+      const RowD<KIND> rd0 = make_row<KIND, MODE>(x0, xprev, prm);
+      const RowD<KIND> rd1 = make_row<KIND, MODE>(x1, x0, prm);
+      xprev = x1;
+      if (lane == 0) {
+        if (sk == 0) {  // the matrix border (stripe_pair's lane 0)
+          if constexpr (BORDERED) {
+            vb = (i0 == 0) ? 0.0 : dadd(vb, rd0.ar);
+            lb0 = (i0 <= w + 1) ? vb : EKB_INF;
+            vb = dadd(vb, rd1.ar);
+            lb1 = (i1 <= w + 1) ? vb : EKB_INF;
+          } else {
+            lb0 = (i0 == 0) ? 0.0 : EKB_INF;
+            lb1 = EKB_INF;
+          }
+          if constexpr (TWE) {
+            lbpc0 = pcost<MODE>(x0, 0.0);
+            lbpc1 = pcost<MODE>(x1, 0.0);
+          }
+          rm0 = (i0 >= 1) ? lb0 : EKB_INF;  // ea: the border cell joins the row minimum
+          rm1 = (i1 >= 1) ? lb1 : EKB_INF;
+        } else {  // the previous strip's last column (already in the previous strip's minimum)
+          rm0 = EKB_INF;
+          rm1 = EKB_INF;
+          lb0 = (i0 >= 0 && i0 <= nl) ? bin[i0] : EKB_INF;
+          lb1 = (i1 >= 0 && i1 <= nl) ? bin[i1] : EKB_INF;
+          if constexpr (TWE) {
+            lbpc0 = pcost<MODE>(x0, ycol0);
+            lbpc1 = pcost<MODE>(x1, ycol0);
+          }
+        }
+      }
+      bool alive = lane == 0 && (hi_word(lb0) <= cut_hi || hi_word(lb1) <= cut_hi);
+      double row0[S];
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2) row0[s2] = val[s2];
+      row_pass(i0, rd0, lb0, dg, dgpc, row0, alive, rm0);
+      if constexpr (TWE) lastpc0 = pcr[S - 1];
+      if (t == nsteps - 1 && last_is_i0) {
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2)
+          if (s2 == sf) fin = row0[s2];
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2) val[s2] = row0[s2];
+      row_pass(i1, rd1, lb1, lb0, lbpc0, val, alive, rm1);
+      if constexpr (TWE) lastpc1 = pcr[S - 1];
+      dg = lb1;
+      dgpc = lbpc1;
+      last0 = row0[S - 1];
+      last1 = val[S - 1];
+      if (!last_strip && lane == 31) {  // this strip's last column for the next strip
+        if (i0 >= 0 && i0 <= nl) bout[i0] = last0;
+        if (i1 >= 0 && i1 <= nl) bout[i1] = last1;
+      }
+      if constexpr (EA) {
+        rmo0 = rm0;
+        rmo1 = rm1;
+        if (lane == lf) {  // the strip's row minima (lane lf holds column nc in the last strip)
+          if (i0 >= 1 && i0 <= nl) rmin[i0] = fmin(rmin[i0], rm0);
+          if (i1 >= 1 && i1 <= nl) rmin[i1] = fmin(rmin[i1], rm1);
+        }
+      }
+      if (nstrips == 1 && !EA) {  // a cut of every path only when the strip spans all columns
+        if (t & 1) {
+          if (!__any_sync(FULL, alive || alive2)) {
+            dead = true;
+            break;
+          }
+        }
+        alive2 = alive;
+      }
+    }
+    steps_done += dead ? t + 1 : nsteps;
+    if (dead) break;
+    if (!last_strip) {
+      __syncwarp();
+      bool any = EA;  // a dead boundary column ends every path
+      for (int i = r0 + lane; i <= nl; i += 32) any |= hi_word(bout[i]) <= cut_hi;
+      if (!__any_sync(FULL, any)) {
+        dead = true;
+        break;
+      }
+      double* tmp = bin;
+      bin = bout;
+      bout = tmp;
+      __syncwarp();
+    } else {
+      double r = val[0];
+#pragma unroll
+      for (int s = 1; s < S; ++s)
+        if (s == sf) r = val[s];
+      if (last_is_i0) r = fin;
+      result = __shfl_sync(FULL, r, lf);
+    }
+  }
+  StripeResult res;
+  res.t_end = steps_done;
+  res.ea_row = 0x7fffffff;
+  if (dead) {
+    res.cost = EKB_INF;
+    return res;
+  }
+  if constexpr (EA) {  // _ea: +inf iff some row minimum exceeds the cutoff, else the exact cost
+    __syncwarp();
+    bool over = false;
+    for (int i = 1 + lane; i <= nl; i += 32) over |= rmin[i] > cut;
+    res.cost = __any_sync(FULL, over) ? EKB_INF : result;
+    return res;
+  }
+  if constexpr (SHARED_CUT) cut = fmin(cut, ld_cut(cutp));
+  res.cost = (result <= cut) ? result : EKB_INF;
+  return res;
+}
+
+}  // namespace ekb

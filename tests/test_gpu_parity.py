@@ -389,3 +389,47 @@ def test_subseq_long_stream_vs_oracle(gpu):
     got = gpu.subsequence_search(q, stream, gpu.SearchConfig(spec=spec, variant="eapruned", normalize=True))[:2]
     want = eko.subsequence(spec, "eapruned", q, stream, True, chunk=2048, threads=16)[:2]
     assert got == want
+
+
+@pytest.mark.parametrize("kind", ["dtw", "wdtw", "erp", "msm", "twe", "cdtw"])
+def test_long_series_strip_engine(gpu, rng, kind):
+    """Series longer than one 512-column strip (up to 1300 points): unconstrained or
+    wide-band pairs run the strip engine (ek_stripe.cuh strip_pair) -- costs equal the
+    oracle's for every variant and cutoff regime, cells for base."""
+    params = {"dtw": {}, "cdtw": dict(window=700), "wdtw": dict(wdtw_g=0.02), "erp": dict(window=900, erp_gap=0.1),
+              "msm": dict(msm_c=0.5), "twe": dict(twe_nu=0.001, twe_lambda=1.0)}[kind]
+    spec = gpu.DistanceSpec(kind=kind, **params)
+    pairs, cuts = [], []
+    for _ in range(4):
+        n1, n2 = int(rng.integers(520, 1300)), int(rng.integers(520, 1300))
+        a, b = np.cumsum(rng.normal(0, 1, n1)), np.cumsum(rng.normal(0, 1, n2))
+        ex = eko.distance(spec, "base", a, b)[0]
+        for f in (np.inf, 1.01, 0.99):
+            pairs.append((a, b))
+            cuts.append(ex * f if np.isfinite(ex) else f)
+    bad = []
+    for variant in ("base", "ea", "eapruned", "pruned_only"):
+        costs, cells = gpu.distance_batch(spec, variant, pairs, cutoffs=cuts)
+        for (a, b), c, got, n in zip(pairs, cuts, costs, cells):
+            ref = eko.distance(spec, variant, a, b, cutoff=c)
+            if not same(got, ref[0]) or (variant == "base" and n != ref[1]):
+                bad.append((variant, c, got, ref[0], int(n), int(ref[1])))
+    assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("kind", ["dtw", "msm"])
+def test_long_series_nn_and_pairwise(gpu, kind):
+    """1-NN and all-pairs on 1000-point series (strip engine; guarded band + strip redo
+    for the cutoff variants) against the oracle."""
+    from paper_2102_05221_b200 import datagen
+
+    C, cl, protos = datagen.warped_prototypes(40, 1000, 4, 0.2, 71)
+    Q, ql, _ = datagen.warped_prototypes(3, 1000, 4, 0.2, 72, protos=protos)
+    spec = gpu.DistanceSpec(kind=kind, msm_c=1.0) if kind == "msm" else gpu.DistanceSpec(kind=kind)
+    for variant in ("eapruned", "base"):
+        idx, dist = gpu.nn_batch(spec, variant, Q, C)[:2]
+        r = eko.nn(spec, variant, Q, C, threads=16)
+        assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"]), variant
+    D, _ = gpu.pairwise(spec, C[:8])
+    Do, _ = eko.pairwise(spec, C[:8], threads=16)
+    assert np.array_equal(D, Do)
