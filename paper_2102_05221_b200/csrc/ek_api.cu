@@ -646,7 +646,10 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   const size_t smem = pair_smem(max_len, eng, wpb);
   DBuf dstrip;
   if (strip_scratch(fn, eng, 32 * wpb, smem, max_len, ph.prm, dstrip, st)) return -1;
-  const int ka = share ? (int)std::min<int64_t>(4, ncand) : 0;
+  // On the LB path phase A joins phase B's single launch: the top ranks are its first
+  // items, and their long DPs no longer leave the GPU idle at a launch boundary.
+  const bool one_launch = use_lb && kind_tag(spec->kind) == K_DTW;
+  const int ka = (share && !one_launch) ? (int)std::min<int64_t>(4, ncand) : 0;
   if (ka > 0) {
     if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
@@ -660,14 +663,13 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // phase B, one launch of two segments: the next-best 64 ranks (where the survivors
   // concentrate) one pair per item for load balance, the rest in items of 8
   // (64 / 8 measured best on C2 against 32..128 / 4..32)
-  const int kb1 = (int)std::min<int64_t>(ncand, ka + 64);
+  const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? 4 : ka) + 64);
   const NNFn fnB = pick_nn(spec->kind, spec->cost_mode, engB);
   const size_t smemB = pair_smem(max_len, engB, wpb);
   // With the LB pre-test most pairs are cheap and the first segment's tail of long DPs
   // would idle the GPU, so both segments share one launch.  Without it (MSM, TWE, ...)
   // every pair runs the DP and the second segment waits for the first one's cutoffs.
   // (a single launch needs k_nn's TWO_SEG, i.e. the dtw kernels)
-  const bool one_launch = use_lb && kind_tag(spec->kind) == K_DTW;
   const int seg_lo[2] = {ka, kb1}, seg_mid[2] = {kb1, (int)ncand};
   for (int sgi = 0; sgi < (one_launch ? 1 : 2); ++sgi) {
     const int lo = one_launch ? ka : seg_lo[sgi], mid = one_launch ? kb1 : seg_mid[sgi];
