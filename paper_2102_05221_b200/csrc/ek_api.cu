@@ -877,9 +877,23 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   mark_reset();
   mark(st, "start");
   const int nl_ = plan.nleaves;
-  // z-normalisation statistics of every window (thread per window)
-  DBuf dstats;
-  if (normalize) {
+  const bool use_lb = share && lq * 5 * sizeof(double) <= 200 * 1024;
+  // z-normalisation statistics: with the LB pass, double-double prefix sums for its
+  // approximate statistics and numpy-exact ones on demand (sampled seeds, survivors);
+  // without it every window runs the DP, so every window's exact statistics
+  DBuf dstats, dplocal, dpseg;
+  const int nseg = (int)((nref + kPrefixSeg - 1) / kPrefixSeg);
+  const int st_wpb = 4;
+  const size_t st_smem = sizeof(double) * (size_t)st_wpb * (nl_ + 16);
+  if (normalize && use_lb) {
+    if (dstats.alloc(sizeof(double2) * (size_t)nwin, st) || dplocal.alloc(sizeof(double) * 6 * (size_t)nref, st) ||
+        dpseg.alloc(sizeof(double) * 6 * (size_t)nseg, st))
+      return -1;
+    if (launch_plain(k_prefix_dd<0>, dim3((unsigned)nseg), dim3(256), 0, st, dref, (long long)nref,
+                     dplocal.as<double>(), dpseg.as<double>(), nseg) ||
+        launch_plain(k_prefix_dd_segs<0>, dim3(1), dim3(256), 0, st, dpseg.as<double>(), nseg))
+      return -1;
+  } else if (normalize) {
     if (dstats.alloc(sizeof(double2) * (size_t)nwin, st)) return -1;
     const size_t ssm = sizeof(double) * (size_t)win_stats_smem((int)lq);
     if (ssm <= 200 * 1024) {
@@ -908,6 +922,11 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     const long long nsamp = std::min<long long>(nwin, 4096);
     const long long stride = std::max<long long>(1, nwin / nsamp);
     if (dukeys.alloc(sizeof(float) * nsamp, st) || dsord.alloc(sizeof(int) * nsamp, st)) return -1;
+    if (normalize && use_lb &&  // exact statistics of the sampled windows
+        launch_plain(k_win_stats_list<0>, dim3((unsigned)((nsamp + st_wpb - 1) / st_wpb)), dim3(32 * st_wpb), st_smem,
+                     st, dref, (int)lq, (const long long*)nullptr, stride, nsamp, (const int*)nullptr, plan,
+                     dstats.as<double2>()))
+      return -1;
     if (launch_plain(get_subseq_ub(spec->cost_mode), dim3((unsigned)((nsamp + 3) / 4)), dim3(128), 0, st,
                      (const double*)dqn.as<double>(), (int)lq, dref, stride, (int)normalize, wst, nsamp,
                      dukeys.as<float>(), dcut.as<unsigned long long>()))
@@ -925,7 +944,6 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   }
   mark(st, "seed_bounds");
   // LB_Keogh envelope of the query (search.py:185-187) and the test order
-  const bool use_lb = share && lq * 5 * sizeof(double) <= 200 * 1024;
   const float2* env = nullptr;
   if (use_lb) {
     if (denv.alloc(sizeof(float2) * (size_t)lq, st) || dzero.alloc(8, st)) return -1;
@@ -966,11 +984,19 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     if (dsurv.alloc(sizeof(long long) * (size_t)nwin, st) || dns.alloc(16, st)) return -1;
     CK(cudaMemsetAsync(dns.p, 0, 16, st));
     if (launch_persistent(get_subseq_lb(spec->cost_mode), 256, sizeof(double) * (size_t)subseq_lb_smem((int)lq), st,
-                          (nwin + 31) / 32, dref, (int)lq, (int)normalize, wst, env, (const int*)dlbo.as<int>(), nwin,
+                          (nwin + 31) / 32, dref, (int)lq, (int)normalize, (const double*)dplocal.as<double>(),
+                          (const double*)dpseg.as<double>(), (long long)nref, nseg, env, (const int*)dlbo.as<int>(),
+                          nwin,
                           (const unsigned long long*)dcut.as<unsigned long long>(), dout.as<double>(),
                           dtend.as<int>(), dsurv.as<long long>(), dns.as<int>(), dcnt.as<int>() + 2))
       return -1;
     mark(st, "subseq_lb");
+    if (normalize &&  // exact statistics of the survivors for their DP
+        launch_plain(k_win_stats_list<0>, dim3((unsigned)(g_ctx.nsm * 8)), dim3(32 * st_wpb), st_smem, st, dref,
+                     (int)lq, (const long long*)dsurv.as<long long>(), 0LL, nwin, (const int*)dns.as<int>(), plan,
+                     dstats.as<double2>()))
+      return -1;
+    mark(st, "survivor_stats");
     if (launch_persistent(fn, 32 * wpb, smem, st, nwin, qn_, (int)lq, dref, (int)normalize, wst,
                           (const long long*)dsurv.as<long long>(), nwin, (const int*)dns.as<int>(), 1, win,
                           (int)share, dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
