@@ -433,3 +433,20 @@ def test_long_series_nn_and_pairwise(gpu, kind):
     D, _ = gpu.pairwise(spec, C[:8])
     Do, _ = eko.pairwise(spec, C[:8], threads=16)
     assert np.array_equal(D, Do)
+
+
+@pytest.mark.parametrize("offset,scale", [(1e7, 1e-3), (1e4, 1.0), (0.0, 1e-9), (-3e5, 50.0)])
+def test_subseq_lb_statistics_regimes(gpu, rng, offset, scale):
+    """The LB pass's prefix-sum statistics across numeric regimes: huge offsets with a
+    tiny spread (the bound gives up and the DP decides), near-zero-std windows, wide
+    walks -- best window and distance equal the oracle's (z-normalised search)."""
+    n, lq = 6000, 200
+    stream = offset + scale * np.cumsum(rng.normal(0, 1, n))
+    stream[2000:2300] = offset  # a flat run: std < 1e-12 windows
+    q = stream[4100:4100 + lq] + scale * 0.01 * rng.normal(0, 1, lq)
+    for kind, w in (("cdtw", 10), ("dtw", None)):
+        spec = gpu.DistanceSpec(kind=kind, window=w)
+        for variant in ("eapruned", "ea"):
+            got = gpu.subsequence_search(q, stream, gpu.SearchConfig(spec=spec, variant=variant, normalize=True))[:2]
+            want = eko.subsequence(spec, "eapruned", q, stream, True, chunk=500, threads=16)[:2]
+            assert got == want, (kind, variant, got, want)
