@@ -973,22 +973,26 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     DBuf dso, dst;
     if (dso.alloc(8 * ns, st) || dst.alloc(4 * ns, st)) return -1;
     if (launch_persistent(fn, 32 * wpb, smem, st, ns, qn_, (int)lq, dref, (int)normalize, wst,
-                          (const long long*)dseed.as<long long>(), ns, (const int*)nullptr, 0, win, (int)share,
+                          (const long long*)dseed.as<long long>(), (const float*)nullptr, ns, (const int*)nullptr, 0,
+                          win, (int)share,
                           dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
       return -1;
   }
   mark(st, "subseq_phaseA");
   if (env) {
     // phase B1: LB_Keogh test of every window (lane per window); B2: DP of the survivors
-    DBuf dsurv, dns;
-    if (dsurv.alloc(sizeof(long long) * (size_t)nwin, st) || dns.alloc(16, st)) return -1;
+    DBuf dsurv, dsurvlb, dns;
+    if (dsurv.alloc(sizeof(long long) * (size_t)nwin, st) || dsurvlb.alloc(sizeof(float) * (size_t)nwin, st) ||
+        dns.alloc(16, st))
+      return -1;
     CK(cudaMemsetAsync(dns.p, 0, 16, st));
     if (launch_persistent(get_subseq_lb(spec->cost_mode), 256, sizeof(double) * (size_t)subseq_lb_smem((int)lq), st,
                           (nwin + 31) / 32, dref, (int)lq, (int)normalize, (const double*)dplocal.as<double>(),
                           (const double*)dpseg.as<double>(), (long long)nref, nseg, env, (const int*)dlbo.as<int>(),
                           nwin,
                           (const unsigned long long*)dcut.as<unsigned long long>(), dout.as<double>(),
-                          dtend.as<int>(), dsurv.as<long long>(), dns.as<int>(), dcnt.as<int>() + 2))
+                          dtend.as<int>(), dsurv.as<long long>(), dsurvlb.as<float>(), dns.as<int>(),
+                          dcnt.as<int>() + 2))
       return -1;
     mark(st, "subseq_lb");
     if (normalize &&  // exact statistics of the survivors for their DP
@@ -998,13 +1002,15 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
       return -1;
     mark(st, "survivor_stats");
     if (launch_persistent(fn, 32 * wpb, smem, st, nwin, qn_, (int)lq, dref, (int)normalize, wst,
-                          (const long long*)dsurv.as<long long>(), nwin, (const int*)dns.as<int>(), 1, win,
+                          (const long long*)dsurv.as<long long>(), (const float*)dsurvlb.as<float>(), nwin,
+                          (const int*)dns.as<int>(), 1, win,
                           (int)share, dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
                           dcnt.as<int>() + 4))
       return -1;
   } else {
     if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, qn_, (int)lq, dref, (int)normalize, wst,
-                          (const long long*)nullptr, nwin, (const int*)nullptr, 0, win, (int)share,
+                          (const long long*)nullptr, (const float*)nullptr, nwin, (const int*)nullptr, 0, win,
+                          (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
       return -1;
   }

@@ -53,7 +53,9 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   const bool lane_on = jbase < nc;
 
   auto cy = [&](int k) { return Y.at(min(max(k, -1), nc)); };  // column records: once per pair
-  auto cx = [&](int k) { return X.at(k); };                      // rows: padded by >= 40
+  // rows: lanes run up to 62 rows ahead of / behind the matrix; clamp to the pads (the
+  // +inf pad past the end, a finite one before it) so those rows stay +inf
+  auto cx = [&](int k) { return X.at(min(max(k, -1), nl)); };
 
   ColD<KIND> cols[S];
   double val[S];
@@ -278,7 +280,7 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
   const int r0 = BORDERED ? 0 : 1;
   const int nstrips = (nc + STRIP - 1) / STRIP;
   auto cy = [&](int k) { return Y.at(min(max(k, -1), nc)); };
-  auto cx = [&](int k) { return X.at(k); };
+  auto cx = [&](int k) { return X.at(min(max(k, -1), nl)); };  // see stripe_pair
   double nextcut = cut;
   int cut_hi = hi_word(cut);
   int steps_done = 0;
