@@ -107,6 +107,13 @@ int ek_subseq_dev(const ek_spec* spec, int32_t variant, const double* d_query, i
 int ek_subseq_profile(const ek_spec* spec, const double* query, int64_t lq, const double* reference, int64_t n_ref,
                       int32_t normalize, double* window_dist);
 
+/* Batched build_envelope (lower_bounds.py:23-57): for n series of equal length L
+ * (series[off[s] .. off[s] + L)), upper / lower[s * L + i] = max / min of the series
+ * over [i - window, i + window] (clipped), bit-identical to the reference's deque.
+ * The GPU 1-NN path builds the same envelopes internally (rounded outward to floats). */
+int ek_envelopes(const double* series, int64_t total, const int64_t* off, int64_t n, int64_t L, int64_t window,
+                 double* upper, double* lower);
+
 /* Number of kernel launches the library issued since the last reset (bench accounting). */
 int64_t ek_launch_count(int32_t reset);
 

@@ -58,6 +58,7 @@ EXPORTS = {
     "ek_subseq_dev": ([C.POINTER(EkSpec), C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                        _i64p, _dp, _i64p, _i64p, _i64p, C.c_void_p], C.c_int),
     "ek_subseq_profile": ([C.POINTER(EkSpec), _dp, C.c_int64, _dp, C.c_int64, C.c_int32, _dp], C.c_int),
+    "ek_envelopes": ([_dp, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int64, _dp, _dp], C.c_int),
 }
 
 _lock = threading.Lock()

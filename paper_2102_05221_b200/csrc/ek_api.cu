@@ -569,7 +569,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
   const long long npairs = (long long)nq * ncand;
-  DBuf dord, dkeys, dout, dtend, dcut, dcnt, denv, denvq;
+  DBuf dord, dkeys, dout, dtend, dcut, dcnt, denv, denvq, denvs;
   if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dout.alloc(sizeof(double) * (size_t)npairs, st) ||
       dtend.alloc(sizeof(int) * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
       dcnt.alloc(sizeof(int) * 16, st))
@@ -595,11 +595,14 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       return -1;
     CK(cudaEventRecord(g_ctx.ev_fork, st));
     CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_fork, 0));
-    if (launch_plain(k_envelope, dim3((unsigned)ncand), dim3(256), sizeof(double) * 5 * (size_t)L, g_ctx.side, dC,
-                     (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>()) ||
-        launch_plain(k_envelope, dim3((unsigned)nq), dim3(256), sizeof(double) * 5 * (size_t)L, g_ctx.side, dQ,
-                     (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>()))
-      return -1;
+    void* scr = nullptr;  // long series: global table rows
+    if (env_scratch_bytes(L, false)) {
+      if (denvs.alloc(env_scratch_bytes(L, false), st)) return -1;
+      scr = denvs.p;
+    }
+    CK(envelope(dC, (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>(), scr, g_ctx.side));
+    CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr, g_ctx.side));
+    g_launches += 2;
     CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
     env = denv.as<float2>();
   }
@@ -617,7 +620,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
         launch_plain(k_paa, blocks((long long)ncand * D), dim3(256), 0, st, dC, (const long long*)dcoff,
                      (const int*)dclen, (int)ncand, R, D, dcp.as<float>()))
       return -1;
-    if (launch_plain(k_rank_paa, dim3((unsigned)((ncand + 63) / 64), (unsigned)((nq + 63) / 64)), dim3(256), 0, st,
+    if (launch_plain(k_rank_paa, dim3((unsigned)((ncand + 63) / 64), (unsigned)((nq + 31) / 32)), dim3(256), 0, st,
                      (const float*)dqp.as<float>(), (int)nq, (const float*)dcp.as<float>(), (int)ncand, D,
                      dkeys.as<float>()))
       return -1;
@@ -907,7 +910,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   }
   const double2* wst = normalize ? (const double2*)dstats.as<double2>() : nullptr;
   // the query, normalised once (search.py:181-182)
-  DBuf dqn, denv, dzero, dkeys, dlbo;
+  DBuf dqn, denv, denvs, dzero, dkeys, dlbo;
   if (dqn.alloc(sizeof(double) * (size_t)lq, st)) return -1;
   if (launch_plain(k_subseq_query<0>, dim3(1), dim3(32), sizeof(double) * ((size_t)lq + nl_ + 16), st, dq, (int)lq,
                    (int)normalize, plan, dqn.as<double>()))
@@ -948,10 +951,14 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   if (use_lb) {
     if (denv.alloc(sizeof(float2) * (size_t)lq, st) || dzero.alloc(8, st)) return -1;
     CK(cudaMemsetAsync(dzero.p, 0, 8, st));
-    if (launch_plain(k_envelope, dim3(1), dim3(256), sizeof(double) * 5 * (size_t)lq, st,
-                     (const double*)dqn.as<double>(), (const long long*)dzero.as<long long>(), (int)lq, 1,
-                     win < 0 ? (int)lq : win, denv.as<float2>()))
-      return -1;
+    void* scr = nullptr;
+    if (env_scratch_bytes((int)lq, false)) {
+      if (denvs.alloc(env_scratch_bytes((int)lq, false), st)) return -1;
+      scr = denvs.p;
+    }
+    CK(envelope((const double*)dqn.as<double>(), (const long long*)dzero.as<long long>(), (int)lq, 1,
+                win < 0 ? (int)lq : win, denv.as<float2>(), scr, st));
+    ++g_launches;
     env = denv.as<float2>();
     // positions by decreasing envelope excess (k_rank_sort on one row)
     if (dkeys.alloc(sizeof(float) * (size_t)lq, st) || dlbo.alloc(sizeof(int) * (size_t)lq, st)) return -1;
@@ -1079,6 +1086,35 @@ int ek_subseq(const ek_spec* spec, int32_t variant, const double* query, int64_t
   if (inputs_finite(dq.as<double>(), lq, dr.as<double>(), n_ref, st)) return -1;
   return subseq_dev_impl(spec, variant, dq.as<double>(), lq, dr.as<double>(), n_ref, normalize, best_off, best_dist,
                          cells, computed, abandoned, st);
+}
+
+int ek_envelopes(const double* series, int64_t total, const int64_t* off, int64_t n, int64_t L, int64_t window,
+                 double* upper, double* lower) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  cudaStream_t st = g_ctx.stream;
+  if (n < 0 || L < 1 || L > (1LL << 30) || window < 0) return fail("invalid envelope batch (n=%lld, L=%lld, window=%lld)",
+                                                                   (long long)n, (long long)L, (long long)window);
+  if (n == 0) return 0;
+  if (!series || !off || !upper || !lower) return fail("null argument");
+  for (int64_t s = 0; s < n; ++s)
+    if (off[s] < 0 || off[s] + L > total) return fail("series %lld lies outside the buffer", (long long)s);
+  const size_t out = sizeof(double) * (size_t)n * (size_t)L;
+  DBuf dx, doff, dup, ddn, dscr;
+  if (dx.alloc(sizeof(double) * (size_t)total, st) || doff.alloc(sizeof(int64_t) * (size_t)n, st) ||
+      dup.alloc(out, st) || ddn.alloc(out, st))
+    return -1;
+  if (env_scratch_bytes((int)L, true) && dscr.alloc(env_scratch_bytes((int)L, true), st)) return -1;
+  CK(cudaMemcpyAsync(dx.p, series, sizeof(double) * (size_t)total, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(doff.p, off, sizeof(int64_t) * (size_t)n, cudaMemcpyHostToDevice, st));
+  if (inputs_finite(dx.as<double>(), total, dx.as<double>(), 0, st)) return -1;
+  CK(envelope_exact(dx.as<double>(), doff.as<long long>(), (int)L, (int)n, (int)std::min<int64_t>(window, L),
+                    dup.as<double>(), ddn.as<double>(), env_scratch_bytes((int)L, true) ? dscr.p : nullptr, st));
+  ++g_launches;
+  CK(cudaMemcpyAsync(upper, dup.p, out, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(lower, ddn.p, out, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
 }
 
 int ek_subseq_profile(const ek_spec* spec, const double* query, int64_t lq, const double* reference, int64_t n_ref,

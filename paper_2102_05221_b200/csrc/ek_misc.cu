@@ -3,6 +3,8 @@
 // lexicographic (distance, index) reduction, and computed-cell accounting.
 #include "ek_misc.cuh"
 #include <cub/block/block_radix_sort.cuh>
+#include <algorithm>
+#include <type_traits>
 
 namespace ekb {
 
@@ -65,33 +67,36 @@ __global__ void k_paa(const double* __restrict__ src, const long long* __restric
   }
 }
 
-// Squared Euclidean distance between PAA rows (FP32), 64x64 (query, candidate) tile per
-// block, 4x4 per thread, D in chunks of 16 through shared memory.  Ranking only.
+// Squared Euclidean distance between PAA rows (FP32), 32x64 (query, candidate) tile per
+// block (enough blocks to fill 148 SMs at 256 x 4096), 2x4 per thread, D in chunks of
+// 16 through shared memory.  Ranking only.
 __global__ void __launch_bounds__(256) k_rank_paa(const float* __restrict__ Qp, int nq, const float* __restrict__ Cp,
                                                   int ncand, int D, float* __restrict__ out) {
-  __shared__ float qs[16][65];
+  __shared__ float qs[16][33];
   __shared__ float cs[16][65];
-  const int q0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  const int q0 = blockIdx.y * 32, c0 = blockIdx.x * 64;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][4] = {};
+  float acc[2][4] = {};
   for (int kb = 0; kb < D; kb += 16) {
     for (int e = threadIdx.x; e < 64 * 16; e += 256) {
       const int r = e >> 4, k = e & 15;
-      const int q = q0 + r, c = c0 + r, kk = kb + k;
-      qs[k][r] = (q < nq && kk < D) ? Qp[(long long)q * D + kk] : 0.f;
+      const int c = c0 + r, kk = kb + k;
       cs[k][r] = (c < ncand && kk < D) ? Cp[(long long)c * D + kk] : 0.f;
+      if (r < 32) {
+        const int q = q0 + r;
+        qs[k][r] = (q < nq && kk < D) ? Qp[(long long)q * D + kk] : 0.f;
+      }
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      float a[4], b[4];
+      float a[2], b[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = qs[k][ty + 16 * u];
-        b[u] = cs[k][tx + 16 * u];
-      }
+      for (int u = 0; u < 2; ++u) a[u] = qs[k][ty + 16 * u];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int v = 0; v < 4; ++v) b[v] = cs[k][tx + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const float d = a[u] - b[v];
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(256) k_rank_paa(const float* __restrict__ Qp, 
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int q = q0 + ty + 16 * u, c = c0 + tx + 16 * v;
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(THREADS) k_rank_radix(const float* __restrict_
     k[u] = key != key ? __int_as_float(0x7f800000) : key;  // NaN ranks last
     v[u] = i;
   }
-  Sort(tmp).Sort(k, v);
+  Sort(tmp).Sort(k, v, 16, 32);  // top 16 key bits (~1% buckets): order is a schedule only
 #pragma unroll
   for (int u = 0; u < ITEMS; ++u) {
     const int i = threadIdx.x * ITEMS + u;
@@ -245,58 +250,128 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const double* __restrict__ di
 }
 
 // Sliding max/min over [k-w, k+w] (build_envelope, lower_bounds.py:23-57) for every
-// candidate, row-major (env[c * L + k] = (upper, lower)) so a warp reads 32
-// consecutive points; stored as floats rounded outward (upper up, lower down).  One block per candidate: doubling max/min tables in shared
-// memory give max(x[s .. s+2w]) (clamped); windows cut by the left edge are scanned
-// directly; a window covering the whole series is the global max/min.
-__global__ void __launch_bounds__(256) k_envelope(const double* __restrict__ C, const long long* __restrict__ coff,
-                                                  int L, int ncand, int w, float2* __restrict__ env) {
-  extern __shared__ double sm[];
-  double* x = sm;
-  double* mx = sm + L;
-  double* mn = sm + 2 * L;
-  double* tmx = sm + 3 * L;
-  double* tmn = sm + 4 * L;
-  const int c = blockIdx.x;
-  const double* src = C + coff[c];
-  for (int k = threadIdx.x; k < L; k += blockDim.x) x[k] = mx[k] = mn[k] = src[k];
-  __syncthreads();
-  const long long want = 2LL * w + 1;
-  int span = 1;
-  while (span < want && span < L) {
-    const int step = (int)min((long long)span, want - span);
-    for (int k = threadIdx.x; k < L; k += blockDim.x) {
-      const int k2 = min(k + step, L - 1);
-      tmx[k] = fmax(mx[k], mx[k2]);
-      tmn[k] = fmin(mn[k], mn[k2]);
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < L; k += blockDim.x) {
-      mx[k] = tmx[k];
-      mn[k] = tmn[k];
-    }
-    __syncthreads();
-    span += step;
-  }
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    double u, l;
-    if (k >= w) {  // [k-w, min(k+w, L-1)] == table run starting at k-w
-      u = mx[k - w];
-      l = mn[k - w];
-    } else if ((long long)k + w >= L - 1) {  // the whole series
-      u = mx[0];
-      l = mn[0];
-    } else {  // [0, k+w], shorter than the table's runs
-      u = x[0];
-      l = x[0];
-      for (int j = 1; j <= k + w; ++j) {
-        u = fmax(u, x[j]);
-        l = fmin(l, x[j]);
+// series, row-major (env[c * L + k] = (upper, lower)) so a warp reads 32 consecutive
+// points; stored as floats rounded outward (upper up, lower down).  Rounding is
+// monotone, so it is applied first and the tables hold floats.
+//
+// Sparse table per series: level p holds max/min of x[k .. k + 2^p - 1].  A clipped
+// window [a, b] of length n is covered by two level-floor(log2 n) runs,
+// max(T[a], T[b - 2^p + 1]).  Window lengths lie in [min(w+1, L), min(2w+1, L)], a
+// factor-of-two range, so only levels pmin and pmin + 1 are needed: level pmin is
+// built in place (rows processed in increasing chunks of the block, each read before
+// any write of its chunk), level pmin + 1 goes to a second pair of rows.  16 L bytes
+// per series: shared memory, or the global `scratch` rows (16 L bytes per block) when
+// L is too long for it.  Blocks stride over the series.
+template <class T>
+__device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }  // no NaNs here (finite inputs)
+template <class T>
+__device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+
+// EXACT = false: float tables, float2 (upper, lower) output for the LB kernels.
+// EXACT = true: double tables, the envelope itself (build_envelope's upper / lower).
+template <bool EXACT>
+__global__ void __launch_bounds__(kEnvThreads) k_envelope(const double* __restrict__ C,
+                                                          const long long* __restrict__ coff, int L, int nser, int w,
+                                                          float2* __restrict__ env, double* __restrict__ up,
+                                                          double* __restrict__ dn, void* __restrict__ scratch) {
+  using T = typename std::conditional<EXACT, double, float>::type;
+  extern __shared__ __align__(16) unsigned char env_sm[];
+  T* const hi = scratch ? static_cast<T*>(scratch) + (size_t)blockIdx.x * 4 * L : reinterpret_cast<T*>(env_sm);
+  T* const lo = hi + L;
+  T* const hi2 = hi + 2 * L;
+  T* const lo2 = hi + 3 * L;
+  const int W = min(w, L - 1);
+  const int pmin = 31 - __clz(min(W + 1, L)), pmax = 31 - __clz(min(2 * W + 1, L));
+  constexpr int R = 4, CH = kEnvThreads * R;
+  for (int c = blockIdx.x; c < nser; c += gridDim.x) {
+    const double* src = C + coff[c];
+    for (int k = threadIdx.x; k < L; k += kEnvThreads) {
+      const double x = src[k];
+      if constexpr (EXACT) {
+        hi[k] = x;
+        lo[k] = x;
+      } else {
+        hi[k] = __double2float_ru(x);
+        lo[k] = __double2float_rd(x);
       }
     }
-    // float with outward rounding: a wider envelope keeps lb_keogh a lower bound
-    env[(long long)c * L + k] = make_float2(__double2float_ru(u), __double2float_rd(l));
+    for (int p = 1; p <= pmax; ++p) {
+      const int s = 1 << (p - 1), n = L - (1 << p) + 1;  // entries of level p
+      const bool inplace = p <= pmin;
+      T* const dh = inplace ? hi : hi2;
+      T* const dl = inplace ? lo : lo2;
+      for (int base = 0; base < n; base += CH) {
+        T vh[R], vl[R];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = base + r * kEnvThreads + threadIdx.x;
+          if (k < n) {
+            vh[r] = tmax(hi[k], hi[k + s]);
+            vl[r] = tmin(lo[k], lo[k + s]);
+          }
+        }
+        if (inplace) __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = base + r * kEnvThreads + threadIdx.x;
+          if (k < n) {
+            dh[k] = vh[r];
+            dl[k] = vl[r];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < L; k += kEnvThreads) {
+      const int a = max(k - W, 0), b = min(k + W, L - 1);
+      const int p = 31 - __clz(b - a + 1);
+      const T* th = p == pmin ? hi : hi2;
+      const T* tl = p == pmin ? lo : lo2;
+      const int b2 = b - (1 << p) + 1;
+      const long long o = (long long)c * L + k;
+      if constexpr (EXACT) {
+        up[o] = tmax(th[a], th[b2]);
+        dn[o] = tmin(tl[a], tl[b2]);
+      } else {
+        env[o] = make_float2(tmax(th[a], th[b2]), tmin(tl[a], tl[b2]));
+      }
+    }
+    __syncthreads();
   }
+}
+
+size_t env_smem_bytes(int L, bool exact) { return (exact ? 32 : 16) * (size_t)L; }
+size_t env_scratch_bytes(int L, bool exact) {
+  return env_smem_bytes(L, exact) > kEnvSmemMax ? env_smem_bytes(L, exact) * kEnvScratchBlocks : 0;
+}
+
+template <bool EXACT>
+static cudaError_t envelope_launch(const double* C, const long long* coff, int L, int nser, int w, float2* env,
+                                   double* up, double* dn, void* scratch, cudaStream_t st) {
+  if (nser <= 0 || L <= 0) return cudaSuccess;
+  const size_t sm = env_smem_bytes(L, EXACT);
+  if (env_scratch_bytes(L, EXACT)) {
+    if (!scratch) return cudaErrorInvalidValue;
+    k_envelope<EXACT><<<(unsigned)std::min(nser, kEnvScratchBlocks), kEnvThreads, 0, st>>>(C, coff, L, nser, w, env,
+                                                                                          up, dn, scratch);
+  } else {
+    if (sm > 48 * 1024) {
+      cudaError_t e =
+          cudaFuncSetAttribute((const void*)k_envelope<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+    }
+    k_envelope<EXACT><<<(unsigned)nser, kEnvThreads, sm, st>>>(C, coff, L, nser, w, env, up, dn, nullptr);
+  }
+  return cudaGetLastError();
+}
+cudaError_t envelope(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
+                     cudaStream_t st) {
+  return envelope_launch<false>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
+}
+cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
+                           void* scratch, cudaStream_t st) {
+  return envelope_launch<true>(C, coff, L, nser, w, nullptr, up, dn, scratch, st);
 }
 
 }  // namespace ekb

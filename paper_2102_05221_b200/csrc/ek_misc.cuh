@@ -4,7 +4,19 @@
 
 namespace ekb {
 
-__global__ void k_envelope(const double* C, const long long* coff, int L, int ncand, int w, float2* env);
+// Envelopes (k_envelope): sparse-table rows in shared memory up to kEnvSmemMax bytes
+// per series, else global scratch rows (env_scratch_bytes(L, exact); kEnvScratchBlocks
+// blocks).  envelope(): float2 (upper rounded up, lower rounded down) for the LB
+// kernels; envelope_exact(): build_envelope's double upper / lower.
+constexpr int kEnvThreads = 128;
+constexpr int kEnvScratchBlocks = 592;  // 4 x 148 SMs
+constexpr size_t kEnvSmemMax = 192 * 1024;
+size_t env_smem_bytes(int L, bool exact);
+size_t env_scratch_bytes(int L, bool exact);
+cudaError_t envelope(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
+                     cudaStream_t st);
+cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
+                           void* scratch, cudaStream_t st);
 
 __global__ void k_rank_dist(const double* Q, const long long* qoff, const int* qlen, int nq, const double* C,
                             const long long* coff, const int* clen, int ncand, float* out);

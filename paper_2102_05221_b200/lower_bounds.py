@@ -79,3 +79,27 @@ def lb_keogh2(q, c, env_c: Envelope, env_q: Envelope, cutoff: float = np.inf,
         return first
     second = lb_keogh(c, env_q, cost_mode)
     return max(first, second) if second > first else first
+
+
+def build_envelopes(batch, window: int) -> list[Envelope]:
+    """build_envelope for a batch of equal-length series in one GPU call
+    (csrc/ek_misc.cu k_envelope, exact double tables); same values as the host
+    function and the reference.  Raises DimensionError for ragged batches."""
+    from . import _lib
+    from .search import _pack
+
+    if window < 0:
+        raise ValueError("window must be >= 0")
+    flat, off, lens = _pack(batch)
+    n = len(lens)
+    if n == 0:
+        return []
+    if np.any(lens != lens[0]):
+        raise DimensionError("build_envelopes needs series of one length")
+    length = int(lens[0])
+    up = np.empty((n, length), dtype=np.float64)
+    lo = np.empty((n, length), dtype=np.float64)
+    L = _lib.lib()
+    _lib.check(L.ek_envelopes(_lib.dptr(flat), len(flat), _lib.iptr(off), n, length, int(window), _lib.dptr(up),
+                              _lib.dptr(lo)))
+    return [Envelope(upper=up[k], lower=lo[k], window=window) for k in range(n)]

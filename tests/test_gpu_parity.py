@@ -450,3 +450,32 @@ def test_subseq_lb_statistics_regimes(gpu, rng, offset, scale):
             got = gpu.subsequence_search(q, stream, gpu.SearchConfig(spec=spec, variant=variant, normalize=True))[:2]
             want = eko.subsequence(spec, "eapruned", q, stream, True, chunk=500, threads=16)[:2]
             assert got == want, (kind, variant, got, want)
+
+
+@pytest.mark.parametrize("length,window", [(1, 0), (7, 3), (100, 0), (100, 1), (128, 51), (512, 51), (300, 299),
+                                           (300, 5000), (1000, 127), (7000, 64), (7000, 3000)])
+def test_build_envelopes_match_host(gpu, rng, length, window):
+    """Batched GPU envelopes (k_envelope, exact tables; shared memory and, past 6144
+    points, global scratch rows) equal build_envelope's values."""
+    from paper_2102_05221_b200 import lower_bounds as lbm
+
+    X = np.cumsum(rng.normal(0, 1, (5, length)), axis=1)
+    X[1] = np.round(X[1])  # ties
+    got = lbm.build_envelopes(X, window)
+    for k in range(len(X)):
+        want = lbm.build_envelope(X[k], window)
+        assert np.array_equal(got[k].upper, want.upper), (k, length, window)
+        assert np.array_equal(got[k].lower, want.lower), (k, length, window)
+
+
+def test_nn_lb_long_series_scratch_envelope(gpu):
+    """cdtw 1-NN on 13000-point series: the LB envelopes exceed shared memory and are
+    built in global scratch rows; the answer must equal the oracle's."""
+    from paper_2102_05221_b200 import datagen
+
+    C, cl, protos = datagen.warped_prototypes(7, 13000, 3, 0.2, 61)
+    Q, ql, _ = datagen.warped_prototypes(2, 13000, 3, 0.2, 62, protos=protos)
+    spec = gpu.DistanceSpec(kind="cdtw", window=20)
+    idx, dist = gpu.nn_batch(spec, "eapruned", Q, C)[:2]
+    r = eko.nn(spec, "eapruned", Q, C, threads=16)
+    assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"])
