@@ -18,9 +18,9 @@ using RefFn = void (*)(const double*, const PairDesc*, int, int, Params, double*
 using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, Params, unsigned long long*);
 
-// diagonal_upper_bound (engines.py:87-103): the diagonal then the last column, summed
-// sequentially in DP order, used to seed a query's cutoff with an exact path cost.
-// One warp per query: lanes evaluate 32 terms at a time, lane 0 adds them in order.
+// diagonal_upper_bound (engines.py:87-103): the diagonal then the last column, the
+// cost of one admissible path, seeds a query's cutoff.  One warp per query, terms
+// summed in parallel and rounded up (k_ub_init).
 template <int KIND, int MODE>
 __device__ __forceinline__ double ub_term(const double* X, const double* Y, int nc, int k, const Params& pp) {
   auto xv = [&](int i) { return i < 0 ? pad_before<KIND>(X[0]) : X[i]; };
@@ -52,7 +52,6 @@ __global__ void __launch_bounds__(128) k_ub_init(const double* __restrict__ Q, c
                                                  const long long* __restrict__ coff, const int* __restrict__ clen,
                                                  int ncand, const int* __restrict__ order, int win, Params prm,
                                                  unsigned long long* cutbits) {
-  __shared__ double terms[4][32];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * 4 + wib;
   if (q >= nq) return;
@@ -68,17 +67,15 @@ __global__ void __launch_bounds__(128) k_ub_init(const double* __restrict__ Q, c
     return;
   }
   const Params pp = pair_params(prm, nl);
+  // Every term is >= 0.  Summed in any order with every addition rounded up, the total
+  // is >= the exact path cost; one more relative 2^-24 (rounded up) covers the
+  // round-to-nearest error of the DP's own in-order sum (<= ~n 2^-53, n < 2^29), so
+  // the seed is never below the candidate's DP value -- it stays a valid cutoff.
   double total = 0.0;
-  for (int base = 1; base <= nl; base += 32) {
-    const int k = base + lane;
-    terms[wib][lane] = (k <= nl) ? ub_term<KIND, MODE>(X, Y, nc, k, pp) : 0.0;
-    __syncwarp();
-    if (lane == 0) {
-      const int m = min(32, nl - base + 1);
-      for (int u = 0; u < m; ++u) total = dadd(total, terms[wib][u]);
-    }
-    __syncwarp();
-  }
+  for (int k = 1 + lane; k <= nl; k += 32) total = __dadd_ru(total, ub_term<KIND, MODE>(X, Y, nc, k, pp));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total = __dadd_ru(total, __shfl_xor_sync(FULL, total, o));
+  total = __dmul_ru(total, 1.0 + 0x1p-24);
   if (lane == 0) cutbits[q] = (unsigned long long)__double_as_longlong(total);
 }
 

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(256) k_rank_paa(const float* __restrict__ Qp, 
 // (ties keep index order).  THREADS x ITEMS >= ncand; padding sorts last.
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS) k_rank_radix(const float* __restrict__ keys, int ncand,
-                                                        int* __restrict__ order) {
+                                                        int* __restrict__ order, int lo_bit) {
   using Sort = cub::BlockRadixSort<float, THREADS, ITEMS, int>;
   extern __shared__ __align__(16) unsigned char rank_sm[];
   auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(rank_sm);
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(THREADS) k_rank_radix(const float* __restrict_
     k[u] = key != key ? __int_as_float(0x7f800000) : key;  // NaN ranks last
     v[u] = i;
   }
-  Sort(tmp).Sort(k, v, 16, 32);  // top 16 key bits (~1% buckets): order is a schedule only
+  Sort(tmp).Sort(k, v, lo_bit, 32);
 #pragma unroll
   for (int u = 0; u < ITEMS; ++u) {
     const int i = threadIdx.x * ITEMS + u;
@@ -142,19 +142,20 @@ __global__ void __launch_bounds__(THREADS) k_rank_radix(const float* __restrict_
 }
 // launched from this unit (a template kernel's host stub must live with its definition)
 cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st) {
+  const int lo_bit = 16;  // top 16 key bits (~1% buckets): the order is a schedule only
   if (ncand <= 128 * 8) {
     using Sort = cub::BlockRadixSort<float, 128, 8, int>;
-    k_rank_radix<128, 8><<<nq, 128, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order);
+    k_rank_radix<128, 8><<<nq, 128, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order, lo_bit);
   } else if (ncand <= 256 * 16) {
     using Sort = cub::BlockRadixSort<float, 256, 16, int>;
-    k_rank_radix<256, 16><<<nq, 256, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order);
+    k_rank_radix<256, 16><<<nq, 256, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order, lo_bit);
   } else {
     using Sort = cub::BlockRadixSort<float, 1024, 16, int>;
     const size_t sm = sizeof(typename Sort::TempStorage);
     cudaError_t e = cudaFuncSetAttribute((const void*)k_rank_radix<1024, 16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    k_rank_radix<1024, 16><<<nq, 1024, sm, st>>>(keys, ncand, order);
+    k_rank_radix<1024, 16><<<nq, 1024, sm, st>>>(keys, ncand, order, lo_bit);
   }
   return cudaGetLastError();
 }
@@ -267,16 +268,20 @@ __device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }  // no NaN
 template <class T>
 __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
 
-// EXACT = false: float tables, float2 (upper, lower) output for the LB kernels.
-// EXACT = true: double tables, the envelope itself (build_envelope's upper / lower).
-template <bool EXACT>
+// FMT (EnvFmt): kEnvPlain float2 (upper, lower); kEnvExact double tables,
+// build_envelope's upper / lower.  GLOBAL: table
+// rows in `scratch` (a compile-time choice, so shared-memory accesses stay LDS/STS).
+template <int FMT, bool GLOBAL>
 __global__ void __launch_bounds__(kEnvThreads) k_envelope(const double* __restrict__ C,
                                                           const long long* __restrict__ coff, int L, int nser, int w,
-                                                          float2* __restrict__ env, double* __restrict__ up,
-                                                          double* __restrict__ dn, void* __restrict__ scratch) {
+                                                          float2* __restrict__ env, double* __restrict__ up, double* __restrict__ dn,
+                                                          void* __restrict__ scratch) {
+  constexpr bool EXACT = FMT == kEnvExact;
   using T = typename std::conditional<EXACT, double, float>::type;
   extern __shared__ __align__(16) unsigned char env_sm[];
-  T* const hi = scratch ? static_cast<T*>(scratch) + (size_t)blockIdx.x * 4 * L : reinterpret_cast<T*>(env_sm);
+  T* hi;
+  if constexpr (GLOBAL) hi = static_cast<T*>(scratch) + (size_t)blockIdx.x * 4 * L;
+  else hi = reinterpret_cast<T*>(env_sm);
   T* const lo = hi + L;
   T* const hi2 = hi + 2 * L;
   T* const lo2 = hi + 3 * L;
@@ -330,11 +335,12 @@ __global__ void __launch_bounds__(kEnvThreads) k_envelope(const double* __restri
       const T* tl = p == pmin ? lo : lo2;
       const int b2 = b - (1 << p) + 1;
       const long long o = (long long)c * L + k;
+      const T u = tmax(th[a], th[b2]), l = tmin(tl[a], tl[b2]);
       if constexpr (EXACT) {
-        up[o] = tmax(th[a], th[b2]);
-        dn[o] = tmin(tl[a], tl[b2]);
+        up[o] = u;
+        dn[o] = l;
       } else {
-        env[o] = make_float2(tmax(th[a], th[b2]), tmin(tl[a], tl[b2]));
+        env[o] = make_float2(u, l);
       }
     }
     __syncthreads();
@@ -346,32 +352,33 @@ size_t env_scratch_bytes(int L, bool exact) {
   return env_smem_bytes(L, exact) > kEnvSmemMax ? env_smem_bytes(L, exact) * kEnvScratchBlocks : 0;
 }
 
-template <bool EXACT>
+template <int FMT>
 static cudaError_t envelope_launch(const double* C, const long long* coff, int L, int nser, int w, float2* env,
                                    double* up, double* dn, void* scratch, cudaStream_t st) {
   if (nser <= 0 || L <= 0) return cudaSuccess;
+  constexpr bool EXACT = FMT == kEnvExact;
   const size_t sm = env_smem_bytes(L, EXACT);
   if (env_scratch_bytes(L, EXACT)) {
     if (!scratch) return cudaErrorInvalidValue;
-    k_envelope<EXACT><<<(unsigned)std::min(nser, kEnvScratchBlocks), kEnvThreads, 0, st>>>(C, coff, L, nser, w, env,
-                                                                                          up, dn, scratch);
+    k_envelope<FMT, true><<<(unsigned)std::min(nser, kEnvScratchBlocks), kEnvThreads, 0, st>>>(C, coff, L, nser, w,
+                                                                                              env, up, dn, scratch);
   } else {
     if (sm > 48 * 1024) {
-      cudaError_t e =
-          cudaFuncSetAttribute((const void*)k_envelope<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaError_t e = cudaFuncSetAttribute((const void*)k_envelope<FMT, false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
     }
-    k_envelope<EXACT><<<(unsigned)nser, kEnvThreads, sm, st>>>(C, coff, L, nser, w, env, up, dn, nullptr);
+    k_envelope<FMT, false><<<(unsigned)nser, kEnvThreads, sm, st>>>(C, coff, L, nser, w, env, up, dn, nullptr);
   }
   return cudaGetLastError();
 }
 cudaError_t envelope(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
                      cudaStream_t st) {
-  return envelope_launch<false>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
+  return envelope_launch<kEnvPlain>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
 }
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
                            void* scratch, cudaStream_t st) {
-  return envelope_launch<true>(C, coff, L, nser, w, nullptr, up, dn, scratch, st);
+  return envelope_launch<kEnvExact>(C, coff, L, nser, w, nullptr, up, dn, scratch, st);
 }
 
 }  // namespace ekb

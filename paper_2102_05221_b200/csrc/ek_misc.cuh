@@ -8,6 +8,7 @@ namespace ekb {
 // per series, else global scratch rows (env_scratch_bytes(L, exact); kEnvScratchBlocks
 // blocks).  envelope(): float2 (upper rounded up, lower rounded down) for the LB
 // kernels; envelope_exact(): build_envelope's double upper / lower.
+enum EnvFmt { kEnvPlain = 0, kEnvExact = 2 };
 constexpr int kEnvThreads = 128;
 constexpr int kEnvScratchBlocks = 592;  // 4 x 148 SMs
 constexpr size_t kEnvSmemMax = 192 * 1024;
