@@ -129,9 +129,19 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workloads
 
+def base_name(name):
+    """'c2_fp32' -> 'c2': the FP32-mode lines run the same workload in float32."""
+    return name[:-5] if name.endswith("_fp32") else name
+
+
+def precision_of(name):
+    return "float32" if name.endswith("_fp32") else "float64"
+
+
 def spec_for(name):
     from paper_2102_05221_b200 import DistanceSpec
 
+    name = base_name(name)
     return {
         "c1": DistanceSpec(kind="dtw"),
         "c2": DistanceSpec(kind="cdtw", window=51),
@@ -160,7 +170,7 @@ _PINNED = []
 def nn_data(name, rank=0):
     from paper_2102_05221_b200 import datagen
 
-    wl = {"c1": datagen.C1, "c2": datagen.C2, "c4m": datagen.C4, "c4t": datagen.C4}[name]
+    wl = {"c1": datagen.C1, "c2": datagen.C2, "c4m": datagen.C4, "c4t": datagen.C4}[base_name(name)]
     C, cl, protos = datagen.warped_prototypes(wl.n_candidates, wl.length, wl.classes, wl.sigma, wl.seed)
     Q, ql, _ = datagen.warped_prototypes(wl.n_queries, wl.length, wl.classes, wl.sigma,
                                          shard_seed(wl.seed, rank), protos=protos)
@@ -173,6 +183,9 @@ WORKLOAD_NAMES = {
     "c4m": "c4_msm_c1_1nn_512x8192_L512", "c4t": "c4_twe_nu0.001_lam1_1nn_512x8192_L512",
     "c5": "c5_cdtw_w51_subseq_q1024_stream2^20",
 }
+# the optional FP32 mode (north star: within 1e-5 relative, NN-index mismatch rate reported)
+FP32_NAMES = {n + "_fp32": WORKLOAD_NAMES[n] + "_fp32" for n in ("c2", "c3w", "c3e", "c4m", "c4t")}
+NN_NAMES = ("c1", "c2", "c4m", "c4t")
 
 
 # ---------------------------------------------------------------- our arm
@@ -186,13 +199,14 @@ class Runner:
         from paper_2102_05221_b200 import _lib
 
         self.name, self.rank, self.device = name, rank, device
+        self.base, self.precision = base_name(name), precision_of(name)
         self.torch = torch
         self.L = _lib.lib()
         self.lib = _lib
         self.spec = spec_for(name)
         self.kind = self.spec.kind
         t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)
-        if name in ("c1", "c2", "c4m", "c4t"):
+        if self.base in NN_NAMES:
             wl, Q, ql, C, cl = nn_data(name, rank)
             self.host = (Q, C)
             self.nq, self.nc, self.Lq = Q.shape[0], C.shape[0], Q.shape[1]
@@ -202,12 +216,12 @@ class Runner:
             self.dql = t(np.full(self.nq, self.Lq), torch.int32)
             self.dcl = t(np.full(self.nc, self.Lq), torch.int32)
             self.out = torch.empty(5 * self.nq, dtype=torch.int64, device=device)
-            self.h = _lib.SpecHandle(self.spec, longest_lengths=[self.Lq])
+            self.h = _lib.SpecHandle(self.spec, longest_lengths=[self.Lq], precision=self.precision)
             self.units = self.nq
             self.pairs = self.nq * self.nc
             self.cell_full = self.Lq * self.Lq
             self.unit = "queries/s"
-        elif name in ("c3w", "c3e"):
+        elif self.base in ("c3w", "c3e"):
             from paper_2102_05221_b200 import datagen
 
             X, _ = datagen.pairwise_workload(seed=3003 + rank)
@@ -217,7 +231,7 @@ class Runner:
             self.doff = t(np.arange(self.n) * self.Lq, torch.int64)
             self.dlen = t(np.full(self.n, self.Lq), torch.int32)
             self.dD = torch.empty(self.n * self.n, dtype=torch.float64, device=device)
-            self.h = _lib.SpecHandle(self.spec, longest_lengths=[self.Lq])
+            self.h = _lib.SpecHandle(self.spec, longest_lengths=[self.Lq], precision=self.precision)
             self.units = 1
             self.pairs = self.n * (self.n - 1) // 2
             self.cell_full = self.Lq * self.Lq
@@ -241,13 +255,13 @@ class Runner:
         import ctypes as C
 
         lib = self.lib
-        if self.name in ("c1", "c2", "c4m", "c4t"):
+        if self.base in NN_NAMES:
             o = self.out.data_ptr()
             lib.check(self.L.ek_nn_dev(self.h.ref, 2, self.dQ.data_ptr(), self.dqo.data_ptr(), self.dql.data_ptr(),
                                        self.nq, self.dC.data_ptr(), self.dco.data_ptr(), self.dcl.data_ptr(), self.nc,
                                        self.Lq, 1, o, o + 8 * self.nq, o + 16 * self.nq, o + 24 * self.nq,
                                        o + 32 * self.nq, stream_handle))
-        elif self.name in ("c3w", "c3e"):
+        elif self.base in ("c3w", "c3e"):
             cells = np.zeros(1, dtype=np.int64)
             lib.check(self.L.ek_pairwise_dev(self.h.ref, 3, self.dX.data_ptr(), self.doff.data_ptr(),
                                              self.dlen.data_ptr(), self.n, self.Lq, self.dD.data_ptr(),
@@ -266,7 +280,7 @@ class Runner:
             _ = C
 
     def cells_after_step(self):
-        if self.name in ("c1", "c2", "c4m", "c4t"):
+        if self.base in NN_NAMES:
             return int(self.out[2 * self.nq: 3 * self.nq].sum().item())
         return self.last.get("cells", 0)
 
@@ -277,13 +291,13 @@ class Runner:
 
         if self.pinned is None:  # the step's inputs live in pinned host memory (copied in once, untimed)
             self.pinned = tuple(pinned_copy(a) for a in self.host)
-        if self.name in ("c1", "c2", "c4m", "c4t"):
+        if self.base in NN_NAMES:
             Q, C = self.pinned
-            ekb.nn_batch(self.spec, "eapruned", Q, C)
+            ekb.nn_batch(self.spec, "eapruned", Q, C, precision=self.precision)
             return Q.nbytes + C.nbytes + 12 * (Q.shape[0] + C.shape[0]), 40 * Q.shape[0]
-        if self.name in ("c3w", "c3e"):
+        if self.base in ("c3w", "c3e"):
             (X,) = self.pinned
-            ekb.pairwise(self.spec, X, variant="pruned_only")
+            ekb.pairwise(self.spec, X, variant="pruned_only", precision=self.precision)
             return X.nbytes + 16 * X.shape[0], 8 * X.shape[0] ** 2 + 8
         q, stream = self.pinned
         ekb.subsequence_search(q, stream, SearchConfig(spec=self.spec, variant="eapruned", normalize=True))
@@ -408,9 +422,12 @@ def run_ours(args):
     L = _lib.lib()
     _lib.check(L.ek_init(local))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    names = [args.config] + ([n for n in WORKLOAD_NAMES if n != args.config] if args.all else [])
+    names = [args.config] + ([n for n in list(WORKLOAD_NAMES) + list(FP32_NAMES) if n != args.config]
+                             if args.all else [])
     results = {}
+    nn_index = {}  # FP64 1-NN answers per config (bit-identical to the reference's) for the FP32 mismatch rate
     peak_ops = L.ek_fp64_peak_ops()
+    peak32_ops = L.ek_fp32_peak_ops() if any(n.endswith("_fp32") for n in names) else 0.0
     work_stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(work_stream)  # events and library launches share this stream
     for name in names:
@@ -427,18 +444,21 @@ def run_ours(args):
         mean_cells = float(np.mean(cells))
         ops = mean_cells * OPS_PER_CELL[r.kind]
         achieved = ops / (kern_ms / 1e3) / 1e12
-        peak = peak_ops / 1e12
+        fp32 = r.precision == "float32"
+        peak = (peak32_ops if fp32 else peak_ops) / 1e12
         res = {
             "value": value, "unit": r.unit, "ms_per_step": ms_max, "step_ms": step_ms,
             "effective_gcups": world * r.pairs * r.cell_full / (ms_max / 1e3) / 1e9,
             "computed_gcups": world * mean_cells / (ms_max / 1e3) / 1e9,
             "computed_cells_per_step": mean_cells,
             "phases_ms": {k: float(np.mean([p.get(k, 0.0) for p in phases])) for k in phases[0]},
-            "roofline": {"bound": "fp64_alu", "kernel": "+".join(kern), "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak if peak > 0 else None, "traffic": None,
-                         "ops_per_cell": OPS_PER_CELL[r.kind],
-                         "peak_source": "measured FP64 DADD/DMUL microbenchmark (ek_fp64_peak_ops), "
-                                        "MEASURED_PEAKS.json has no FP64 entry"},
+            "roofline": {"bound": "fp32_alu" if fp32 else "fp64_alu", "kernel": "+".join(kern), "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak > 0 else None,
+                         "traffic": None, "ops_per_cell": OPS_PER_CELL[r.kind],
+                         "peak_source": ("measured FP32 FADD/FMUL microbenchmark (ek_fp32_peak_ops)" if fp32 else
+                                         "measured FP64 DADD/DMUL microbenchmark (ek_fp64_peak_ops)") +
+                                        ", MEASURED_PEAKS.json has no non-tensor entry"},
+            "dtype": "f32" if fp32 else "f64",
             "gpu_launches": launches // max(1, steps), "clocks": clk.summary(), "wall_s": wall,
         }
         # end to end through the public API with host buffers
@@ -451,6 +471,12 @@ def run_ours(args):
                     t_e2e.append(time.perf_counter() - t0)
             res["e2e"] = {"value": r.units / float(np.mean(t_e2e)), "unit": r.unit, "h2d_bytes_per_step": int(hb),
                           "d2h_bytes_per_step": int(db), "path": "public Python API (pinned numpy in, numpy out)"}
+        if r.base in NN_NAMES:
+            idx = r.out[: r.nq].cpu().numpy().copy()
+            if not fp32:
+                nn_index[r.base] = idx
+            elif r.base in nn_index:  # FP32 vs the FP64 (= reference) answers on the same queries
+                res["nn_index_mismatch_rate"] = float(np.mean(idx != nn_index[r.base]))
         results[name] = res
         del r
         torch.cuda.empty_cache()

@@ -49,6 +49,9 @@ typedef struct ek_spec {
   const double* wdtw_tables;     /* host memory, also for _dev calls */
   const int64_t* wdtw_table_off; /* indexed by longest length m */
   int64_t wdtw_max_len;
+  int32_t precision;     /* 0 float64 (bit-identical to the reference), 1 float32 (optional
+                            faster mode, within 1e-5 relative; ek_distance_batch / ek_nn /
+                            ek_pairwise only, cells are the engine's band cells) */
 } ek_spec;
 
 /* status / diagnostics */
@@ -124,6 +127,8 @@ int32_t ek_phase_times(double* ms, const char** names, int32_t max);
 
 /* Measured FP64 (non-tensor) DADD/DMUL throughput of the device, ops/s. */
 double ek_fp64_peak_ops(void);
+/* Measured FP32 (non-tensor) FADD/FMUL throughput (roofline of the FP32 mode), ops/s. */
+double ek_fp32_peak_ops(void);
 
 #ifdef __cplusplus
 }

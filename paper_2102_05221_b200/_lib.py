@@ -31,7 +31,20 @@ class EkSpec(C.Structure):
         ("kind", C.c_int32), ("cost_mode", C.c_int32), ("window", C.c_int64),
         ("erp_gap", C.c_double), ("msm_c", C.c_double), ("twe_nu", C.c_double), ("twe_lambda", C.c_double),
         ("wdtw_tables", _dp), ("wdtw_table_off", _i64p), ("wdtw_max_len", C.c_int64),
+        ("precision", C.c_int32),
     ]
+
+
+PRECISIONS = ("float64", "float32")
+
+
+def precision_code(precision: str) -> int:
+    """``float64`` (default): the reference's arithmetic, bit-identical results.
+    ``float32``: the optional faster mode (values within 1e-5 relative; not part of
+    the reference's API)."""
+    if precision not in PRECISIONS:
+        raise SpecError(f"unknown precision {precision!r}; expected one of {PRECISIONS}")
+    return PRECISIONS.index(precision)
 
 
 EXPORTS = {
@@ -43,6 +56,7 @@ EXPORTS = {
     "ek_set_profiling": ([C.c_int32], None),
     "ek_phase_times": ([_dp, C.POINTER(C.c_char_p), C.c_int32], C.c_int32),
     "ek_fp64_peak_ops": ([], C.c_double),
+    "ek_fp32_peak_ops": ([], C.c_double),
     "ek_distance_batch": ([C.POINTER(EkSpec), C.c_int32, C.c_int64, _dp, C.c_int64, _i64p, _i64p, _i64p, _i64p,
                            _dp, _i64p, _dp, _i64p], C.c_int),
     "ek_nn": ([C.POINTER(EkSpec), C.c_int32, _dp, C.c_int64, _i64p, _i64p, C.c_int64, _dp, C.c_int64, _i64p, _i64p,
@@ -105,7 +119,7 @@ def iptr(a: np.ndarray):
 class SpecHandle:
     """ek_spec plus the host arrays its pointers reference (WDTW tables)."""
 
-    def __init__(self, spec: DistanceSpec, longest_lengths=(), window_override=None):
+    def __init__(self, spec: DistanceSpec, longest_lengths=(), window_override=None, precision="float64"):
         if spec.kind not in KINDS:
             raise SpecError(f"unknown distance kind {spec.kind!r}")
         self._keep = []
@@ -130,6 +144,7 @@ class SpecHandle:
             float(spec.erp_gap or 0.0), float(spec.msm_c or 0.0),
             float(spec.twe_nu or 0.0), float(spec.twe_lambda or 0.0),
             dptr(tabs) if tabs is not None else None, iptr(offs) if offs is not None else None, mx,
+            precision_code(precision),
         )
 
     @property

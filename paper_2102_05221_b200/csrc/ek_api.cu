@@ -324,6 +324,7 @@ int check_spec(const ek_spec* sp) {
   if (!sp) return fail("spec is NULL");
   if (sp->kind < 0 || sp->kind > 5) return fail("unknown distance kind code %d", sp->kind);
   if (sp->cost_mode != 0 && sp->cost_mode != 1) return fail("unknown cost mode code %d", sp->cost_mode);
+  if (sp->precision != 0 && sp->precision != 1) return fail("unknown precision code %d", sp->precision);
   if (sp->kind == K_WDTW && (!sp->wdtw_tables || !sp->wdtw_table_off))
     return fail("wdtw requires weight tables");
   return 0;
@@ -357,12 +358,19 @@ struct ParamHolder {
   }
 };
 
-size_t pair_smem(int lmax, int eng, int wpb) { return sizeof(double) * (size_t)wpb * warp_stride(lmax, eng); }
+// template MODE of the engines: cost mode | M_F32 for the float32 precision
+int spec_mode(const ek_spec* sp) { return sp->cost_mode | (sp->precision ? (int)M_F32 : 0); }
+// bytes per staged element (the FP32 mode stages floats)
+size_t elem_size(const ek_spec* sp) { return sp->precision ? sizeof(float) : sizeof(double); }
+
+size_t pair_smem(int lmax, int eng, int wpb, size_t esz = sizeof(double)) {
+  return esz * (size_t)wpb * warp_stride(lmax, eng);
+}
 
 // warps per block: up to `want`, as many as the per-warp shared memory allows
-int pick_wpb(int lmax, int eng, int want, int extra_per_warp = 0) {
+int pick_wpb(int lmax, int eng, int want, int extra_per_warp = 0, size_t esz = sizeof(double)) {
   int wpb = want;
-  while (wpb > 1 && (size_t)wpb * (sizeof(double) * (size_t)(warp_stride(lmax, eng) + extra_per_warp)) > 220 * 1024)
+  while (wpb > 1 && (size_t)wpb * (esz * (size_t)(warp_stride(lmax, eng) + extra_per_warp)) > 220 * 1024)
     --wpb;
   return wpb;
 }
@@ -467,7 +475,7 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
     pd.cut = cut;
     // ea with a finite cutoff, eapruned and pruned_only report the reference's own cell
     // count (ek_refcells.cuh) when the row-stripe replay engine holds the pair
-    if ((ea_rows || variant == 2 || variant == 3) && pd.nc <= kRefMaxCols && pd.nl <= 2048) {
+    if ((ea_rows || variant == 2 || variant == 3) && pd.nc <= kRefMaxCols && pd.nl <= 2048 && !spec->precision) {
       const int reng = ea_rows ? E_STR16_EA : (w < pd.nl - 1 ? E_STRB16 : E_STR16);
       pd.pad_ = ea_rows ? 1 : variant;
       rgroups[reng].push_back(pd);
@@ -493,9 +501,9 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
     if (dp.alloc(sizeof(PairDesc) * n, st) || dc.alloc(sizeof(double) * n, st) || dt.alloc(sizeof(int) * n, st))
       return -1;
     CK(cudaMemcpyAsync(dp.p, groups[eng].data(), sizeof(PairDesc) * n, cudaMemcpyHostToDevice, st));
-    const int wpb = pick_wpb(glmax[eng], eng, 4);
-    const size_t smem = pair_smem(glmax[eng], eng, wpb);
-    const PairsFn pf = pick_pairs(spec->kind, spec->cost_mode, eng);
+    const int wpb = pick_wpb(glmax[eng], eng, 4, 0, elem_size(spec));
+    const size_t smem = pair_smem(glmax[eng], eng, wpb, elem_size(spec));
+    const PairsFn pf = pick_pairs(spec->kind, spec_mode(spec), eng);
     Params prm = ph.prm;
     DBuf dstrip;
     if (strip_scratch(pf, eng, 32 * wpb, smem, glmax[eng], prm, dstrip, st)) return -1;
@@ -632,7 +640,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   mark(st, "rank");
   // 2. cutoff seed: exact diagonal upper bound of each query's top-ranked candidate
   if (share) {
-    if (launch_plain(pick_ub(spec->kind, spec->cost_mode), dim3((unsigned)((nq + 3) / 4)), dim3(128), 0, st, dQ,
+    if (launch_plain(pick_ub(spec->kind, spec_mode(spec)), dim3((unsigned)((nq + 3) / 4)), dim3(128), 0, st, dQ,
                      (const long long*)dqoff, (const int*)dqlen, (int)nq, dC, (const long long*)dcoff,
                      (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), win, ph.prm,
                      dcut.as<unsigned long long>()))
@@ -644,9 +652,9 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   }
   mark(st, "seed_cutoff");
   // 3. phase A: the top-ranked few per query; phase B: everything else
-  const NNFn fn = pick_nn(spec->kind, spec->cost_mode, eng);
-  const int wpb = pick_wpb(max_len, eng, 4);
-  const size_t smem = pair_smem(max_len, eng, wpb);
+  const NNFn fn = pick_nn(spec->kind, spec_mode(spec), eng);
+  const int wpb = pick_wpb(max_len, eng, 4, 0, elem_size(spec));
+  const size_t smem = pair_smem(max_len, eng, wpb, elem_size(spec));
   DBuf dstrip;
   if (strip_scratch(fn, eng, 32 * wpb, smem, max_len, ph.prm, dstrip, st)) return -1;
   // On the LB path phase A joins phase B's single launch: the top ranks are its first
@@ -667,8 +675,8 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // concentrate) one pair per item for load balance, the rest in items of 8
   // (64 / 8 measured best on C2 against 32..128 / 4..32)
   const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? 4 : ka) + 64);
-  const NNFn fnB = pick_nn(spec->kind, spec->cost_mode, engB);
-  const size_t smemB = pair_smem(max_len, engB, wpb);
+  const NNFn fnB = pick_nn(spec->kind, spec_mode(spec), engB);
+  const size_t smemB = pair_smem(max_len, engB, wpb, elem_size(spec));
   // With the LB pre-test most pairs are cheap and the first segment's tail of long DPs
   // would idle the GPU, so both segments share one launch.  Without it (MSM, TWE, ...)
   // every pair runs the DP and the second segment waits for the first one's cutoffs.
@@ -689,7 +697,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   }
   mark(st, "nn_phaseB");
   if (engB != eng) {  // redo guarded-band overflows with the full-band engine
-    const NNFixFn ff = pick_nn_fix(spec->kind, spec->cost_mode, eng);
+    const NNFixFn ff = pick_nn_fix(spec->kind, spec_mode(spec), eng);
     Params fprm = ph.prm;
     DBuf dstrip2;
     if (strip_scratch(ff, eng, 32 * wpb, smem, max_len, fprm, dstrip2, st)) return -1;
@@ -794,11 +802,12 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
   if (dcnt.alloc(8, st) || dtot.alloc(8, st)) return -1;
   CK(cudaMemsetAsync(dcnt.p, 0, 8, st));
   CK(cudaMemsetAsync(dtot.p, 0, 8, st));
-  const int wpb = pick_wpb(max_len, eng, 4);
-  const TriFn tf = pick_tri(spec->kind, spec->cost_mode, eng);
+  const int wpb = pick_wpb(max_len, eng, 4, 0, elem_size(spec));
+  const TriFn tf = pick_tri(spec->kind, spec_mode(spec), eng);
   DBuf dstrip;
-  if (strip_scratch(tf, eng, 32 * wpb, pair_smem(max_len, eng, wpb), max_len, ph.prm, dstrip, st)) return -1;
-  if (launch_persistent(tf, 32 * wpb, pair_smem(max_len, eng, wpb), st, np,
+  const size_t tsmem = pair_smem(max_len, eng, wpb, elem_size(spec));
+  if (strip_scratch(tf, eng, 32 * wpb, tsmem, max_len, ph.prm, dstrip, st)) return -1;
+  if (launch_persistent(tf, 32 * wpb, tsmem, st, np,
                         d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, ph.prm, d_D,
                         dtot.as<unsigned long long>(), dcnt.as<int>()))
     return -1;
@@ -857,6 +866,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                            int64_t* computed, int64_t* abandoned, cudaStream_t st, double* profile = nullptr) {
   if (check_spec(spec)) return -1;
   if (spec->kind != K_DTW && spec->kind != K_CDTW) return fail("subsequence search supports dtw and cdtw only");
+  if (spec->precision) return fail("subsequence search runs in float64 only");
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
   if (lq < 1 || lq > nref) return fail("query length %lld exceeds reference length %lld", (long long)lq, (long long)nref);
   const long long nwin = nref - lq + 1;
@@ -1161,43 +1171,47 @@ int32_t ek_phase_times(double* ms, const char** names, int32_t max) {
 
 }  // extern "C"
 
-// ---- FP64 roofline denominator (bench.py) ---------------------------------------
+// ---- FP64 / FP32 roofline denominators (bench.py) -------------------------------
 
 namespace {
 
-__global__ void k_fp64_peak(double* out, int iters, double a, double b) {
-  // 8 independent DADD/DMUL chains per thread: the FP64 pipe's throughput
-  double r0 = threadIdx.x * 1e-9, r1 = r0 + 1, r2 = r0 + 2, r3 = r0 + 3, r4 = r0 + 4, r5 = r0 + 5, r6 = r0 + 6,
-         r7 = r0 + 7;
+__device__ __forceinline__ double padd(double x, double y) { return __dadd_rn(x, y); }
+__device__ __forceinline__ double pmul(double x, double y) { return __dmul_rn(x, y); }
+__device__ __forceinline__ float padd(float x, float y) { return __fadd_rn(x, y); }
+__device__ __forceinline__ float pmul(float x, float y) { return __fmul_rn(x, y); }
+
+template <class T>
+__global__ void k_alu_peak(T* out, int iters, T a, T b) {
+  // 8 independent add/mul chains per thread: the FP64 (or FP32) pipe's throughput
+  T r0 = (T)(threadIdx.x * 1e-9), r1 = r0 + 1, r2 = r0 + 2, r3 = r0 + 3, r4 = r0 + 4, r5 = r0 + 5, r6 = r0 + 6,
+    r7 = r0 + 7;
   for (int i = 0; i < iters; ++i) {
-    r0 = __dadd_rn(r0, a); r1 = __dmul_rn(r1, b); r2 = __dadd_rn(r2, a); r3 = __dmul_rn(r3, b);
-    r4 = __dadd_rn(r4, a); r5 = __dmul_rn(r5, b); r6 = __dadd_rn(r6, a); r7 = __dmul_rn(r7, b);
+    r0 = padd(r0, a); r1 = pmul(r1, b); r2 = padd(r2, a); r3 = pmul(r3, b);
+    r4 = padd(r4, a); r5 = pmul(r5, b); r6 = padd(r6, a); r7 = pmul(r7, b);
   }
-  const double s = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
-  if (s == 12345.678) out[0] = s;  // keep the chains live
+  const T s = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  if (s == (T)12345.678) out[0] = s;  // keep the chains live
 }
 
-}  // namespace
-
-extern "C" {
-
-// Measured FP64 (non-tensor) add/mul throughput of this device in ops/s (best of 5).
-double ek_fp64_peak_ops(void) {
+// Measured add/mul throughput of this device in ops/s (best of 5).
+template <class T>
+double alu_peak_ops() {
   std::lock_guard<std::mutex> lk(g_mu);
   if (ensure_ctx()) return -1.0;
   cudaStream_t st = g_ctx.stream;
-  double* d = nullptr;
-  if (cudaMalloc(&d, 8) != cudaSuccess) return -1.0;
+  T* d = nullptr;
+  if (cudaMalloc(&d, sizeof(T)) != cudaSuccess) return -1.0;
   const int block = 256, iters = 1 << 14;
   const int grid = g_ctx.nsm * 8;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  k_fp64_peak<<<grid, block, 0, st>>>(d, 256, 1.0000001, 0.9999999);
+  const T a = (T)1.0000001, b = (T)0.9999999;
+  k_alu_peak<T><<<grid, block, 0, st>>>(d, 256, a, b);
   float best = 1e30f;
   for (int rep = 0; rep < 5; ++rep) {
     cudaEventRecord(e0, st);
-    k_fp64_peak<<<grid, block, 0, st>>>(d, iters, 1.0000001, 0.9999999);
+    k_alu_peak<T><<<grid, block, 0, st>>>(d, iters, a, b);
     cudaEventRecord(e1, st);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -1209,5 +1223,12 @@ double ek_fp64_peak_ops(void) {
   cudaFree(d);
   return (double)grid * block * iters * 8.0 / (best * 1e-3);
 }
+
+}  // namespace
+
+extern "C" {
+
+double ek_fp64_peak_ops(void) { return alu_peak_ops<double>(); }
+double ek_fp32_peak_ops(void) { return alu_peak_ops<float>(); }
 
 }  // extern "C"

@@ -22,7 +22,11 @@
 namespace ekb {
 
 enum Kind : int { K_DTW = 0, K_CDTW = 1, K_WDTW = 2, K_ERP = 3, K_MSM = 4, K_TWE = 5 };
-enum Mode : int { M_SQ = 0, M_ABS = 1 };
+enum Mode : int { M_SQ = 0, M_ABS = 1, M_F32 = 2 };
+// MODE = cost mode (bit 0) | M_F32 (bit 1).  The FP32 mode (not the reference's
+// arithmetic: an optional faster mode, within 1e-5 relative of it) runs the same
+// engines on float values staged from the float64 inputs.
+template <int MODE> using real_t = typename std::conditional<(MODE & M_F32) != 0, float, double>::type;
 
 #define EKB_INF (__longlong_as_double(0x7ff0000000000000LL))
 #define EKB_DI __device__ __forceinline__
@@ -55,38 +59,47 @@ __device__ __forceinline__ Params pair_params(const Params& p, int m) {
 EKB_DI double dadd(double a, double b) { return __dadd_rn(a, b); }
 EKB_DI double dsub(double a, double b) { return __dsub_rn(a, b); }
 EKB_DI double dmul(double a, double b) { return __dmul_rn(a, b); }
-EKB_DI double dmin_ref(double v, double a) { return (a < v) ? a : v; }  // "if a < v: v = a"
+EKB_DI float dadd(float a, float b) { return __fadd_rn(a, b); }
+EKB_DI float dsub(float a, float b) { return __fsub_rn(a, b); }
+EKB_DI float dmul(float a, float b) { return __fmul_rn(a, b); }
+template <class R>
+EKB_DI R dmin_ref(R v, R a) { return (a < v) ? a : v; }  // "if a < v: v = a"
+template <class R> EKB_DI R rinf();
+template <> EKB_DI double rinf<double>() { return EKB_INF; }
+template <> EKB_DI float rinf<float>() { return __int_as_float(0x7f800000); }
 
 // point_cost (kernels.py:70-77; _speedups.pyx:33-38)
 template <int MODE>
-EKB_DI double pcost(double a, double b) {
-  double d = dsub(a, b);
-  if (MODE == M_SQ) return dmul(d, d);
+EKB_DI real_t<MODE> pcost(real_t<MODE> a, real_t<MODE> b) {
+  real_t<MODE> d = dsub(a, b);
+  if ((MODE & 1) == M_SQ) return dmul(d, d);
   return fabs(d);
 }
 
-// IEEE sign bit (0 / 1) of a double
+// IEEE sign bit (0 / 1)
 EKB_DI int sign_bit(double v) { return (int)((unsigned)__double2hiint(v) >> 31); }
+EKB_DI int sign_bit(float v) { return (int)(__float_as_uint(v) >> 31); }
 
 // ---- row / column data ----
-template <int KIND> struct RowD { double x; };
-template <int KIND> struct ColD { double y; };
-template <> struct RowD<K_ERP> { double x, ar; };
-template <> struct ColD<K_ERP> { double y, ac; };
-template <> struct RowD<K_TWE> { double x, ar; };
-template <> struct ColD<K_TWE> { double y, ac; };
-template <> struct RowD<K_MSM> { double x, dr; int s; };  // s: sign bit of x - xprev
-template <> struct ColD<K_MSM> { double y, dc; int s; };  // s: sign bit of y - yprev
+template <int KIND, class R = double> struct RowD { R x; };
+template <int KIND, class R = double> struct ColD { R y; };
+template <class R> struct RowD<K_ERP, R> { R x, ar; };
+template <class R> struct ColD<K_ERP, R> { R y, ac; };
+template <class R> struct RowD<K_TWE, R> { R x, ar; };
+template <class R> struct ColD<K_TWE, R> { R y, ac; };
+template <class R> struct RowD<K_MSM, R> { R x, dr; int s; };  // s: sign bit of x - xprev
+template <class R> struct ColD<K_MSM, R> { R y, dc; int s; };  // s: sign bit of y - yprev
 
 // x = l[i-1], xp = l[i-2] (pad: MSM uses l[0] at index -1, TWE a phantom 0.0)
 template <int KIND, int MODE>
-EKB_DI RowD<KIND> make_row(double x, double xp, const Params& p) {
-  RowD<KIND> r;
+EKB_DI RowD<KIND, real_t<MODE>> make_row(real_t<MODE> x, real_t<MODE> xp, const Params& p) {
+  using R = real_t<MODE>;
+  RowD<KIND, R> r;
   r.x = x;
-  if constexpr (KIND == K_ERP) r.ar = pcost<MODE>(x, p.gap);                 // alt_row: pc(l_i, g)
-  if constexpr (KIND == K_TWE) r.ar = dadd(dadd(pcost<MODE>(x, xp), p.nu), p.lam);  // (pc(l_i,l_{i-1})+nu)+lam
+  if constexpr (KIND == K_ERP) r.ar = pcost<MODE>(x, (R)p.gap);                 // alt_row: pc(l_i, g)
+  if constexpr (KIND == K_TWE) r.ar = dadd(dadd(pcost<MODE>(x, xp), (R)p.nu), (R)p.lam);  // (pc(l_i,l_{i-1})+nu)+lam
   if constexpr (KIND == K_MSM) {
-    const double d = dsub(x, xp);
+    const R d = dsub(x, xp);
     r.dr = fabs(d);  // fabs(np - x) in msm_cost(l_i, l_{i-1}, c_j)
     r.s = sign_bit(d);
   }
@@ -94,13 +107,14 @@ EKB_DI RowD<KIND> make_row(double x, double xp, const Params& p) {
 }
 
 template <int KIND, int MODE>
-EKB_DI ColD<KIND> make_col(double y, double yp, const Params& p) {
-  ColD<KIND> c;
+EKB_DI ColD<KIND, real_t<MODE>> make_col(real_t<MODE> y, real_t<MODE> yp, const Params& p) {
+  using R = real_t<MODE>;
+  ColD<KIND, R> c;
   c.y = y;
-  if constexpr (KIND == K_ERP) c.ac = pcost<MODE>(p.gap, y);                 // alt_col: pc(g, c_j)
-  if constexpr (KIND == K_TWE) c.ac = dadd(dadd(pcost<MODE>(y, yp), p.nu), p.lam);
+  if constexpr (KIND == K_ERP) c.ac = pcost<MODE>((R)p.gap, y);                 // alt_col: pc(g, c_j)
+  if constexpr (KIND == K_TWE) c.ac = dadd(dadd(pcost<MODE>(y, yp), (R)p.nu), (R)p.lam);
   if constexpr (KIND == K_MSM) {
-    const double d = dsub(y, yp);
+    const R d = dsub(y, yp);
     c.dc = fabs(d);  // fabs(np - y) in msm_cost(c_j, l_i, c_{j-1})
     c.s = sign_bit(d);
   }
@@ -110,22 +124,24 @@ EKB_DI ColD<KIND> make_col(double y, double yp, const Params& p) {
 // ---- per-diagonal constant and per-slot state ----
 // off: +inf for a diagonal outside the band (its cells must stay +inf), 0.0 inside;
 // the DTW family adds it to the move cost, which replaces two selects per cell.
-template <int KIND> struct DiagK { double off; };
-template <> struct DiagK<K_WDTW> { double w, off; };
-template <> struct DiagK<K_TWE> { double tw; };
-template <int KIND> struct SlotS {};
-template <> struct SlotS<K_TWE> { double pcp; };  // pc(l_{i-2}, c_{j-2}) = previous cell's pc on this diagonal
+template <int KIND, class R = double> struct DiagK { R off; };
+template <class R> struct DiagK<K_WDTW, R> { R w, off; };
+template <class R> struct DiagK<K_TWE, R> { R tw; };
+template <int KIND, class R = double> struct SlotS {};
+template <class R> struct SlotS<K_TWE, R> { R pcp; };  // pc(l_{i-2}, c_{j-2}) = previous cell's pc on this diagonal
 
-template <int KIND>
-EKB_DI DiagK<KIND> make_diag(int d, const Params& p, bool in_band = true) {
-  DiagK<KIND> k;
+// FP32 mode: the WDTW weight is the host table's value rounded to float; TWE's
+// nu*(d+d) is evaluated in float.
+template <int KIND, class R = double>
+EKB_DI DiagK<KIND, R> make_diag(int d, const Params& p, bool in_band = true) {
+  DiagK<KIND, R> k;
   int ad = d < 0 ? -d : d;
   if constexpr (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW || KIND == K_ERP || KIND == K_MSM)
-    k.off = in_band ? p.zero : EKB_INF;
-  if constexpr (KIND == K_WDTW) k.w = (ad < p.wt_len) ? p.wt[ad] : 0.0;  // wt[|i-j|]
+    k.off = in_band ? (R)p.zero : rinf<R>();
+  if constexpr (KIND == K_WDTW) k.w = (ad < p.wt_len) ? (R)p.wt[ad] : (R)0.0;  // wt[|i-j|]
   if constexpr (KIND == K_TWE) {
-    double dij = (double)ad;
-    k.tw = dmul(p.nu, dadd(dij, dij));  // nu * (dij + dij)
+    R dij = (R)ad;
+    k.tw = dmul((R)p.nu, dadd(dij, dij));  // nu * (dij + dij)
   }
   return k;
 }
@@ -139,45 +155,46 @@ EKB_DI DiagK<KIND> make_diag(int d, const Params& p, bool in_band = true) {
 // dc = c_j - c_{j-1} do.  Reading "strict sign" as the IEEE sign bit only misclassifies
 // a zero (e or dr / dc == +0: an exact difference is never -0), and then both outcomes
 // give the same value: c, or c + min(|d|, 0) = c + 0 = c.
-EKB_DI double msm_alt(bool between, double c, double dother, double de) {
-  double m = (dother < de) ? dother : de;  // "d1 if d1 < d2 else d2" (value-identical)
+template <class R>
+EKB_DI R msm_alt(bool between, R c, R dother, R de) {
+  R m = (dother < de) ? dother : de;  // "d1 if d1 < d2 else d2" (value-identical)
   return between ? c : dadd(c, m);
 }
 
 // One cell.  D, T, L are the dependency values; the result is the reference's
 // value bit-for-bit whenever the dependencies are.  (For the DTW family the
 // band offset k.off is folded into the cost: cost + 0.0 == cost exactly.)
-template <int KIND, int MODE, bool OFF = true>
-EKB_DI double cell(double D, double T, double L, const RowD<KIND>& r, const ColD<KIND>& c,
-                   const DiagK<KIND>& k, SlotS<KIND>& st, const Params& p) {
+template <int KIND, int MODE, bool OFF = true, class R = real_t<MODE>>
+EKB_DI R cell(R D, R T, R L, const RowD<KIND, R>& r, const ColD<KIND, R>& c, const DiagK<KIND, R>& k,
+              SlotS<KIND, R>& st, const Params& p) {
   if constexpr (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW) {
     // all three move costs are equal: min(D+c, T+c, L+c) == min(D,T,L)+c (monotone rounding)
-    double cost = pcost<MODE>(r.x, c.y);
+    R cost = pcost<MODE>(r.x, c.y);
     if constexpr (KIND == K_WDTW) cost = dmul(cost, k.w);
     if constexpr (OFF) cost = dadd(cost, k.off);  // +0.0 in band (exact), +inf outside
-    double m = dmin_ref(D, T);
+    R m = dmin_ref(D, T);
     m = dmin_ref(m, L);
     return dadd(m, cost);
   } else if constexpr (KIND == K_ERP) {
-    double v = dadd(D, pcost<MODE>(r.x, c.y));
+    R v = dadd(D, pcost<MODE>(r.x, c.y));
     v = dmin_ref(v, dadd(T, r.ar));
     return dmin_ref(v, dadd(L, c.ac));
   } else if constexpr (KIND == K_TWE) {
-    double pc = pcost<MODE>(r.x, c.y);
-    double canon = dadd(dadd(pc, st.pcp), k.tw);  // (pc(l_i,c_j) + pc(l_{i-1},c_{j-1})) + nu*(d+d)
+    R pc = pcost<MODE>(r.x, c.y);
+    R canon = dadd(dadd(pc, st.pcp), k.tw);  // (pc(l_i,c_j) + pc(l_{i-1},c_{j-1})) + nu*(d+d)
     st.pcp = pc;
-    double v = dadd(D, canon);
+    R v = dadd(D, canon);
     v = dmin_ref(v, dadd(T, r.ar));
     return dmin_ref(v, dadd(L, c.ac));
   } else {  // MSM: canonical |l_i - c_j| regardless of cost mode
-    double e = dsub(r.x, c.y);
-    double de = fabs(e);
+    R e = dsub(r.x, c.y);
+    R de = fabs(e);
     const int se = sign_bit(e);
     bool brow = se != r.s;  // l_{i-1}<=l_i<=c_j or l_{i-1}>=l_i>=c_j (see msm_alt)
     bool bcol = se == c.s;  // l_i<=c_j<=c_{j-1} or l_i>=c_j>=c_{j-1}
-    double ar = msm_alt(brow, p.msm_c, r.dr, de);
-    double ac = msm_alt(bcol, p.msm_c, c.dc, de);
-    double v = dadd(D, de);
+    R ar = msm_alt(brow, (R)p.msm_c, r.dr, de);
+    R ac = msm_alt(bcol, (R)p.msm_c, c.dc, de);
+    R v = dadd(D, de);
     v = dmin_ref(v, dadd(T, ar));
     return dmin_ref(v, dadd(L, ac));
   }
@@ -186,9 +203,9 @@ EKB_DI double cell(double D, double T, double L, const RowD<KIND>& r, const ColD
 // Pads around a series in shared memory: index -1 and index n.  Index -1 is the
 // "previous" of the first element (MSM: the point itself; TWE: phantom 0.0);
 // index n is +inf so cells past the end of the matrix evaluate to +inf.
-template <int KIND>
-EKB_DI double pad_before(double first) {
-  return KIND == K_MSM ? first : 0.0;
+template <int KIND, class R = double>
+EKB_DI R pad_before(R first) {
+  return KIND == K_MSM ? first : (R)0.0;
 }
 
 }  // namespace ekb

@@ -61,6 +61,14 @@ __device__ __forceinline__ double ld_cut(const unsigned long long* p) {
 }
 
 __device__ __forceinline__ int hi_word(double v) { return __double2hiint(v); }
+// FP32 mode: the whole image (values are >= +0 or +inf, so the bits order as integers)
+__device__ __forceinline__ int hi_word(float v) { return __float_as_int(v); }
+
+// A cutoff in the engine's precision.  FP32 keep-if-<= against a float64 cutoff c:
+// a float v satisfies v <= c iff v <= RD(c), so the cutoff is rounded down.
+template <class R> __device__ __forceinline__ R to_cut(double c);
+template <> __device__ __forceinline__ double to_cut<double>(double c) { return c; }
+template <> __device__ __forceinline__ float to_cut<float>(double c) { return __double2float_rd(c); }
 
 // Loader protocol: next_t(dlo, dhi, H) = first double-step time at which the
 // engine needs data beyond what is staged; ensure(t, dlo, dhi, H) stages more.
@@ -76,10 +84,11 @@ __host__ __device__ constexpr int diag_pad(int P) { return 16 * P + 8; }
 // Series accessor over shared memory padded on both sides (see stage_series):
 // index -1 holds the kind's "previous of the first element", indices < -1 hold
 // 0.0, indices >= n hold +inf.
-struct SmemSeries {
-  const double* p;
+template <class R>
+struct SmemSeriesT {
+  const R* p;
   int n;
-  __device__ __forceinline__ double at(int k) const {
+  __device__ __forceinline__ R at(int k) const {
 #ifdef EKB_BOUNDS
     if (k < -EKB_BOUNDS || k >= n + EKB_BOUNDS) {
       printf("SmemSeries OOB k=%d n=%d block=%d warp=%d\n", k, n, blockIdx.x, threadIdx.x >> 5);
@@ -89,6 +98,7 @@ struct SmemSeries {
     return p[k];
   }
 };
+using SmemSeries = SmemSeriesT<double>;
 
 // Runs f(integral_constant<S>) for S = S0 .. U-1 until one returns true.
 template <int S0, int U, class F>
@@ -113,10 +123,13 @@ __device__ __forceinline__ bool unrolled_steps(F& f) {
 // decreases, so a path <= the final cutoff is live at every check.  On that event the
 // pair stops with ovf set and the caller redoes it with a full-band engine.
 template <int KIND, int MODE, int P, bool SHARED_CUT, bool GUARD = false, class XAcc, class YAcc, class Loader>
-__device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
+__device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut64,
                                 const unsigned long long* cutp, const Params& prm, Loader& ld,
                                 unsigned guard = 0u) {
   static_assert(P % 2 == 0 && P >= 2, "P must be even");
+  using R = real_t<MODE>;
+  const R INF = rinf<R>();
+  R cut = to_cut<R>(cut64);
   constexpr int H = P / 2;
   constexpr bool BORDERED = (KIND == K_ERP);
   // the DTW family masks out-of-band diagonals through their cost (+inf offset)
@@ -131,34 +144,34 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     ld.ensure(2, dlo, dhi, H);
     t_load = ld.next_t(dlo, dhi, H);
   }
-  double val[P];
+  R val[P];
   bool upd[P];
   int tb[P];  // ERP: border time of a virtual diagonal, else -1
-  DiagK<KIND> kk[P];
-  SlotS<KIND> st[P];
+  DiagK<KIND, R> kk[P];
+  SlotS<KIND, R> st[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const int d = d0 + p;
     upd[p] = (d >= dlo) && (d <= dhi);
     tb[p] = (BORDERED && (d == dlo - 1 || d == dhi + 1)) ? (d < 0 ? -d : d) : -1;
-    kk[p] = make_diag<KIND>(d, prm, upd[p] || !COST_MASK);
-    val[p] = EKB_INF;
-    if constexpr (KIND == K_TWE) st[p].pcp = 0.0;
-    if (d == 0) val[p] = 0.0;  // corner, t = 0
+    kk[p] = make_diag<KIND, R>(d, prm, upd[p] || !COST_MASK);
+    val[p] = INF;
+    if constexpr (KIND == K_TWE) st[p].pcp = (R)0.0;
+    if (d == 0) val[p] = (R)0.0;  // corner, t = 0
     if (d == 1) {              // border cell (1,0) at t = 1
-      if constexpr (BORDERED) val[p] = dadd(0.0, pcost<MODE>(X.at(0), prm.gap));
-      if constexpr (KIND == K_TWE) st[p].pcp = pcost<MODE>(X.at(0), 0.0);
+      if constexpr (BORDERED) val[p] = dadd((R)0.0, pcost<MODE>(X.at(0), (R)prm.gap));
+      if constexpr (KIND == K_TWE) st[p].pcp = pcost<MODE>(X.at(0), (R)0.0);
     }
     if (d == -1) {             // border cell (0,1) at t = 1
-      if constexpr (BORDERED) val[p] = dadd(0.0, pcost<MODE>(prm.gap, Y.at(0)));
-      if constexpr (KIND == K_TWE) st[p].pcp = pcost<MODE>(0.0, Y.at(0));
+      if constexpr (BORDERED) val[p] = dadd((R)0.0, pcost<MODE>((R)prm.gap, Y.at(0)));
+      if constexpr (KIND == K_TWE) st[p].pcp = pcost<MODE>((R)0.0, Y.at(0));
     }
   }
 
   int t = 2;
   int I0 = (t + d0) >> 1, J0 = (t - d0) >> 1;
-  RowD<KIND> xw[H + 1];
-  ColD<KIND> yw[H];
+  RowD<KIND, R> xw[H + 1];
+  ColD<KIND, R> yw[H];
 #pragma unroll
   for (int k = 0; k <= H; ++k) xw[k] = make_row<KIND, MODE>(X.at(I0 + k - 1), X.at(I0 + k - 2), prm);
 #pragma unroll
@@ -183,43 +196,43 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     constexpr int S = decltype(S_)::value;
     constexpr int rx = ROT ? S % (H + 1) : 0;
     constexpr int ry = ROT ? (H - S % H) % H : 0;
-    auto XW = [&](int k) -> RowD<KIND>& { return xw[(k + rx) % (H + 1)]; };
-    auto YW = [&](int m) -> ColD<KIND>& { return yw[(m + ry) % H]; };
+    auto XW = [&](int k) -> RowD<KIND, R>& { return xw[(k + rx) % (H + 1)]; };
+    auto YW = [&](int m) -> ColD<KIND, R>& { return yw[(m + ry) % H]; };
     // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
-    double tin = __shfl_up_sync(FULL, val[P - 1], 1);
+    R tin = __shfl_up_sync(FULL, val[P - 1], 1);
     if constexpr (BORDERED) {
-      if (lane == 0) tin = EKB_INF;
+      if (lane == 0) tin = INF;
     }
 #pragma unroll
     for (int m = 0; m < H; ++m) {
       const int p = 2 * m;
-      const double T = (m == 0) ? tin : val[p - 1];
-      const double v = cell<KIND, MODE>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm);
+      const R T = (m == 0) ? tin : val[p - 1];
+      const R v = cell<KIND, MODE>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm);
       if constexpr (BORDERED) {
-        val[p] = (upd[p] || tb[p] == t) ? v : EKB_INF;
+        val[p] = (upd[p] || tb[p] == t) ? v : INF;
       } else if constexpr (COST_MASK) {
         val[p] = v;
       } else {
-        val[p] = upd[p] ? v : EKB_INF;
+        val[p] = upd[p] ? v : INF;
       }
       alive |= hi_word(val[p]) <= cut_hi;
     }
     // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
-    double lin = __shfl_down_sync(FULL, val[0], 1);
+    R lin = __shfl_down_sync(FULL, val[0], 1);
     if constexpr (BORDERED) {
-      if (lane == 31) lin = EKB_INF;
+      if (lane == 31) lin = INF;
     }
 #pragma unroll
     for (int m = 0; m < H; ++m) {
       const int p = 2 * m + 1;
-      const double L = (p == P - 1) ? lin : val[p + 1];
-      const double v = cell<KIND, MODE>(val[p], val[p - 1], L, XW(m + 1), YW(m), kk[p], st[p], prm);
+      const R L = (p == P - 1) ? lin : val[p + 1];
+      const R v = cell<KIND, MODE>(val[p], val[p - 1], L, XW(m + 1), YW(m), kk[p], st[p], prm);
       if constexpr (BORDERED) {
-        val[p] = (upd[p] || tb[p] == t + 1) ? v : EKB_INF;
+        val[p] = (upd[p] || tb[p] == t + 1) ? v : INF;
       } else if constexpr (COST_MASK) {
         val[p] = v;
       } else {
-        val[p] = upd[p] ? v : EKB_INF;
+        val[p] = upd[p] ? v : INF;
       }
       alive |= hi_word(val[p]) <= cut_hi;
     }
@@ -256,8 +269,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     }
     if constexpr (ROT) {
       // logical xw[H] of the next step is ring slot rx; logical yw[0] is ring slot (ry+H-1)%H
-      const double xprev = XW(H).x;
-      const double yprev = YW(0).y;
+      const R xprev = XW(H).x;
+      const R yprev = YW(0).y;
       xw[rx] = make_row<KIND, MODE>(X.at(I0 + H - 1), xprev, prm);
       yw[(ry + H - 1) % H] = make_col<KIND, MODE>(Y.at(J0 - 1), yprev, prm);
     } else {
@@ -273,8 +286,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   constexpr int REP = (U >= 16) ? 1 : 16 / U;  // unrolled blocks between cutoff refreshes
   bool finished = false;
   while (!finished) {
-    double nextcut = cut;
-    if constexpr (SHARED_CUT) nextcut = ld_cut(cutp);  // consumed after this block of double steps
+    R nextcut = cut;
+    if constexpr (SHARED_CUT) nextcut = to_cut<R>(ld_cut(cutp));  // consumed after this block of double steps
 #pragma unroll 1
     for (int b = 0; b < REP && !finished; ++b) {
       if constexpr (ROT) {  // stage series data for the whole unrolled block at once
@@ -298,15 +311,15 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     res.cost = EKB_INF;
     return res;
   }
-  if constexpr (SHARED_CUT) cut = fmin(cut, ld_cut(cutp));
+  if constexpr (SHARED_CUT) cut = fmin(cut, to_cut<R>(ld_cut(cutp)));
   const int sf = (nl - nc) - dbase;
   const int pf = sf % P;
-  double r = val[0];
+  R r = val[0];
 #pragma unroll
   for (int p = 1; p < P; ++p)
     if (p == pf) r = val[p];
   r = __shfl_sync(FULL, r, sf / P);
-  res.cost = (r <= cut) ? r : EKB_INF;
+  res.cost = (r <= cut) ? (double)r : EKB_INF;
   return res;
 }
 

@@ -70,17 +70,18 @@ struct PairDesc {
 // ---- staging helpers -------------------------------------------------------
 
 // pads: index -1 = the kind's predecessor of element 0, [-pad, -2] = 0.0, [n, n+pad) = +inf
-template <int KIND>
-__device__ __forceinline__ void stage_pads(double* dst, int n, int pad, double first) {
+// R = float (FP32 mode) stages the float64 inputs rounded to nearest.
+template <int KIND, class R>
+__device__ __forceinline__ void stage_pads(R* dst, int n, int pad, double first) {
   const int lane = threadIdx.x & 31;
   for (int k = lane + 1; k <= pad; k += 32) {
-    dst[-k] = (k == 1) ? pad_before<KIND>(first) : 0.0;
-    dst[n + k - 1] = EKB_INF;
+    dst[-k] = (k == 1) ? pad_before<KIND, R>((R)first) : (R)0.0;
+    dst[n + k - 1] = rinf<R>();
   }
 }
 
-template <int KIND>
-__device__ __forceinline__ void stage_series(double* dst, const double* __restrict__ src, int n, int pad) {
+template <int KIND, class R>
+__device__ __forceinline__ void stage_series(R* dst, const double* __restrict__ src, int n, int pad) {
   const int lane = threadIdx.x & 31;
   int k = lane;
   for (; k + 7 * 32 < n; k += 8 * 32) {  // eight loads in flight per lane before the stores
@@ -88,21 +89,21 @@ __device__ __forceinline__ void stage_series(double* dst, const double* __restri
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = __ldg(src + k + 32 * u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) dst[k + 32 * u] = v[u];
+    for (int u = 0; u < 8; ++u) dst[k + 32 * u] = (R)v[u];
   }
-  for (; k < n; k += 32) dst[k] = __ldg(src + k);
+  for (; k < n; k += 32) dst[k] = (R)__ldg(src + k);
   stage_pads<KIND>(dst, n, pad, __ldg(src));
 }
 
-template <int KIND>
-__device__ __forceinline__ void stage_table(double* tab, int len, const Params& prm) {
+template <int KIND, class R>
+__device__ __forceinline__ void stage_table(R* tab, int len, const Params& prm) {
   const int lane = threadIdx.x & 31;
   if constexpr (KIND == K_WDTW) {
-    for (int k = lane; k < len; k += 32) tab[k] = (k < prm.wt_len) ? prm.wt[k] : 0.0;
+    for (int k = lane; k < len; k += 32) tab[k] = (k < prm.wt_len) ? (R)prm.wt[k] : (R)0.0;
   } else if constexpr (KIND == K_TWE) {
     for (int k = lane; k < len; k += 32) {
-      double dij = (double)k;
-      tab[k] = dmul(prm.nu, dadd(dij, dij));
+      R dij = (R)k;
+      tab[k] = dmul((R)prm.nu, dadd(dij, dij));
     }
   }
 }
@@ -123,7 +124,7 @@ __device__ __forceinline__ int engine_band(int nl, int nc, int w) {
 
 template <int KIND, int MODE, int ENG, bool SHARED_CUT, class XAcc, class YAcc, class Loader>
 __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
-                                           const unsigned long long* cutp, const double* tab, int tablen,
+                                           const unsigned long long* cutp, const real_t<MODE>* tab, int tablen,
                                            const Params& prm, Loader& ld, double& cost, int& tend) {
   if constexpr (engine_guarded(ENG)) {
     // the widest band that fits 32 lanes of P slots; guard the sides it narrows
@@ -150,7 +151,8 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
     cost = r.cost;
     tend = r.t_end;
   } else if constexpr (engine_is_strip(ENG)) {
-    double* sb = prm.strip_buf + (size_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 3 * prm.strip_stride;
+    real_t<MODE>* sb = (real_t<MODE>*)prm.strip_buf +
+                       (size_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 3 * prm.strip_stride;
     StripeResult r = strip_pair<KIND, MODE, ENG != E_STRIP16, SHARED_CUT, ENG == E_STRIP16_EA>(
         X, nl, Y, nc, w, cut, cutp, tab, tablen, prm, sb, sb + prm.strip_stride, sb + 2 * prm.strip_stride);
     cost = r.cost;
@@ -204,9 +206,10 @@ __global__ void __launch_bounds__(128) k_pairs(const double* __restrict__ series
   constexpr int PAD = engine_pad(ENG);
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double* X = smem + wib * warp_stride(lmax, ENG) + PAD;
-  double* Y = X + series_slot(lmax, PAD);
-  double* tab = Y - PAD + series_slot(lmax, PAD);
+  using R = real_t<MODE>;
+  R* X = (R*)smem + wib * warp_stride(lmax, ENG) + PAD;
+  R* Y = X + series_slot(lmax, PAD);
+  R* tab = Y - PAD + series_slot(lmax, PAD);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   NoLoader ld;
   for (int pid = blockIdx.x * (blockDim.x >> 5) + wib; pid < npairs; pid += nwarps) {
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(128) k_pairs(const double* __restrict__ series
     __syncwarp();
     double cost;
     int tend;
-    run_engine<KIND, MODE, ENG, false>(SmemSeries{X, pd.nl}, pd.nl, SmemSeries{Y, pd.nc}, pd.nc, pd.w, pd.cut,
+    run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{X, pd.nl}, pd.nl, SmemSeriesT<R>{Y, pd.nc}, pd.nc, pd.w, pd.cut,
                                        nullptr, tab, tablen, pp, ld, cost, tend);
     const int cells = warp_cells<ENG>(pd.nl, pd.nc, pd.w, tend, KIND == K_ERP ? 0 : 1);
     if (lane == 0) {
@@ -255,9 +258,10 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
   constexpr int PAD = engine_pad(ENG);
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double* X = smem + wib * warp_stride(lmax, ENG) + PAD;
-  double* Y = X + series_slot(lmax, PAD);
-  double* tab = Y - PAD + series_slot(lmax, PAD);
+  using R = real_t<MODE>;
+  R* X = (R*)smem + wib * warp_stride(lmax, ENG) + PAD;
+  R* Y = X + series_slot(lmax, PAD);
+  R* tab = Y - PAD + series_slot(lmax, PAD);
   const long long npairs = (long long)n * (n - 1) / 2;
   NoLoader ld;
   unsigned long long my_cells = 0;
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
       const int tablen = max(nl, nc) + 1;
       if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
       __syncwarp();
-      run_engine<KIND, MODE, ENG, false>(SmemSeries{X, nl}, nl, SmemSeries{Y, nc}, nc, w, EKB_INF, nullptr, tab,
+      run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, EKB_INF, nullptr, tab,
                                          tablen, pp, ld, cost, tend);
       my_cells += (unsigned long long)warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1);
     }
@@ -300,8 +304,9 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
 constexpr int kChunk = 128;  // candidate staging granule (4 doubles per lane)
 
 // Lazily staged candidate; the first chunk arrives prefetched.
+template <class R>
 struct LazyCand {
-  double* buf;
+  R* buf;
   const double* src;
   int n, loaded;
   bool is_x;  // backs the lines series (else the cols series)
@@ -313,7 +318,7 @@ struct LazyCand {
 #pragma unroll
       for (int u = 0; u < kChunk / 32; ++u) {
         const int k = base + u * 32 + lane;
-        if (k < n) buf[k] = __ldg(src + k);
+        if (k < n) buf[k] = (R)__ldg(src + k);
       }
       loaded = min(base + kChunk, n);
     }
@@ -346,9 +351,10 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
   constexpr int PF = kChunk / 32;
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double* QB = smem + wib * warp_stride(lmax, ENG) + PAD;
-  double* CB = QB + series_slot(lmax, PAD);
-  double* tab = CB - PAD + series_slot(lmax, PAD);
+  using R = real_t<MODE>;
+  R* QB = (R*)smem + wib * warp_stride(lmax, ENG) + PAD;
+  R* CB = QB + series_slot(lmax, PAD);
+  R* tab = CB - PAD + series_slot(lmax, PAD);
   // two segments in one launch: ranks [rank_lo, rank_mid) in items of K1, then
   // [rank_mid, rank_hi) in items of K2, each round-major over the queries, so warps
   // that finish the first segment's tail start on the second at once.  Only the
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
           return t;
         };
         const float t0 = (i & 1) ? first(envB) : first(envA);
-        const LBScale sc = lb_scale(lb_threshold(cut));
+        const LBScale sc = lb_scale(lb_threshold<MODE>(cut, nl));
         const unsigned tot0 = lb_reduce(t0, sc);
         evaluate = evaluate && !sc.all && tot0 <= sc.T &&
                    warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, sc, tot0);
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < PF; ++u)
-          if (u * 32 + lane < lc) CB[u * 32 + lane] = pf[u];
+          if (u * 32 + lane < lc) CB[u * 32 + lane] = (R)pf[u];
         const double first = __shfl_sync(FULL, pf[0], 0);
         if (lc != cb_len || KIND == K_MSM) {
           stage_pads<KIND>(CB, lc, PAD, first);
@@ -464,15 +470,15 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
       int tend = 0;
       if (evaluate) {
         const Params pp = pair_params(prm, nl);
-        LazyCand ld{CB, csrc, lc, staged, !q_rows};
+        LazyCand<R> ld{CB, csrc, lc, staged, !q_rows};
         const int tablen = max(nl, nc) + 1;
         if constexpr (!engine_is_diag(ENG)) {
           ld.load_to(lc);  // the stripe engine reads all columns up front
           stage_table<KIND>(tab, tablen, pp);
         }
         __syncwarp();
-        const SmemSeries X{q_rows ? QB : CB, nl};
-        const SmemSeries Y{q_rows ? CB : QB, nc};
+        const SmemSeriesT<R> X{q_rows ? QB : CB, nl};
+        const SmemSeriesT<R> Y{q_rows ? CB : QB, nc};
         run_engine<KIND, MODE, ENG, true>(X, nl, Y, nc, w, cut, cutbits + q, tab, tablen, pp, ld, cost, tend);
         if (share && lane == 0 && cost < EKB_INF) {
           // values are >= 0 (or +inf), so IEEE bits order as unsigned integers
@@ -507,9 +513,10 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
   constexpr int PAD = engine_pad(ENG);
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double* X = smem + wib * warp_stride(lmax, ENG) + PAD;
-  double* Y = X + series_slot(lmax, PAD);
-  double* tab = Y - PAD + series_slot(lmax, PAD);
+  using R = real_t<MODE>;
+  R* X = (R*)smem + wib * warp_stride(lmax, ENG) + PAD;
+  R* Y = X + series_slot(lmax, PAD);
+  R* tab = Y - PAD + series_slot(lmax, PAD);
   const int n = *count;
   NoLoader ld;
   for (;;) {
@@ -533,7 +540,7 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
     const double cut = ld_cut(cutbits + q);
     double cost;
     int tend;
-    run_engine<KIND, MODE, ENG, true>(SmemSeries{X, nl}, nl, SmemSeries{Y, nc}, nc, w, cut, cutbits + q, tab, tablen,
+    run_engine<KIND, MODE, ENG, true>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, cut, cutbits + q, tab, tablen,
                                       pp, ld, cost, tend);
     const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) : 0;
     if (lane == 0) {

@@ -21,28 +21,30 @@ using UBFn = void (*)(const double*, const long long*, const int*, int, const do
 // diagonal_upper_bound (engines.py:87-103): the diagonal then the last column, the
 // cost of one admissible path, seeds a query's cutoff.  One warp per query, terms
 // summed in parallel and rounded up (k_ub_init).
-template <int KIND, int MODE>
-__device__ __forceinline__ double ub_term(const double* X, const double* Y, int nc, int k, const Params& pp) {
-  auto xv = [&](int i) { return i < 0 ? pad_before<KIND>(X[0]) : X[i]; };
-  auto yv = [&](int j) { return j < 0 ? pad_before<KIND>(Y[0]) : Y[j]; };
+// (FP32 mode: the same terms in float, from the float-rounded series, as the DP sees them)
+template <int KIND, int MODE, class Acc>
+__device__ __forceinline__ real_t<MODE> ub_term(const Acc& X, const Acc& Y, int nc, int k, const Params& pp) {
+  using R = real_t<MODE>;
+  auto xv = [&](int i) -> R { return i < 0 ? pad_before<KIND, R>((R)X[0]) : (R)X[i]; };
+  auto yv = [&](int j) -> R { return j < 0 ? pad_before<KIND, R>((R)Y[0]) : (R)Y[j]; };
   if (k <= nc) {  // canonical(k, k)
-    const RowD<KIND> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
-    const double y = yv(k - 1);
-    if constexpr (KIND == K_WDTW) return dmul(pcost<MODE>(r.x, y), pp.wt[0]);
+    const RowD<KIND, R> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
+    const R y = yv(k - 1);
+    if constexpr (KIND == K_WDTW) return dmul(pcost<MODE>(r.x, y), (R)pp.wt[0]);
     else if constexpr (KIND == K_MSM) return fabs(dsub(r.x, y));
     else if constexpr (KIND == K_TWE)
-      return dadd(dadd(pcost<MODE>(r.x, y), pcost<MODE>(k >= 2 ? X[k - 2] : 0.0, k >= 2 ? Y[k - 2] : 0.0)),
-                  dmul(pp.nu, dadd(0.0, 0.0)));
+      return dadd(dadd(pcost<MODE>(r.x, y), pcost<MODE>(k >= 2 ? (R)X[k - 2] : (R)0.0, k >= 2 ? (R)Y[k - 2] : (R)0.0)),
+                  dmul((R)pp.nu, dadd((R)0.0, (R)0.0)));
     else return pcost<MODE>(r.x, y);
   }
   // alt_row(k, nc) for the rows below the diagonal's end
-  const RowD<KIND> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
-  const double y = Y[nc - 1];
-  if constexpr (KIND == K_WDTW) return dmul(pcost<MODE>(r.x, y), pp.wt[k - nc]);
+  const RowD<KIND, R> r = make_row<KIND, MODE>(xv(k - 1), xv(k - 2), pp);
+  const R y = (R)Y[nc - 1];
+  if constexpr (KIND == K_WDTW) return dmul(pcost<MODE>(r.x, y), (R)pp.wt[k - nc]);
   else if constexpr (KIND == K_ERP || KIND == K_TWE) return r.ar;
   else if constexpr (KIND == K_MSM) {
-    const double e = dsub(r.x, y);
-    return msm_alt(sign_bit(e) != r.s, pp.msm_c, r.dr, fabs(e));
+    const R e = dsub(r.x, y);
+    return msm_alt(sign_bit(e) != r.s, (R)pp.msm_c, r.dr, fabs(e));
   } else return pcost<MODE>(r.x, y);
 }
 
@@ -71,11 +73,20 @@ __global__ void __launch_bounds__(128) k_ub_init(const double* __restrict__ Q, c
   // is >= the exact path cost; one more relative 2^-24 (rounded up) covers the
   // round-to-nearest error of the DP's own in-order sum (<= ~n 2^-53, n < 2^29), so
   // the seed is never below the candidate's DP value -- it stays a valid cutoff.
+  //
+  // FP32 mode: the float terms are summed exactly as above (rounded up, in double), and
+  // the DP's in-order float sum of n of them is at most (1 + 2^-24)^n times their exact
+  // sum, covered by (1 + (n+2) 2^-23); the seed is then rounded up to a float.
   double total = 0.0;
-  for (int k = 1 + lane; k <= nl; k += 32) total = __dadd_ru(total, ub_term<KIND, MODE>(X, Y, nc, k, pp));
+  for (int k = 1 + lane; k <= nl; k += 32) total = __dadd_ru(total, (double)ub_term<KIND, MODE>(X, Y, nc, k, pp));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total = __dadd_ru(total, __shfl_xor_sync(FULL, total, o));
-  total = __dmul_ru(total, 1.0 + 0x1p-24);
+  if constexpr ((MODE & M_F32) != 0) {
+    total = __dmul_ru(total, 1.0 + (double)(nl + 2) * 0x1p-23);
+    total = (double)__double2float_ru(total);
+  } else {
+    total = __dmul_ru(total, 1.0 + 0x1p-24);
+  }
   if (lane == 0) cutbits[q] = (unsigned long long)__double_as_longlong(total);
 }
 
@@ -121,7 +132,7 @@ __global__ void __launch_bounds__(32) k_pairs_ref(const double* __restrict__ ser
       double total = 0.0;
       for (int base = 1; base <= nl; base += 32) {
         const int k = base + lane;
-        terms[lane] = (k <= nl) ? ub_term<KIND, MODE>(X, Y, nc, k, pp) : 0.0;
+        terms[lane] = (k <= nl) ? ub_term<KIND, MODE>((const double*)X, (const double*)Y, nc, k, pp) : 0.0;
         __syncwarp();
         if (lane == 0)
           for (int u = 0; u < min(32, nl - base + 1); ++u) total = dadd(total, terms[u]);
@@ -172,10 +183,16 @@ PairsFn get_pairs(int mode, int eng) {
   switch (mode * 16 + eng) {
     EKB_ENG_CASES(0, k_pairs)
     EKB_ENG_CASES(1, k_pairs)
+    EKB_ENG_CASES(2, k_pairs)
+    EKB_ENG_CASES(3, k_pairs)
     case 0 * 16 + E_STR16_EA: return k_pairs<KIND, 0, E_STR16_EA>;
     case 1 * 16 + E_STR16_EA: return k_pairs<KIND, 1, E_STR16_EA>;
+    case 2 * 16 + E_STR16_EA: return k_pairs<KIND, 2, E_STR16_EA>;
+    case 3 * 16 + E_STR16_EA: return k_pairs<KIND, 3, E_STR16_EA>;
     case 0 * 16 + E_STRIP16_EA: return k_pairs<KIND, 0, E_STRIP16_EA>;
     case 1 * 16 + E_STRIP16_EA: return k_pairs<KIND, 1, E_STRIP16_EA>;
+    case 2 * 16 + E_STRIP16_EA: return k_pairs<KIND, 2, E_STRIP16_EA>;
+    case 3 * 16 + E_STRIP16_EA: return k_pairs<KIND, 3, E_STRIP16_EA>;
   }
   return nullptr;
 }
@@ -185,8 +202,12 @@ TriFn get_triangle(int mode, int eng) {
   switch (mode * 16 + eng) {
     EKB_ENG_CASES(0, k_triangle)
     EKB_ENG_CASES(1, k_triangle)
+    EKB_ENG_CASES(2, k_triangle)
+    EKB_ENG_CASES(3, k_triangle)
     case 0 * 16 + E_DIAG2: return k_triangle<KIND, 0, E_DIAG2>;
     case 1 * 16 + E_DIAG2: return k_triangle<KIND, 1, E_DIAG2>;
+    case 2 * 16 + E_DIAG2: return k_triangle<KIND, 2, E_DIAG2>;
+    case 3 * 16 + E_DIAG2: return k_triangle<KIND, 3, E_DIAG2>;
   }
   return nullptr;
 }
@@ -196,10 +217,16 @@ NNFn get_nn(int mode, int eng) {
   switch (mode * 16 + eng) {
     EKB_ENG_CASES(0, k_nn)
     EKB_ENG_CASES(1, k_nn)
+    EKB_ENG_CASES(2, k_nn)
+    EKB_ENG_CASES(3, k_nn)
     case 0 * 16 + E_GDIAG8: return k_nn<KIND, 0, E_GDIAG8>;
     case 1 * 16 + E_GDIAG8: return k_nn<KIND, 1, E_GDIAG8>;
+    case 2 * 16 + E_GDIAG8: return k_nn<KIND, 2, E_GDIAG8>;
+    case 3 * 16 + E_GDIAG8: return k_nn<KIND, 3, E_GDIAG8>;
     case 0 * 16 + E_GDIAG16: return k_nn<KIND, 0, E_GDIAG16>;
     case 1 * 16 + E_GDIAG16: return k_nn<KIND, 1, E_GDIAG16>;
+    case 2 * 16 + E_GDIAG16: return k_nn<KIND, 2, E_GDIAG16>;
+    case 3 * 16 + E_GDIAG16: return k_nn<KIND, 3, E_GDIAG16>;
   }
   return nullptr;
 }
@@ -222,13 +249,33 @@ NNFixFn get_nn_fix(int mode, int eng) {
     case 1 * 16 + E_STRIP16: return k_nn_fix<KIND, 1, E_STRIP16>;
     case 0 * 16 + E_STRIPB16: return k_nn_fix<KIND, 0, E_STRIPB16>;
     case 1 * 16 + E_STRIPB16: return k_nn_fix<KIND, 1, E_STRIPB16>;
+    case 2 * 16 + E_STR4: return k_nn_fix<KIND, 2, E_STR4>;
+    case 3 * 16 + E_STR4: return k_nn_fix<KIND, 3, E_STR4>;
+    case 2 * 16 + E_STR8: return k_nn_fix<KIND, 2, E_STR8>;
+    case 3 * 16 + E_STR8: return k_nn_fix<KIND, 3, E_STR8>;
+    case 2 * 16 + E_STR16: return k_nn_fix<KIND, 2, E_STR16>;
+    case 3 * 16 + E_STR16: return k_nn_fix<KIND, 3, E_STR16>;
+    case 2 * 16 + E_DIAG16: return k_nn_fix<KIND, 2, E_DIAG16>;
+    case 3 * 16 + E_DIAG16: return k_nn_fix<KIND, 3, E_DIAG16>;
+    case 2 * 16 + E_STRB16: return k_nn_fix<KIND, 2, E_STRB16>;
+    case 3 * 16 + E_STRB16: return k_nn_fix<KIND, 3, E_STRB16>;
+    case 2 * 16 + E_STRIP16: return k_nn_fix<KIND, 2, E_STRIP16>;
+    case 3 * 16 + E_STRIP16: return k_nn_fix<KIND, 3, E_STRIP16>;
+    case 2 * 16 + E_STRIPB16: return k_nn_fix<KIND, 2, E_STRIPB16>;
+    case 3 * 16 + E_STRIPB16: return k_nn_fix<KIND, 3, E_STRIPB16>;
   }
   return nullptr;
 }
 
 template <int KIND>
 UBFn get_ub(int mode) {
-  return mode == 0 ? k_ub_init<KIND, 0> : k_ub_init<KIND, 1>;
+  switch (mode) {
+    case 0: return k_ub_init<KIND, 0>;
+    case 1: return k_ub_init<KIND, 1>;
+    case 2: return k_ub_init<KIND, 2>;
+    case 3: return k_ub_init<KIND, 3>;
+  }
+  return nullptr;
 }
 
 #define EKB_INSTANTIATE_KIND(K)                  \

@@ -30,18 +30,25 @@ constexpr int LB_BATCH = 4;
 // the sum is a guaranteed lower bound of the exact bound: q is widened to
 // [RD(q), RU(q)], the distances to the (outward-rounded) envelope are rounded down,
 // squared and summed rounding down.  Returns this lane's partial sum.
-template <int MODE>
-__device__ __forceinline__ float lb_lane_terms(const double* qs, int base, int L, const float2 (&e)[LB_BATCH]) {
+// FP32 mode (R = float): the staged values are floats already, the interval is a point.
+template <int MODE, class R>
+__device__ __forceinline__ float lb_lane_terms(const R* qs, int base, int L, const float2 (&e)[LB_BATCH]) {
   const int lane = threadIdx.x & 31;
   float t = 0.f;
 #pragma unroll
   for (int b = 0; b < LB_BATCH; ++b) {
     const int k = base + b * 32 + lane;
-    const double qi = k < L ? qs[k] : 0.0;
-    const float qlo = __double2float_rd(qi), qhi = __double2float_ru(qi);
+    float qlo, qhi;
+    if constexpr (std::is_same<R, float>::value) {
+      qlo = qhi = k < L ? qs[k] : 0.f;
+    } else {
+      const double qi = k < L ? qs[k] : 0.0;
+      qlo = __double2float_rd(qi);
+      qhi = __double2float_ru(qi);
+    }
     // distance to [lower, upper] (upper >= lower), branch-free; neutral interval -> 0
     const float d = fmaxf(fmaxf(__fsub_rd(qlo, e[b].x), __fsub_rd(e[b].y, qhi)), 0.f);
-    t = __fadd_rd(t, MODE == 0 ? __fmul_rd(d, d) : d);
+    t = __fadd_rd(t, (MODE & 1) == 0 ? __fmul_rd(d, d) : d);
   }
   return t;
 }
@@ -90,8 +97,8 @@ __device__ __forceinline__ void lb_load(const float2* __restrict__ env, int base
 
 // Continues the test past the prefetched first batch (running scaled total `total`).
 // Returns true when the candidate must still be evaluated.
-template <int MODE>
-__device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __restrict__ env, int L,
+template <int MODE, class R>
+__device__ __forceinline__ bool warp_lb_rest(const R* qs, const float2* __restrict__ env, int L,
                                              const LBScale& sc, unsigned total) {
   for (int base = 32 * LB_BATCH; base < L; base += 32 * LB_BATCH) {
     float2 e[LB_BATCH];
@@ -105,8 +112,8 @@ __device__ __forceinline__ bool warp_lb_rest(const double* qs, const float2* __r
 // The reverse bound LB_Keogh(candidate, envelope(query)) (lb_keogh2's second order,
 // lower_bounds.py:87-98) over a candidate staged in shared memory; the query
 // envelope comes from global memory.  true when the pair must still be evaluated.
-template <int MODE>
-__device__ __forceinline__ bool warp_lb_reverse(const double* cs, const float2* __restrict__ envq, int L,
+template <int MODE, class R>
+__device__ __forceinline__ bool warp_lb_reverse(const R* cs, const float2* __restrict__ envq, int L,
                                                 const LBScale& sc) {
   unsigned total = 0;
   for (int base = 0; base < L; base += 32 * LB_BATCH) {
@@ -118,7 +125,16 @@ __device__ __forceinline__ bool warp_lb_reverse(const double* cs, const float2* 
   return true;
 }
 
-// bound > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header)
-__device__ __forceinline__ double lb_threshold(double cut) { return cut * (1.0 + 2.3283064365386963e-10); }
+// bound > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header).
+// FP32 mode: the bound is exact for the float-rounded series the DP sees (rounding is
+// monotone, so the outward float envelope still encloses them), and the float DP value
+// of any path is >= its exact cost * (1 - u)^(2n+3), u = 2^-24 (each term passes
+// through <= 2n+3 roundings); hence the wider margin (1 + (2n+8) 2^-24), rounded up.
+template <int MODE>
+__device__ __forceinline__ double lb_threshold(double cut, int n) {
+  if constexpr ((MODE & M_F32) != 0) return __dmul_ru(cut, 1.0 + (double)(2 * n + 8) * 0x1p-24);
+  return cut * (1.0 + 2.3283064365386963e-10);
+}
+__device__ __forceinline__ double lb_threshold(double cut) { return lb_threshold<0>(cut, 0); }
 
 }  // namespace ekb

@@ -41,9 +41,12 @@ struct NoRec {
 // tab: per-pair |i-j| table in shared memory (WDTW: weights; TWE: nu*(d+d)); len >= max(nl,nc)+1.
 template <int KIND, int MODE, int S, bool BANDED, bool SHARED_CUT, bool EA, class XAcc, class YAcc,
           class Rec = NoRec>
-__device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
-                                    const unsigned long long* cutp, const double* tab, int tablen,
+__device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut64,
+                                    const unsigned long long* cutp, const real_t<MODE>* tab, int tablen,
                                     const Params& prm, const Rec& rec = Rec{}) {
+  using R = real_t<MODE>;
+  const R INF = rinf<R>();
+  R cut = to_cut<R>(cut64);
   const int lane = threadIdx.x & 31;
   constexpr bool BORDERED = (KIND == K_ERP);
   constexpr bool TWE = (KIND == K_TWE);
@@ -57,24 +60,24 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   // +inf pad past the end, a finite one before it) so those rows stay +inf
   auto cx = [&](int k) { return X.at(min(max(k, -1), nl)); };
 
-  ColD<KIND> cols[S];
-  double val[S];
-  double pcr[TWE ? S : 1];  // TWE: pc of the previous row per column
+  ColD<KIND, R> cols[S];
+  R val[S];
+  R pcr[TWE ? S : 1];  // TWE: pc of the previous row per column
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int j = jbase + 1 + s;
     cols[s] = make_col<KIND, MODE>(cy(j - 1), cy(j - 2), prm);
-    val[s] = EKB_INF;
+    val[s] = INF;
     if constexpr (TWE) pcr[s] = pcost<MODE>(cx(r0 - 2), cols[s].y);
   }
   // hand-over state from the left neighbour (value of column jbase for the previous row)
-  double dg = EKB_INF;     // (i-1, jbase)
-  double dgpc = 0.0;       // TWE: pc at (i-1, jbase)
-  double xprev = cx(r0 - 2);
-  double vb = 0.0;         // lane 0: ERP left border accumulator
-  const double ycol0 = cy(jbase - 1);  // c_{jbase} for the column-0 pc of lane 0 / TWE hand-over
+  R dg = INF;     // (i-1, jbase)
+  R dgpc = R(0);       // TWE: pc at (i-1, jbase)
+  R xprev = cx(r0 - 2);
+  R vb = R(0);         // lane 0: ERP left border accumulator
+  const R ycol0 = cy(jbase - 1);  // c_{jbase} for the column-0 pc of lane 0 / TWE hand-over
   if (lane == 0) {
-    dg = BORDERED ? EKB_INF : 0.0;  // (r0-1, 0): ERP starts at row 0 (nothing above); else corner (0,0)
+    dg = BORDERED ? INF : R(0);  // (r0-1, 0): ERP starts at row 0 (nothing above); else corner (0,0)
     if constexpr (TWE) dgpc = pcost<MODE>(cx(r0 - 2), ycol0);
   }
   if constexpr (TWE) {
@@ -88,20 +91,20 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   const bool last_is_i0 = ((nl - r0) & 1) == 0;
   bool alive2 = false;   // alive over the previous step
   bool ea_flag = false;  // EA: some row minimum exceeded the cutoff
-  double nextcut = cut;
+  R nextcut = cut;
   int cut_hi = hi_word(cut);
   int t = 0;
   bool dead = false;
-  double last0 = EKB_INF, last1 = EKB_INF;  // this lane's last column for rows i0 / i1
-  double lastpc0 = 0.0, lastpc1 = 0.0;
-  double rmo0 = EKB_INF, rmo1 = EKB_INF;
-  double fin = EKB_INF;  // final cell when row nl is an i0 row
+  R last0 = INF, last1 = INF;  // this lane's last column for rows i0 / i1
+  R lastpc0 = R(0), lastpc1 = R(0);
+  R rmo0 = INF, rmo1 = INF;
+  R fin = INF;  // final cell when row nl is an i0 row
   const int sf = (nc - 1) % S;
 
   // one row over this lane's S columns; prev[] holds row i-1 on entry, row i on exit
   int ea_row = 0x7fffffff;
-  auto row_pass = [&](int i, const RowD<KIND>& rd, double lft, double dgl, double dpc, double& rmin,
-                      double (&row)[S], bool& alive) {
+  auto row_pass = [&](int i, const RowD<KIND, R>& rd, R lft, R dgl, R dpc, R& rmin,
+                      R (&row)[S], bool& alive) {
     unsigned live_bits = 0;
     int a = 0, b = S - 1;
     if constexpr (BANDED) {
@@ -112,18 +115,18 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int j = jbase + 1 + s;
-      const double up = row[s];
-      DiagK<KIND> k{};  // off = 0.0: the stripe engine masks the band itself
+      const R up = row[s];
+      DiagK<KIND, R> k{};  // off = 0.0: the stripe engine masks the band itself
       if constexpr (KIND == K_WDTW) k.w = tab[min(abs(i - j), tablen - 1)];
       if constexpr (TWE) k.tw = tab[min(abs(i - j), tablen - 1)];
-      SlotS<KIND> stt;
-      double upc = 0.0;
+      SlotS<KIND, R> stt;
+      R upc = R(0);
       if constexpr (TWE) {
         stt.pcp = dpc;
         upc = pcr[s];
       }
-      double v = cell<KIND, MODE, false>(dgl, up, lft, rd, cols[s], k, stt, prm);
-      if constexpr (BANDED) v = (s >= a && s <= b) ? v : EKB_INF;
+      R v = cell<KIND, MODE, false>(dgl, up, lft, rd, cols[s], k, stt, prm);
+      if constexpr (BANDED) v = (s >= a && s <= b) ? v : INF;
       if constexpr (TWE) {
         pcr[s] = stt.pcp;  // pc(l_i, c_j) for the next row
         dpc = upc;
@@ -144,7 +147,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
 
   for (t = 0; t < nsteps; ++t) {
     if constexpr (SHARED_CUT) {
-      if ((t & 15) == 0) nextcut = ld_cut(cutp);
+      if ((t & 15) == 0) nextcut = to_cut<R>(ld_cut(cutp));
       if ((t & 15) == 12) {
         cut = fmin(cut, nextcut);
         cut_hi = hi_word(cut);
@@ -152,40 +155,40 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
     }
     const int i0 = r0 + 2 * (t - lane), i1 = i0 + 1;
     // the left neighbour's last column for rows i0, i1 (computed at step t-1)
-    double lb0 = __shfl_up_sync(FULL, last0, 1);
-    double lb1 = __shfl_up_sync(FULL, last1, 1);
-    double lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1) : 0.0;
-    double lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1) : 0.0;
-    double rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1) : EKB_INF;
-    double rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1) : EKB_INF;
-    const double x0 = cx(i0 - 1), x1 = cx(i1 - 1);
-    const RowD<KIND> rd0 = make_row<KIND, MODE>(x0, xprev, prm);
-    const RowD<KIND> rd1 = make_row<KIND, MODE>(x1, x0, prm);
+    R lb0 = __shfl_up_sync(FULL, last0, 1);
+    R lb1 = __shfl_up_sync(FULL, last1, 1);
+    R lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1) : R(0);
+    R lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1) : R(0);
+    R rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1) : INF;
+    R rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1) : INF;
+    const R x0 = cx(i0 - 1), x1 = cx(i1 - 1);
+    const RowD<KIND, R> rd0 = make_row<KIND, MODE>(x0, xprev, prm);
+    const RowD<KIND, R> rd1 = make_row<KIND, MODE>(x1, x0, prm);
     xprev = x1;
     if (lane == 0) {
       // border cells (i0, 0), (i1, 0)
       if constexpr (BORDERED) {
-        vb = (i0 == 0) ? 0.0 : dadd(vb, rd0.ar);  // vb[i] = vb[i-1] + pc(l_i, g)
-        lb0 = (i0 <= w + 1) ? vb : EKB_INF;
+        vb = (i0 == 0) ? R(0) : dadd(vb, rd0.ar);  // vb[i] = vb[i-1] + pc(l_i, g)
+        lb0 = (i0 <= w + 1) ? vb : INF;
         vb = dadd(vb, rd1.ar);
-        lb1 = (i1 <= w + 1) ? vb : EKB_INF;
+        lb1 = (i1 <= w + 1) ? vb : INF;
       } else {
-        lb0 = (i0 == 0) ? 0.0 : EKB_INF;
-        lb1 = EKB_INF;
+        lb0 = (i0 == 0) ? R(0) : INF;
+        lb1 = INF;
       }
       if constexpr (TWE) {
-        lbpc0 = pcost<MODE>(x0, 0.0);  // pc(l_i, c_0 := 0) of the border cell
-        lbpc1 = pcost<MODE>(x1, 0.0);
+        lbpc0 = pcost<MODE>(x0, R(0));  // pc(l_i, c_0 := 0) of the border cell
+        lbpc1 = pcost<MODE>(x1, R(0));
       }
-      rm0 = (i0 >= 1) ? lb0 : EKB_INF;  // ea: the border cell joins the row minimum
-      rm1 = (i1 >= 1) ? lb1 : EKB_INF;
+      rm0 = (i0 >= 1) ? lb0 : INF;  // ea: the border cell joins the row minimum
+      rm1 = (i1 >= 1) ? lb1 : INF;
       if constexpr (Rec::on) {
         if (i0 >= 1 && i0 <= nl) rec.vb(i0, lb0 <= cut);
         if (i1 >= 1 && i1 <= nl) rec.vb(i1, lb1 <= cut);
       }
     }
     bool alive = lane == 0 && (hi_word(lb0) <= cut_hi || hi_word(lb1) <= cut_hi);
-    double row0[S];
+    R row0[S];
 #pragma unroll
     for (int s2 = 0; s2 < S; ++s2) row0[s2] = val[s2];
     // row i0: diagonal input (i0-1, jbase) is the left neighbour's row i1 of step t-1
@@ -237,7 +240,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
     return res;
   }
   // cell (nl, nc) lives in lane lf, slot (nc-1) % S, computed at its last step
-  double r = val[0];
+  R r = val[0];
 #pragma unroll
   for (int s = 1; s < S; ++s)
     if (s == sf) r = val[s];
@@ -245,10 +248,10 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   r = __shfl_sync(FULL, r, lf);
   if constexpr (EA) {
     const bool flagged = __any_sync(FULL, ea_flag);
-    res.cost = flagged ? EKB_INF : r;
+    res.cost = flagged ? INF : r;
   } else {
-    if constexpr (SHARED_CUT) cut = fmin(cut, ld_cut(cutp));
-    res.cost = (r <= cut) ? r : EKB_INF;
+    if constexpr (SHARED_CUT) cut = fmin(cut, to_cut<R>(ld_cut(cutp)));
+    res.cost = (r <= cut) ? r : INF;
   }
   return res;
 }
@@ -269,9 +272,12 @@ namespace ekb {
 // (border cell included, _speedups.pyx:147-160) into `rmin` and the result is +inf if
 // any row minimum exceeds the cutoff, else the exact cost.
 template <int KIND, int MODE, bool BANDED, bool SHARED_CUT, bool EA, class XAcc, class YAcc>
-__device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut,
-                                   const unsigned long long* cutp, const double* tab, int tablen,
-                                   const Params& prm, double* bin, double* bout, double* rmin) {
+__device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut64,
+                                   const unsigned long long* cutp, const real_t<MODE>* tab, int tablen,
+                                   const Params& prm, real_t<MODE>* bin, real_t<MODE>* bout, real_t<MODE>* rmin) {
+  using R = real_t<MODE>;
+  const R INF = rinf<R>();
+  R cut = to_cut<R>(cut64);
   constexpr int S = 16;
   constexpr int STRIP = 32 * S;
   const int lane = threadIdx.x & 31;
@@ -281,13 +287,13 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
   const int nstrips = (nc + STRIP - 1) / STRIP;
   auto cy = [&](int k) { return Y.at(min(max(k, -1), nc)); };
   auto cx = [&](int k) { return X.at(min(max(k, -1), nl)); };  // see stripe_pair
-  double nextcut = cut;
+  R nextcut = cut;
   int cut_hi = hi_word(cut);
   int steps_done = 0;
-  double result = EKB_INF;
+  R result = INF;
   bool dead = false;
   if constexpr (EA) {
-    for (int i = lane; i <= nl; i += 32) rmin[i] = EKB_INF;
+    for (int i = lane; i <= nl; i += 32) rmin[i] = INF;
     __syncwarp();
   }
 
@@ -296,31 +302,31 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
     const bool last_strip = sk == nstrips - 1;
     const int lf = last_strip ? (nc - 1 - sk * STRIP) / S : 31;
     const int sf = (nc - 1) % S;
-    ColD<KIND> cols[S];
-    double val[S];
-    double pcr[TWE ? S : 1];
+    ColD<KIND, R> cols[S];
+    R val[S];
+    R pcr[TWE ? S : 1];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int j = jbase + 1 + s;
       cols[s] = make_col<KIND, MODE>(cy(j - 1), cy(j - 2), prm);
-      val[s] = EKB_INF;
+      val[s] = INF;
       if constexpr (TWE) pcr[s] = pcost<MODE>(cx(r0 - 2), cols[s].y);
     }
-    double dg = EKB_INF, dgpc = 0.0;
-    double xprev = cx(r0 - 2);
-    double vb = 0.0;
-    const double ycol0 = cy(jbase - 1);
-    if (lane == 0 && sk == 0) dg = BORDERED ? EKB_INF : 0.0;
+    R dg = INF, dgpc = R(0);
+    R xprev = cx(r0 - 2);
+    R vb = R(0);
+    const R ycol0 = cy(jbase - 1);
+    if (lane == 0 && sk == 0) dg = BORDERED ? INF : R(0);
     if constexpr (TWE) dgpc = pcost<MODE>(cx(r0 - 2), ycol0);
     const int nsteps = lf + (nl - r0) / 2 + 1;
     const bool last_is_i0 = ((nl - r0) & 1) == 0;
     bool alive2 = false;
-    double last0 = EKB_INF, last1 = EKB_INF, lastpc0 = 0.0, lastpc1 = 0.0;
-    double rmo0 = EKB_INF, rmo1 = EKB_INF;
-    double fin = EKB_INF;
+    R last0 = INF, last1 = INF, lastpc0 = R(0), lastpc1 = R(0);
+    R rmo0 = INF, rmo1 = INF;
+    R fin = INF;
 
-    auto row_pass = [&](int i, const RowD<KIND>& rd, double lft, double dgl, double dpc, double (&row)[S],
-                        bool& alive, double& rm) {
+    auto row_pass = [&](int i, const RowD<KIND, R>& rd, R lft, R dgl, R dpc, R (&row)[S],
+                        bool& alive, R& rm) {
       int a = 0, b = S - 1;
       if constexpr (BANDED) {
         const int hi = (i == 0) ? w + 1 : i + w;
@@ -330,18 +336,18 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int j = jbase + 1 + s;
-        const double up = row[s];
-        DiagK<KIND> k{};
+        const R up = row[s];
+        DiagK<KIND, R> k{};
         if constexpr (KIND == K_WDTW) k.w = tab[min(abs(i - j), tablen - 1)];
         if constexpr (TWE) k.tw = tab[min(abs(i - j), tablen - 1)];
-        SlotS<KIND> stt;
-        double upc = 0.0;
+        SlotS<KIND, R> stt;
+        R upc = R(0);
         if constexpr (TWE) {
           stt.pcp = dpc;
           upc = pcr[s];
         }
-        double v = cell<KIND, MODE, false>(dgl, up, lft, rd, cols[s], k, stt, prm);
-        if constexpr (BANDED) v = (s >= a && s <= b) ? v : EKB_INF;
+        R v = cell<KIND, MODE, false>(dgl, up, lft, rd, cols[s], k, stt, prm);
+        if constexpr (BANDED) v = (s >= a && s <= b) ? v : INF;
         if constexpr (TWE) {
           pcr[s] = stt.pcp;
           dpc = upc;
@@ -357,45 +363,45 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
     int t = 0;
     for (t = 0; t < nsteps; ++t) {
       if constexpr (SHARED_CUT) {
-        if ((t & 15) == 0) nextcut = ld_cut(cutp);
+        if ((t & 15) == 0) nextcut = to_cut<R>(ld_cut(cutp));
         if ((t & 15) == 12) {
           cut = fmin(cut, nextcut);
           cut_hi = hi_word(cut);
         }
       }
       const int i0 = r0 + 2 * (t - lane), i1 = i0 + 1;
-      double lb0 = __shfl_up_sync(FULL, last0, 1);
-      double lb1 = __shfl_up_sync(FULL, last1, 1);
-      double lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1) : 0.0;
-      double lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1) : 0.0;
-      double rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1) : EKB_INF;
-      double rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1) : EKB_INF;
-      const double x0 = cx(i0 - 1), x1 = cx(i1 - 1);
-      const RowD<KIND> rd0 = make_row<KIND, MODE>(x0, xprev, prm);
-      const RowD<KIND> rd1 = make_row<KIND, MODE>(x1, x0, prm);
+      R lb0 = __shfl_up_sync(FULL, last0, 1);
+      R lb1 = __shfl_up_sync(FULL, last1, 1);
+      R lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1) : R(0);
+      R lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1) : R(0);
+      R rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1) : INF;
+      R rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1) : INF;
+      const R x0 = cx(i0 - 1), x1 = cx(i1 - 1);
+      const RowD<KIND, R> rd0 = make_row<KIND, MODE>(x0, xprev, prm);
+      const RowD<KIND, R> rd1 = make_row<KIND, MODE>(x1, x0, prm);
       xprev = x1;
       if (lane == 0) {
         if (sk == 0) {  // the matrix border (stripe_pair's lane 0)
           if constexpr (BORDERED) {
-            vb = (i0 == 0) ? 0.0 : dadd(vb, rd0.ar);
-            lb0 = (i0 <= w + 1) ? vb : EKB_INF;
+            vb = (i0 == 0) ? R(0) : dadd(vb, rd0.ar);
+            lb0 = (i0 <= w + 1) ? vb : INF;
             vb = dadd(vb, rd1.ar);
-            lb1 = (i1 <= w + 1) ? vb : EKB_INF;
+            lb1 = (i1 <= w + 1) ? vb : INF;
           } else {
-            lb0 = (i0 == 0) ? 0.0 : EKB_INF;
-            lb1 = EKB_INF;
+            lb0 = (i0 == 0) ? R(0) : INF;
+            lb1 = INF;
           }
           if constexpr (TWE) {
-            lbpc0 = pcost<MODE>(x0, 0.0);
-            lbpc1 = pcost<MODE>(x1, 0.0);
+            lbpc0 = pcost<MODE>(x0, R(0));
+            lbpc1 = pcost<MODE>(x1, R(0));
           }
-          rm0 = (i0 >= 1) ? lb0 : EKB_INF;  // ea: the border cell joins the row minimum
-          rm1 = (i1 >= 1) ? lb1 : EKB_INF;
+          rm0 = (i0 >= 1) ? lb0 : INF;  // ea: the border cell joins the row minimum
+          rm1 = (i1 >= 1) ? lb1 : INF;
         } else {  // the previous strip's last column (already in the previous strip's minimum)
-          rm0 = EKB_INF;
-          rm1 = EKB_INF;
-          lb0 = (i0 >= 0 && i0 <= nl) ? bin[i0] : EKB_INF;
-          lb1 = (i1 >= 0 && i1 <= nl) ? bin[i1] : EKB_INF;
+          rm0 = INF;
+          rm1 = INF;
+          lb0 = (i0 >= 0 && i0 <= nl) ? bin[i0] : INF;
+          lb1 = (i1 >= 0 && i1 <= nl) ? bin[i1] : INF;
           if constexpr (TWE) {
             lbpc0 = pcost<MODE>(x0, ycol0);
             lbpc1 = pcost<MODE>(x1, ycol0);
@@ -403,7 +409,7 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
         }
       }
       bool alive = lane == 0 && (hi_word(lb0) <= cut_hi || hi_word(lb1) <= cut_hi);
-      double row0[S];
+      R row0[S];
 #pragma unroll
       for (int s2 = 0; s2 < S; ++s2) row0[s2] = val[s2];
       row_pass(i0, rd0, lb0, dg, dgpc, row0, alive, rm0);
@@ -453,12 +459,12 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
         dead = true;
         break;
       }
-      double* tmp = bin;
+      R* tmp = bin;
       bin = bout;
       bout = tmp;
       __syncwarp();
     } else {
-      double r = val[0];
+      R r = val[0];
 #pragma unroll
       for (int s = 1; s < S; ++s)
         if (s == sf) r = val[s];
@@ -477,11 +483,11 @@ __device__ StripeResult strip_pair(const XAcc& X, int nl, const YAcc& Y, int nc,
     __syncwarp();
     bool over = false;
     for (int i = 1 + lane; i <= nl; i += 32) over |= rmin[i] > cut;
-    res.cost = __any_sync(FULL, over) ? EKB_INF : result;
+    res.cost = __any_sync(FULL, over) ? INF : result;
     return res;
   }
-  if constexpr (SHARED_CUT) cut = fmin(cut, ld_cut(cutp));
-  res.cost = (result <= cut) ? result : EKB_INF;
+  if constexpr (SHARED_CUT) cut = fmin(cut, to_cut<R>(ld_cut(cutp)));
+  res.cost = (result <= cut) ? result : INF;
   return res;
 }
 

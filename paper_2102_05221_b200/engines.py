@@ -39,18 +39,22 @@ class EngineResult(NamedTuple):
     cells_computed: int
 
 
-def distance_batch(spec: DistanceSpec, variant: str, pairs, cutoffs=None, windows=None, backend=None):
+def distance_batch(spec: DistanceSpec, variant: str, pairs, cutoffs=None, windows=None, backend=None,
+                   precision: str = "float64"):
     """One GPU call for many (s, t) pairs -> (costs float64[n], cells int64[n]).
 
     ``pairs`` is a sequence of (s, t) series (already validated or raw);
     ``cutoffs`` per pair (default +inf); ``windows`` per pair overrides
     ``spec.window`` like the ``window`` argument of compute_ea/eapruned.
+    ``precision="float32"`` runs the optional FP32 engines (costs within 1e-5
+    relative of the reference; cells are the band cells the engine evaluated).
     """
     from .series import as_series
 
     if variant not in VARIANTS:
         raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
     _backend.resolve(backend)
+    _lib.precision_code(precision)
     n = len(pairs)
     costs = np.empty(n, dtype=np.float64)
     cells = np.empty(n, dtype=np.int64)
@@ -60,7 +64,7 @@ def distance_batch(spec: DistanceSpec, variant: str, pairs, cutoffs=None, window
     ts = [as_series(p[1]) for p in pairs]
     flat, off, lens = _lib.ragged(ss + ts)
     longest = np.maximum(lens[:n], lens[n:])
-    h = _lib.SpecHandle(spec, longest_lengths=np.unique(longest))
+    h = _lib.SpecHandle(spec, longest_lengths=np.unique(longest), precision=precision)
     co = None
     if cutoffs is not None:
         co = np.ascontiguousarray(np.broadcast_to(np.asarray(cutoffs, dtype=np.float64), (n,)))

@@ -44,6 +44,9 @@ class SearchConfig:
     normalize: bool = False
     debug: bool = False
     backend: str | None = None
+    # not in the reference: "float32" selects the optional FP32 engines for nn_search /
+    # classify_1nn (distances within 1e-5 relative; near-ties may pick another index)
+    precision: str = "float64"
 
     def __post_init__(self):
         if self.variant not in VARIANTS:
@@ -52,6 +55,7 @@ class SearchConfig:
             raise SpecError(f"unknown lb mode {self.lb!r}; expected one of {LB_MODES}")
         if self.lb != "none" and self.spec.kind not in ("dtw", "cdtw"):
             raise SpecError("lower bounds are only available for dtw and cdtw")
+        _lib.precision_code(self.precision)
 
 
 @dataclass
@@ -98,13 +102,15 @@ def _pack(series):
     return _lib.ragged([as_series(x) for x in series])
 
 
-def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None):
+def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None, precision: str = "float64"):
     """1-NN of every query in one GPU call.
 
     Returns arrays (nn_index int64, nn_distance float64, cells, computed,
-    abandoned); nn_index is -1 when every candidate is +inf.
+    abandoned); nn_index is -1 when every candidate is +inf.  ``precision``
+    "float32" runs the optional FP32 engines.
     """
     _backend.resolve(backend)
+    _lib.precision_code(precision)
     if variant not in VARIANTS:
         raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
     qf, qo, ql = _pack(queries)
@@ -117,7 +123,7 @@ def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None
     if nq == 0:
         return tuple(out)
     longest = np.unique(np.maximum.outer(np.unique(ql), np.unique(cl)))
-    h = _lib.SpecHandle(spec, longest_lengths=longest)
+    h = _lib.SpecHandle(spec, longest_lengths=longest, precision=precision)
     L = _lib.lib()
     _lib.check(L.ek_nn(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(qf), len(qf), _lib.iptr(qo), _lib.iptr(ql), nq,
                        _lib.dptr(cf), len(cf), _lib.iptr(co), _lib.iptr(cl), len(cl), _lib.iptr(out[0]),
@@ -132,7 +138,8 @@ def nn_search(query, candidates, cfg: SearchConfig, envelopes=None):
     if not candidates:
         raise SearchError("candidate set is empty")
     start = time.perf_counter()
-    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, [query], candidates, backend=cfg.backend)
+    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, [query], candidates, backend=cfg.backend,
+                                          precision=cfg.precision)
     stats = SearchStats(computed=int(comp[0]), abandoned=int(ab[0]), cells=int(cells[0]))
     stats.wall_time = time.perf_counter() - start
     return float(dist[0]), int(idx[0]), stats
@@ -147,7 +154,8 @@ def classify_1nn(train: LabeledDataset, test: LabeledDataset, cfg: SearchConfig,
     """
     labels = train.labels
     start = time.perf_counter()
-    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, test.series, train.series, backend=cfg.backend)
+    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, test.series, train.series, backend=cfg.backend,
+                                          precision=cfg.precision)
     per_query = (time.perf_counter() - start) / max(1, len(test))
     records = []
     for q, (actual, _) in enumerate(test.entries):
@@ -167,6 +175,8 @@ def subsequence_search(query, reference, cfg: SearchConfig):
     """
     if cfg.spec.kind not in ("dtw", "cdtw"):
         raise SpecError("subsequence search supports dtw and cdtw only")
+    if cfg.precision != "float64":
+        raise SpecError("subsequence search runs in float64 only")
     query = as_series(query)
     reference = as_series(reference)
     lq = len(query)
@@ -214,23 +224,24 @@ def subsequence_profile(query, reference, spec: DistanceSpec, normalize: bool = 
     return out
 
 
-def pairwise(spec: DistanceSpec, X, variant: str = "pruned_only", backend=None):
+def pairwise(spec: DistanceSpec, X, variant: str = "pruned_only", backend=None, precision: str = "float64"):
     """Full symmetric matrix of ``distance(spec, variant, X[i], X[j])``, diagonal 0.0.
 
     The all-pairs loop of SURVEY.md 3.4 in one GPU call; d(a,b) == d(b,a)
     bit-exactly, so the upper triangle is evaluated and mirrored.  Returns
-    ``(D, cells)``.
+    ``(D, cells)``.  ``precision="float32"``: the optional FP32 engines.
     """
     if variant not in VARIANTS:
         raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
     _backend.resolve(backend)
+    _lib.precision_code(precision)
     flat, off, lens = _pack(X)
     n = len(lens)
     D = np.zeros((n, n), dtype=np.float64)
     if n == 0:
         return D, 0
     longest = np.unique(np.maximum.outer(np.unique(lens), np.unique(lens)))
-    h = _lib.SpecHandle(spec, longest_lengths=longest)
+    h = _lib.SpecHandle(spec, longest_lengths=longest, precision=precision)
     cells = np.zeros(1, dtype=np.int64)
     _lib.check(_lib.lib().ek_pairwise(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(flat), len(flat),
                                       _lib.iptr(off), _lib.iptr(lens), n, _lib.dptr(D), _lib.iptr(cells)))

@@ -2,6 +2,7 @@
 and failing loudly when no GPU is present (there is no CPU fallback)."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -73,6 +74,24 @@ def test_search_config_validation():
         SearchConfig(spec=dtw, lb="keogh3")
     with pytest.raises(SpecError):
         SearchConfig(spec=DistanceSpec(kind="msm", msm_c=0.5), lb="keogh2")
+    with pytest.raises(SpecError, match="unknown precision"):
+        SearchConfig(spec=dtw, precision="float16")
+    assert SearchConfig(spec=dtw, precision="float32").precision == "float32"
+
+
+def test_spec_struct_matches_header():
+    """EkSpec (ctypes) mirrors ek_spec of include/elastik_b200.h, precision last."""
+    import re
+
+    from paper_2102_05221_b200 import _lib
+
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "include", "elastik_b200.h")).read()
+    body = hdr[hdr.index("typedef struct ek_spec {"):hdr.index("} ek_spec;")]
+    names = re.findall(r"\b(\w+);", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
+    assert names == [f[0] for f in _lib.EkSpec._fields_]
+    with pytest.raises(SpecError, match="unknown precision"):
+        _lib.SpecHandle(DistanceSpec(kind="dtw"), precision="half")
 
 
 def test_backend_seam():

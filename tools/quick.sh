@@ -9,5 +9,5 @@ print("c2", round(d["value"]), round(d["ms_per_step"], 3), {a: round(b, 3) for a
       round(d["roofline"]["frac"], 3), "e2e", round(d.get("e2e", {}).get("value", 0)))
 for k, v in d.get("per_config", {}).items():
     print(k, round(v["value"], 2), v["unit"], round(v["ms_per_step"], 3), {a: round(b, 3) for a, b in v["phases_ms"].items()},
-          round(v["roofline"]["frac"], 3))
+          round(v["roofline"]["frac"], 3), v["roofline"]["bound"], v.get("nn_index_mismatch_rate", ""))
 PY
