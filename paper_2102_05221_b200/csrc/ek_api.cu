@@ -358,6 +358,12 @@ struct ParamHolder {
   }
 };
 
+// integer tuning knob from the environment (scheduling only; never changes a result)
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 // template MODE of the engines: cost mode | M_F32 for the float32 precision
 int spec_mode(const ek_spec* sp) { return sp->cost_mode | (sp->precision ? (int)M_F32 : 0); }
 // bytes per staged element (the FP32 mode stages floats)
@@ -577,12 +583,14 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
   const long long npairs = (long long)nq * ncand;
-  DBuf dord, dkeys, dout, dtend, dcut, dcnt, denv, denvq, denvs;
+  DBuf dord, dkeys, dskeys, dout, dtend, dcut, dcnt, denv, denvq, denvs;
   if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dout.alloc(sizeof(double) * (size_t)npairs, st) ||
       dtend.alloc(sizeof(int) * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
-      dcnt.alloc(sizeof(int) * 16, st))
+      dcnt.alloc(sizeof(int) * 128, st))
     return -1;
-  CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 16, st));
+  // ints 8, 9: guarded-band overflows and their redo counter; 32 / 64 / 96: the k_nn work
+  // counters (kNnCounters x u64) of phase A and of phase B's launches
+  CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 128, st));
   int* const ovf_count = dcnt.as<int>() + 8;  // guarded-band overflows (phase B) and their redo counter
   // phase B engine: with a cutoff, wide bands run as a guarded P=8 band (EAPruned's pruned
   // columns skipped wholesale; overflows are redone by k_nn_fix).  ERP keeps its window
@@ -594,29 +602,46 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     engB = guard_engine();
   DBuf dovf;
   if (engB != eng && dovf.alloc(sizeof(int2) * (size_t)npairs, st)) return -1;
-  // 0. LB envelopes on a side stream, overlapping the ranking and phase A: candidates'
-  //    for lb_keogh(query, env(candidate)), queries' for the survivors' reverse bound
-  const float2* env = nullptr;
+  // 0-1. candidate order.  LB path: envelopes, the LB_Keogh(q, env(c)) key of every pair
+  //      (k_lb_matrix, rounded down) and the candidates ranked by it; the query envelopes
+  //      for the survivors' reverse bound on a side stream.  Otherwise an approximate
+  //      Euclidean ranking.  The order is a schedule only: it never decides a result.
+  const bool rank = share && ncand <= 16384 && ncand > 1;
   if (use_lb) {
     const int L = max_len;
-    if (denv.alloc(sizeof(float2) * (size_t)L * ncand, st) || denvq.alloc(sizeof(float2) * (size_t)L * nq, st))
+    if (denv.alloc(sizeof(float2) * (size_t)L * ncand, st) || denvq.alloc(sizeof(float2) * (size_t)L * nq, st) ||
+        dskeys.alloc(sizeof(float) * (size_t)npairs, st))
       return -1;
+    void* scr = nullptr;  // long series: global table rows
+    DBuf denvs2;
+    void* scr2 = nullptr;
+    if (env_scratch_bytes(L, false)) {
+      if (denvs.alloc(env_scratch_bytes(L, false), st) || denvs2.alloc(env_scratch_bytes(L, false), st)) return -1;
+      scr = denvs.p;
+      scr2 = denvs2.p;
+    }
     CK(cudaEventRecord(g_ctx.ev_fork, st));
     CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_fork, 0));
-    void* scr = nullptr;  // long series: global table rows
-    if (env_scratch_bytes(L, false)) {
-      if (denvs.alloc(env_scratch_bytes(L, false), st)) return -1;
-      scr = denvs.p;
-    }
-    CK(envelope(dC, (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>(), scr, g_ctx.side));
-    CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr, g_ctx.side));
-    g_launches += 2;
+    CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr2, g_ctx.side));
     CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
-    env = denv.as<float2>();
-  }
-  // 1. candidate order: approximate Euclidean ranking (scheduling only)
-  const bool rank = share && ncand <= 16384 && ncand > 1;
-  if (rank) {
+    CK(envelope_pm(dC, (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>(), scr, st));
+    mark(st, "envelope");
+    DBuf dqt;
+    if (dkeys.alloc(sizeof(float) * (size_t)npairs, st) || dqt.alloc(sizeof(float2) * (size_t)nq * L, st)) return -1;
+    CK(lb_matrix(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, (const float2*)denv.as<float2>(), (int)ncand,
+                 L, dqt.as<float2>(), dkeys.as<float>(), st));
+    mark(st, "lb_keys");
+    // dkeys: the keys per (query, candidate); dskeys: the same in rank order
+    if (ncand <= 16384) {
+      CK(rank_radix((const float*)dkeys.as<float>(), (int)nq, (int)ncand, dord.as<int>(), st, dskeys.as<float>()));
+    } else {
+      if (launch_plain(k_identity_order, dim3(1024), dim3(256), 0, st, (int)nq, (int)ncand, dord.as<int>())) return -1;
+      CK(cudaMemcpyAsync(dskeys.p, dkeys.p, sizeof(float) * (size_t)npairs, cudaMemcpyDeviceToDevice, st));
+    }
+    if (launch_plain(k_fill_nn_out, dim3(592), dim3(256), 0, st, dout.as<double>(), dtend.as<int>(), npairs))
+      return -1;
+    g_launches += 4;
+  } else if (rank) {
     if (dkeys.alloc(sizeof(float) * (size_t)npairs, st)) return -1;
     // FP32 Euclidean distance between piecewise aggregates (segments of 4 points)
     const int R = 4, D = (max_len + R - 1) / R;
@@ -638,16 +663,19 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     if (launch_plain(k_identity_order, dim3(1024), dim3(256), 0, st, (int)nq, (int)ncand, dord.as<int>())) return -1;
   }
   mark(st, "rank");
-  // 2. cutoff seed: exact diagonal upper bound of each query's top-ranked candidate
+  // 2. cutoff seed: the least exact diagonal upper bound over each query's top-ranked
+  //    candidates (one on the Euclidean ranking, whose top candidate minimises that bound
+  //    approximately; several on the LB ranking)
+  if (launch_plain(k_fill_u64, dim3(64), dim3(256), 0, st, dcut.as<unsigned long long>(), (long long)nq,
+                   0x7ff0000000000000ULL))
+    return -1;
   if (share) {
-    if (launch_plain(pick_ub(spec->kind, spec_mode(spec)), dim3((unsigned)((nq + 3) / 4)), dim3(128), 0, st, dQ,
-                     (const long long*)dqoff, (const int*)dqlen, (int)nq, dC, (const long long*)dcoff,
+    // (the LB ranking's top candidates are not the Euclidean nearest: take the best of 16)
+    const int nseed = (int)std::min<int64_t>(ncand, use_lb ? env_int("EKB_NN_SEEDS", 16) : 1);
+    if (launch_plain(pick_ub(spec->kind, spec_mode(spec)), dim3((unsigned)((nq * nseed + 3) / 4)), dim3(128), 0, st,
+                     dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC, (const long long*)dcoff,
                      (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), win, ph.prm,
-                     dcut.as<unsigned long long>()))
-      return -1;
-  } else {
-    if (launch_plain(k_fill_u64, dim3(64), dim3(256), 0, st, dcut.as<unsigned long long>(), (long long)nq,
-                     0x7ff0000000000000ULL))
+                     dcut.as<unsigned long long>(), nseed))
       return -1;
   }
   mark(st, "seed_cutoff");
@@ -665,16 +693,19 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
                           (const int*)dord.as<int>(), 0, ka, ka, 1, 1, win, (int)max_len, ph.prm, (int)share,
-                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>(),
-                          (const float2*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count))
+                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 32,
+                          (const float*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count))
       return -1;
   }
   mark(st, "nn_phaseA");
-  if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the envelopes (side stream)
-  // phase B, one launch of two segments: the next-best 64 ranks (where the survivors
-  // concentrate) one pair per item for load balance, the rest in items of 8
-  // (64 / 8 measured best on C2 against 32..128 / 4..32)
-  const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? 4 : ka) + 64);
+  if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the LB keys and envelopes (side stream)
+  // phase B, one launch of two segments: the best ranks (where the survivors concentrate)
+  // in small items for load balance, the rest in larger ones.  Without the LB path:
+  // 4 + 64 ranks one pair per item, then items of 8 (measured best on C2 before the LB
+  // keys).  LB path: items whose pairs all fail their key cost a load and a ballot, so
+  // the tail uses full-warp items of 32.
+  const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? env_int("EKB_NN_SEG1", 64) : ka + 64));
+  const int K1_lb = env_int("EKB_NN_K1", 1), K2 = one_launch ? env_int("EKB_NN_K2", 4) : 8;
   const NNFn fnB = pick_nn(spec->kind, spec_mode(spec), engB);
   const size_t smemB = pair_smem(max_len, engB, wpb, elem_size(spec));
   // With the LB pre-test most pairs are cheap and the first segment's tail of long DPs
@@ -685,13 +716,14 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   for (int sgi = 0; sgi < (one_launch ? 1 : 2); ++sgi) {
     const int lo = one_launch ? ka : seg_lo[sgi], mid = one_launch ? kb1 : seg_mid[sgi];
     const int hi = one_launch ? (int)ncand : mid;
-    const int K1 = (one_launch || sgi == 0) ? 1 : 8;
+    const int K1 = one_launch ? K1_lb : sgi == 0 ? 1 : 8;
     if (lo >= hi) continue;
-    const long long items = (long long)nq * ((mid - lo + K1 - 1) / K1 + (hi - mid + 7) / 8);
+    const long long items = (long long)nq * ((mid - lo + K1 - 1) / K1 + (hi - mid + K2 - 1) / K2);
     if (launch_persistent(fnB, 32 * wpb, smemB, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
                           (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), lo, mid,
-                          hi, K1, 8, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
-                          dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2 + 2 * sgi, env,
+                          hi, K1, K2, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
+                          dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 64 + 32 * sgi,
+                          (const float*)(use_lb ? dskeys.as<float>() : nullptr),
                           (const float2*)denvq.as<float2>(), dovf.as<int2>(), ovf_count))
       return -1;
   }

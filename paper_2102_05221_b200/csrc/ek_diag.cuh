@@ -54,11 +54,17 @@ struct DiagResult {
 // per-lane load can observe two different values around another warp's atomicMin;
 // every decision taken on the cutoff must be the same in all 32 lanes, hence lane
 // 0's value is broadcast.  Call from converged code only.
-__device__ __forceinline__ double ld_cut(const unsigned long long* p) {
+// Split form: ld_cut_raw issues lane 0's load, bcast_cut broadcasts it; placing the
+// broadcast well after the load hides its latency.
+__device__ __forceinline__ unsigned long long ld_cut_raw(const unsigned long long* p) {
   unsigned long long v = 0;
   if ((threadIdx.x & 31) == 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double bcast_cut(unsigned long long v) {
   return __longlong_as_double((long long)__shfl_sync(0xffffffffu, v, 0));
 }
+__device__ __forceinline__ double ld_cut(const unsigned long long* p) { return bcast_cut(ld_cut_raw(p)); }
 
 __device__ __forceinline__ int hi_word(double v) { return __double2hiint(v); }
 // FP32 mode: the whole image (values are >= +0 or +inf, so the bits order as integers)
@@ -286,8 +292,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   constexpr int REP = (U >= 16) ? 1 : 16 / U;  // unrolled blocks between cutoff refreshes
   bool finished = false;
   while (!finished) {
-    R nextcut = cut;
-    if constexpr (SHARED_CUT) nextcut = to_cut<R>(ld_cut(cutp));  // consumed after this block of double steps
+    unsigned long long nextcut = 0;
+    if constexpr (SHARED_CUT) nextcut = ld_cut_raw(cutp);  // broadcast after this block of double steps
 #pragma unroll 1
     for (int b = 0; b < REP && !finished; ++b) {
       if constexpr (ROT) {  // stage series data for the whole unrolled block at once
@@ -299,7 +305,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       finished = unrolled_steps<0, U>(dstep);
     }
     if constexpr (SHARED_CUT) {
-      cut = fmin(cut, nextcut);
+      cut = fmin(cut, to_cut<R>(bcast_cut(nextcut)));
       cut_hi = hi_word(cut);
     }
   }

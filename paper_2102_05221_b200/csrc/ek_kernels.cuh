@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
 // ---- 1-NN with a shared per-query cutoff -----------------------------------------
 
 constexpr int kChunk = 128;  // candidate staging granule (4 doubles per lane)
+constexpr int kNnCounters = 8;  // k_nn work counters (64-bit each)
 
 // Lazily staged candidate; the first chunk arrives prefetched.
 template <class R>
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
                                             int rank_hi, int K1, int K2, int win, int lmax, Params prm, int share,
                                             unsigned long long* cutbits, double* __restrict__ out,
                                             int* __restrict__ tend_out, int* __restrict__ counter,
-                                            const float2* __restrict__ env, const float2* __restrict__ envq,
+                                            const float* __restrict__ skeys, const float2* __restrict__ envq,
                                             int2* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
@@ -363,14 +364,32 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
   constexpr bool TWO_SEG = (KIND == K_DTW);
   const long long items1 = (long long)((rank_mid - rank_lo + K1 - 1) / K1) * nq;
   const long long nitems = TWO_SEG ? items1 + (long long)((rank_hi - rank_mid + K2 - 1) / K2) * nq : items1;
-  // LB_Keogh pre-test (dtw/cdtw, equal lengths): env != nullptr
-  const bool use_lb = env != nullptr;
+  // LB path (dtw/cdtw, equal lengths): skeys[q * ncand + rank] = LB_Keogh(q, env(c)) of the
+  // rank's candidate, rounded down (k_lb_matrix; the ranks are ordered by it).  Pairs whose
+  // key exceeds the cutoff are never visited (their outputs are prefilled: +inf, 0 cells).
+  const bool use_lb = skeys != nullptr;
   int staged_q = -1, cb_len = -1;
+  unsigned long long* const ctr = (unsigned long long*)counter;
+  // Items are claimed from kNnCounters interleaved counters (item = local * kNnCounters
+  // + k), starting at the warp's own: one counter would serialise ~10^5..10^6 claims at
+  // L2.  (Claiming one item ahead measured slower: a claimed item waits behind the
+  // current one's DPs, which unbalances the tail.)
+  int ck = (int)((blockIdx.x * (blockDim.x >> 5) + wib) % kNnCounters), ctr_left = kNnCounters;
   for (;;) {
-    long long it = 0;
-    if (lane == 0) it = (long long)atomicAdd((unsigned long long*)counter, 1ULL);
+    long long it = -1;
+    if (lane == 0) {
+      while (ctr_left > 0) {
+        const long long cand = (long long)atomicAdd(ctr + ck, 1ULL) * kNnCounters + ck;
+        if (cand < nitems) {
+          it = cand;
+          break;
+        }
+        ck = (ck + 1) % kNnCounters;  // counter ck is exhausted: the next one
+        --ctr_left;
+      }
+    }
     it = __shfl_sync(FULL, it, 0);
-    if (it >= nitems) break;
+    if (it < 0) break;
     const bool first_seg = !TWO_SEG || it < items1;
     const long long is = first_seg ? it : it - items1;
     const int q = (int)(is % nq);
@@ -380,6 +399,17 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
     const int k_lo = (first_seg ? rank_lo : rank_mid) + r * K;
     const int k_hi = min(k_lo + K, first_seg ? rank_mid : rank_hi);
     const int cnt = k_hi - k_lo;
+    double cut = ld_cut(cutbits + q);
+    // this item's pairs to visit: all of them, or (LB path) those whose key passes the cutoff
+    unsigned todo = cnt >= 32 ? FULL : (1u << cnt) - 1u;
+    float key = 0.f;
+    double pf[PF];
+    if (use_lb) {
+      key = lane < cnt ? skeys[(long long)q * ncand + k_lo + lane] : 0.f;
+      const double thr = lb_threshold<MODE>(cut, lq);
+      todo = __ballot_sync(FULL, lane < cnt && (double)key <= thr);
+      if (!todo) continue;  // nothing to visit: the query is not even staged
+    }
     // this item's candidates and their metadata, one per lane (K <= 32)
     const int ord = lane < cnt ? order[(long long)q * ncand + k_lo + lane] : 0;
 #ifdef EKB_BOUNDS
@@ -401,23 +431,16 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
       stage_series<KIND>(QB, Q + qoff[q], lq, PAD);
       staged_q = q;
     }
-    double cut = ld_cut(cutbits + q);
-    // prefetch: LB path keeps the first envelope batch of pairs i+1 and i+2 in two
-    // register sets (envA for even i, envB for odd i); otherwise the next pair's
-    // first data chunk
-    float2 envA[LB_BATCH], envB[LB_BATCH];
-    double pf[PF];
-    if (use_lb) {
-      lb_load(env + (long long)__shfl_sync(FULL, ord, 0) * lmax, 0, __shfl_sync(FULL, olen, 0), envA);
-      if (cnt > 1) lb_load(env + (long long)__shfl_sync(FULL, ord, 1) * lmax, 0, __shfl_sync(FULL, olen, 1), envB);
-    } else {
+    if (!use_lb) {  // the first pair's first data chunk
       const double* s = C + __shfl_sync(FULL, ooff, 0);
       const int lc = __shfl_sync(FULL, olen, 0);
 #pragma unroll
       for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < lc) ? __ldg(s + u * 32 + lane) : 0.0;
     }
     __syncwarp();
-    for (int i = 0; i < cnt; ++i) {
+    while (todo) {
+      const int i = __ffs(todo) - 1;
+      todo &= todo - 1;
       const int c = __shfl_sync(FULL, ord, i);
       const int lc = __shfl_sync(FULL, olen, i);
       const double* csrc = C + __shfl_sync(FULL, ooff, i);
@@ -428,26 +451,16 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
       bool evaluate = w >= nl - nc;
       int staged = min(kChunk, lc);  // candidate elements already in CB
       if (use_lb) {
-        const int i2 = min(i + 2, cnt - 1);
-        const int c2 = __shfl_sync(FULL, ord, i2), l2 = __shfl_sync(FULL, olen, i2);
-        // first batch from the prefetched set, which is then refilled for pair i+2
-        auto first = [&](float2 (&e)[LB_BATCH]) {
-          const float t = lb_lane_terms<MODE>(QB, 0, lc, e);
-          if (i + 2 < cnt) lb_load(env + (long long)c2 * lmax, 0, l2, e);
-          return t;
-        };
-        const float t0 = (i & 1) ? first(envB) : first(envA);
-        const LBScale sc = lb_scale(lb_threshold<MODE>(cut, nl));
-        const unsigned tot0 = lb_reduce(t0, sc);
-        evaluate = evaluate && !sc.all && tot0 <= sc.T &&
-                   warp_lb_rest<MODE>(QB, env + (long long)c * lmax, lc, sc, tot0);
+        // the key against the current (tighter) cutoff, then the reverse bound
+        const double thr = lb_threshold<MODE>(cut, nl);
+        evaluate = evaluate && (double)__shfl_sync(FULL, key, i) <= thr;
         if (evaluate) {  // survivor: stage the whole candidate, then the reverse bound
           __syncwarp();
           stage_series<KIND>(CB, csrc, lc, PAD);
           cb_len = lc;
           staged = lc;
           __syncwarp();
-          evaluate = warp_lb_reverse<MODE>(CB, envq + (long long)q * lmax, lc, sc);
+          evaluate = warp_lb_reverse<MODE>(CB, envq + (long long)q * lmax, lc, lb_scale(thr));
         }
       } else {
         __syncwarp();
@@ -459,7 +472,7 @@ __global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const 
           stage_pads<KIND>(CB, lc, PAD, first);
           cb_len = lc;
         }
-        if (i + 1 < cnt) {  // prefetch the next candidate's first chunk
+        if (i + 1 < cnt) {  // prefetch the next candidate's first chunk (todo holds every pair)
           const double* s = C + __shfl_sync(FULL, ooff, i + 1);
           const int ln = __shfl_sync(FULL, olen, i + 1);
 #pragma unroll

@@ -11,12 +11,12 @@ using TriFn = void (*)(const double*, const long long*, const int*, int, int, in
                       unsigned long long*, int*);
 using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, int, int, int, int, int, int, Params, int, unsigned long long*,
-                      double*, int*, int*, const float2*, const float2*, int2*, int*);
+                      double*, int*, int*, const float*, const float2*, int2*, int*);
 using NNFixFn = void (*)(const double*, const long long*, const int*, const double*, const long long*, const int*,
                          int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*);
 using RefFn = void (*)(const double*, const PairDesc*, int, int, Params, double*, long long*);
 using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
-                      const int*, int, const int*, int, Params, unsigned long long*);
+                      const int*, int, const int*, int, Params, unsigned long long*, int);
 
 // diagonal_upper_bound (engines.py:87-103): the diagonal then the last column, the
 // cost of one admissible path, seeds a query's cutoff.  One warp per query, terms
@@ -53,21 +53,20 @@ __global__ void __launch_bounds__(128) k_ub_init(const double* __restrict__ Q, c
                                                  const int* __restrict__ qlen, int nq, const double* __restrict__ C,
                                                  const long long* __restrict__ coff, const int* __restrict__ clen,
                                                  int ncand, const int* __restrict__ order, int win, Params prm,
-                                                 unsigned long long* cutbits) {
+                                                 unsigned long long* cutbits, int nseed) {
+  // one warp per (query, seed rank); the query's cutoff (prefilled +inf) takes the least
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = blockIdx.x * 4 + wib;
-  if (q >= nq) return;
-  const int c = order ? order[(long long)q * ncand] : 0;
+  const long long wid = (long long)blockIdx.x * 4 + wib;
+  const int q = (int)(wid / nseed), rk = (int)(wid % nseed);
+  if (q >= nq || rk >= ncand) return;
+  const int c = order ? order[(long long)q * ncand + rk] : rk;
   const int lq = qlen[q], lc = clen[c];
   const bool q_rows = lq >= lc;
   const double* X = q_rows ? Q + qoff[q] : C + coff[c];
   const double* Y = q_rows ? C + coff[c] : Q + qoff[q];
   const int nl = q_rows ? lq : lc, nc = q_rows ? lc : lq;
   const int w = win < 0 ? nl : win;
-  if (w < nl - nc) {
-    if (lane == 0) cutbits[q] = 0x7ff0000000000000ULL;
-    return;
-  }
+  if (w < nl - nc) return;  // infeasible: +inf, the prefilled value
   const Params pp = pair_params(prm, nl);
   // Every term is >= 0.  Summed in any order with every addition rounded up, the total
   // is >= the exact path cost; one more relative 2^-24 (rounded up) covers the
@@ -87,7 +86,7 @@ __global__ void __launch_bounds__(128) k_ub_init(const double* __restrict__ Q, c
   } else {
     total = __dmul_ru(total, 1.0 + 0x1p-24);
   }
-  if (lane == 0) cutbits[q] = (unsigned long long)__double_as_longlong(total);
+  if (lane == 0) atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(total));
 }
 
 // Single pairs with the reference's own cells_computed (ek_refcells.cuh): one warp per

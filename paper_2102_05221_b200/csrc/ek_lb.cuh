@@ -1,4 +1,6 @@
-// ek_lb.cuh -- LB_Keogh pre-test for dtw/cdtw 1-NN.
+// ek_lb.cuh -- LB_Keogh pre-tests for dtw/cdtw 1-NN: the rounding
+// rules and the warp-cooperative reverse bound; the forward bound of every pair is
+// k_lb_matrix (ek_misc.cu), which uses the same rounding.
 //
 // Reference: lower_bounds.build_envelope / lb_keogh (pkg/src/elastik/lower_bounds.py:23-84)
 // and their use as a skip test in search.nn_search (search.py:104-112).  Here the
@@ -93,20 +95,6 @@ __device__ __forceinline__ void lb_load(const float2* __restrict__ env, int base
     const int k = base + b * 32 + lane;
     e[b] = k < L ? __ldg(env + k) : make_float2(__int_as_float(0x7f800000), __int_as_float(0xff800000));
   }
-}
-
-// Continues the test past the prefetched first batch (running scaled total `total`).
-// Returns true when the candidate must still be evaluated.
-template <int MODE, class R>
-__device__ __forceinline__ bool warp_lb_rest(const R* qs, const float2* __restrict__ env, int L,
-                                             const LBScale& sc, unsigned total) {
-  for (int base = 32 * LB_BATCH; base < L; base += 32 * LB_BATCH) {
-    float2 e[LB_BATCH];
-    lb_load(env, base, L, e);
-    total += lb_reduce(lb_lane_terms<MODE>(qs, base, L, e), sc);
-    if (total > sc.T) return false;
-  }
-  return true;
 }
 
 // The reverse bound LB_Keogh(candidate, envelope(query)) (lb_keogh2's second order,

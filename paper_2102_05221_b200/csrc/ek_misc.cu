@@ -114,11 +114,153 @@ __global__ void __launch_bounds__(256) k_rank_paa(const float* __restrict__ Qp, 
     }
 }
 
+// LB_Keogh(q, env(c)) of every (query, candidate) pair of a dense batch (all series of
+// length L), as a tiled matrix: 32 queries x 64 candidates per 128-thread block (enough
+// blocks to keep every SM busy at 256 x 4096), 4 x 4 per thread, points in chunks of 32
+// through shared memory.  Every operation rounds toward -inf (the query point widened to
+// [RD(q), RU(q)], distances to the outward-rounded float envelope rounded down, squared
+// and accumulated with fma.rm), so each value is a guaranteed lower bound of the exact
+// LB_Keogh and hence of the DP value (ek_lb.cuh).  FP32 mode (MODE & M_F32): the query
+// point is the float the DP stages.  Two candidates per packed FADD2 / FFMA2 (sm_100):
+// per (query, candidate, point) 2.5 instructions.  These keys order the 1-NN candidates
+// and drop pairs whose bound exceeds the running cutoff.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(u64 v, float& a, float& b) { asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ u64 add2_rd(u64 a, u64 b) {
+  u64 r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2_rd(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// qt[k * nq + q] = (RD(q), -RU(q)) (FP32 mode: (q, -q)): the queries point-major
+template <int MODE>
+__global__ void k_lb_qprep(const double* __restrict__ Q, const long long* __restrict__ qoff, int nq, int L,
+                           float2* __restrict__ qt) {
+  const long long n = (long long)nq * L;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / L), k = (int)(e % L);
+    const double x = Q[qoff[q] + k];
+    float lo, hi;
+    if constexpr ((MODE & M_F32) != 0) {
+      lo = hi = (float)x;
+    } else {
+      lo = __double2float_rd(x);
+      hi = __double2float_ru(x);
+    }
+    qt[(long long)k * nq + q] = make_float2(lo, -hi);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_lb_matrix(const float2* __restrict__ qt, int nq, const float2* __restrict__ envp,
+                                                   int ncand, int L, float* __restrict__ out) {
+  constexpr int KP = 32;
+  __shared__ __align__(16) float2 qs[KP][32];  // (RD(q), -RU(q))
+  __shared__ __align__(16) float nus[KP][64];  // -upper
+  __shared__ __align__(16) float los[KP][64];  // lower
+  const int q0 = blockIdx.y * 32, c0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  u64 acc[4][2] = {};
+  const float PINF = __int_as_float(0x7f800000), NINF = __int_as_float(0xff800000);
+  // fills (point-major sources, consecutive threads = consecutive candidates / queries:
+  // coalesced loads, conflict-free stores): candidates cc = t % 64 at points t / 64 + 2 i,
+  // queries qq = t % 32 at points t / 32 + 4 i; all of a chunk's loads are issued first
+  const int cc = threadIdx.x & 63, kc = threadIdx.x >> 6, qq = threadIdx.x & 31, kq = threadIdx.x >> 5;
+  const bool c_ok = c0 + cc < ncand, q_ok = q0 + qq < nq;
+  for (int k0 = 0; k0 < L; k0 += KP) {
+    float2 ev[KP / 2], qv[KP / 4];
+#pragma unroll
+    for (int i = 0; i < KP / 2; ++i) {
+      const int k = k0 + kc + 2 * i;
+      ev[i] = (c_ok && k < L) ? envp[(long long)k * ncand + c0 + cc] : make_float2(NINF, NINF);  // neutral
+    }
+#pragma unroll
+    for (int i = 0; i < KP / 4; ++i) {
+      const int k = k0 + kq + 4 * i;
+      qv[i] = (q_ok && k < L) ? qt[(long long)k * nq + q0 + qq] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < KP / 2; ++i) {
+      nus[kc + 2 * i][cc] = ev[i].x;
+      los[kc + 2 * i][cc] = ev[i].y;
+    }
+#pragma unroll
+    for (int i = 0; i < KP / 4; ++i) qs[kq + 4 * i][qq] = qv[i];
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < KP; ++k) {
+      const float4 nu = *reinterpret_cast<const float4*>(&nus[k][tx * 4]);
+      const float4 lo = *reinterpret_cast<const float4*>(&los[k][tx * 4]);
+      const float4 qa = *reinterpret_cast<const float4*>(&qs[k][ty * 4]);
+      const float4 qb = *reinterpret_cast<const float4*>(&qs[k][ty * 4 + 2]);
+      const u64 nU[2] = {pk2(nu.x, nu.y), pk2(nu.z, nu.w)}, Lo[2] = {pk2(lo.x, lo.y), pk2(lo.z, lo.w)};
+      const float ql[4] = {qa.x, qa.z, qb.x, qb.z}, nqh[4] = {qa.y, qa.w, qb.y, qb.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const u64 l2 = pk2(ql[u], ql[u]), h2 = pk2(nqh[u], nqh[u]);  // scalar operands broadcast (.F32)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          float a0, a1, b0, b1;
+          upk2(add2_rd(l2, nU[v]), a0, a1);  // RD(q) - upper
+          upk2(add2_rd(Lo[v], h2), b0, b1);  // lower - RU(q)
+          const u64 d = pk2(fmaxf(fmaxf(a0, b0), 0.f), fmaxf(fmaxf(a1, b1), 0.f));
+          acc[u][v] = (MODE & 1) == 0 ? fma2_rd(d, d, acc[u][v]) : add2_rd(acc[u][v], d);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int q = q0 + ty * 4 + u;
+    if (q >= nq) continue;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      float a, b;
+      upk2(acc[u][v], a, b);
+      const int c = c0 + tx * 4 + 2 * v;
+      if (c < ncand) out[(long long)q * ncand + c] = a;
+      if (c + 1 < ncand) out[(long long)q * ncand + c + 1] = b;
+    }
+  }
+}
+
+cudaError_t lb_matrix(int mode, const double* Q, const long long* qoff, int nq, const float2* envp, int ncand, int L,
+                      float2* qt, float* out, cudaStream_t st) {
+  const dim3 grid((unsigned)((ncand + 63) / 64), (unsigned)((nq + 31) / 32));
+  const unsigned pb = (unsigned)std::min<long long>(1024, ((long long)nq * L + 255) / 256);
+  switch (mode) {
+    case 0: k_lb_qprep<0><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<0><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
+    case 1: k_lb_qprep<1><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<1><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
+    case 2: k_lb_qprep<2><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<2><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
+    default: k_lb_qprep<3><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<3><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
+  }
+  return cudaGetLastError();
+}
+
+__global__ void k_fill_nn_out(double* __restrict__ out, int* __restrict__ tend, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    out[i] = __longlong_as_double(0x7ff0000000000000LL);
+    tend[i] = 0;
+  }
+}
+
 // Per query: stable block radix sort of (key, candidate) -> ranked candidate order
 // (ties keep index order).  THREADS x ITEMS >= ncand; padding sorts last.
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS) k_rank_radix(const float* __restrict__ keys, int ncand,
-                                                        int* __restrict__ order, int lo_bit) {
+                                                        int* __restrict__ order, int lo_bit,
+                                                        float* __restrict__ skeys) {
   using Sort = cub::BlockRadixSort<float, THREADS, ITEMS, int>;
   extern __shared__ __align__(16) unsigned char rank_sm[];
   auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(rank_sm);
@@ -137,25 +279,28 @@ __global__ void __launch_bounds__(THREADS) k_rank_radix(const float* __restrict_
 #pragma unroll
   for (int u = 0; u < ITEMS; ++u) {
     const int i = threadIdx.x * ITEMS + u;
-    if (i < ncand) order[(long long)q * ncand + i] = v[u];
+    if (i < ncand) {
+      order[(long long)q * ncand + i] = v[u];
+      if (skeys) skeys[(long long)q * ncand + i] = k[u];  // the keys in rank order
+    }
   }
 }
 // launched from this unit (a template kernel's host stub must live with its definition)
-cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st) {
+cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st, float* skeys) {
   const int lo_bit = 16;  // top 16 key bits (~1% buckets): the order is a schedule only
   if (ncand <= 128 * 8) {
     using Sort = cub::BlockRadixSort<float, 128, 8, int>;
-    k_rank_radix<128, 8><<<nq, 128, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order, lo_bit);
+    k_rank_radix<128, 8><<<nq, 128, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order, lo_bit, skeys);
   } else if (ncand <= 256 * 16) {
     using Sort = cub::BlockRadixSort<float, 256, 16, int>;
-    k_rank_radix<256, 16><<<nq, 256, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order, lo_bit);
+    k_rank_radix<256, 16><<<nq, 256, sizeof(typename Sort::TempStorage), st>>>(keys, ncand, order, lo_bit, skeys);
   } else {
     using Sort = cub::BlockRadixSort<float, 1024, 16, int>;
     const size_t sm = sizeof(typename Sort::TempStorage);
     cudaError_t e = cudaFuncSetAttribute((const void*)k_rank_radix<1024, 16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    k_rank_radix<1024, 16><<<nq, 1024, sm, st>>>(keys, ncand, order, lo_bit);
+    k_rank_radix<1024, 16><<<nq, 1024, sm, st>>>(keys, ncand, order, lo_bit, skeys);
   }
   return cudaGetLastError();
 }
@@ -334,11 +479,13 @@ __global__ void __launch_bounds__(kEnvThreads) k_envelope(const double* __restri
       const T* th = p == pmin ? hi : hi2;
       const T* tl = p == pmin ? lo : lo2;
       const int b2 = b - (1 << p) + 1;
-      const long long o = (long long)c * L + k;
+      const long long o = FMT == kEnvPointMajor ? (long long)k * nser + c : (long long)c * L + k;
       const T u = tmax(th[a], th[b2]), l = tmin(tl[a], tl[b2]);
       if constexpr (EXACT) {
         up[o] = u;
         dn[o] = l;
+      } else if constexpr (FMT == kEnvPointMajor) {
+        env[o] = make_float2(-u, l);
       } else {
         env[o] = make_float2(u, l);
       }
@@ -375,6 +522,10 @@ static cudaError_t envelope_launch(const double* C, const long long* coff, int L
 cudaError_t envelope(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
                      cudaStream_t st) {
   return envelope_launch<kEnvPlain>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
+}
+cudaError_t envelope_pm(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
+                        cudaStream_t st) {
+  return envelope_launch<kEnvPointMajor>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
 }
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
                            void* scratch, cudaStream_t st) {

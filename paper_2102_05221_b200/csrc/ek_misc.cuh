@@ -8,7 +8,7 @@ namespace ekb {
 // per series, else global scratch rows (env_scratch_bytes(L, exact); kEnvScratchBlocks
 // blocks).  envelope(): float2 (upper rounded up, lower rounded down) for the LB
 // kernels; envelope_exact(): build_envelope's double upper / lower.
-enum EnvFmt { kEnvPlain = 0, kEnvExact = 2 };
+enum EnvFmt { kEnvPlain = 0, kEnvPointMajor = 1, kEnvExact = 2 };
 constexpr int kEnvThreads = 128;
 constexpr int kEnvScratchBlocks = 592;  // 4 x 148 SMs
 constexpr size_t kEnvSmemMax = 192 * 1024;
@@ -16,6 +16,9 @@ size_t env_smem_bytes(int L, bool exact);
 size_t env_scratch_bytes(int L, bool exact);
 cudaError_t envelope(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
                      cudaStream_t st);
+// point-major float2 (-upper, lower) at env[k * nser + c]: the layout k_lb_matrix reads
+cudaError_t envelope_pm(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
+                        cudaStream_t st);
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
                            void* scratch, cudaStream_t st);
 
@@ -23,7 +26,13 @@ __global__ void k_rank_dist(const double* Q, const long long* qoff, const int* q
                             const long long* coff, const int* clen, int ncand, float* out);
 __global__ void k_rank_sort(const float* keys, int ncand, int npow2, int* order);
 // per-query stable radix sort of the rank keys (ncand <= 16384); launches k_rank_radix
-cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st);
+cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st, float* skeys = nullptr);
+// LB_Keogh(q, env(c)) for all pairs of a dense batch, rounded down (keys of the LB path)
+// (envp: envelope_pm of the candidates; qt: scratch of nq * L float2)
+cudaError_t lb_matrix(int mode, const double* Q, const long long* qoff, int nq, const float2* envp, int ncand, int L,
+                      float2* qt, float* out, cudaStream_t st);
+// out[i] = +inf, tend[i] = 0 (pairs the LB path never visits)
+__global__ void k_fill_nn_out(double* out, int* tend, long long n);
 __global__ void k_paa(const double* src, const long long* off, const int* len, int n, int R, int D, float* dst);
 __global__ void k_rank_paa(const float* Qp, int nq, const float* Cp, int ncand, int D, float* out);
 __global__ void k_identity_order(int nq, int ncand, int* order);
