@@ -198,8 +198,10 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   // (and the guard test: a path needs >= P/2 double steps to cross a P-diagonal guard
   // lane) runs half as often
   bool alive = false;
-  auto dstep = [&](auto S_) -> bool {
+  // CHK: test for the end of the matrix after the step (only the block that can reach it)
+  auto dstep = [&](auto S_, auto CHK_) -> bool {
     constexpr int S = decltype(S_)::value;
+    constexpr bool CHK = decltype(CHK_)::value;
     constexpr int rx = ROT ? S % (H + 1) : 0;
     constexpr int ry = ROT ? (H - S % H) % H : 0;
     auto XW = [&](int k) -> RowD<KIND, R>& { return xw[(k + rx) % (H + 1)]; };
@@ -244,7 +246,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     }
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
-    if (t + 1 >= Tf) return true;
+    if (CHK && t + 1 >= Tf) return true;
     const bool vote = ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1;
     if (vote) {
       if constexpr (GUARD) {
@@ -302,7 +304,14 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
           t_load = ld.next_t(dlo, dhi, H);
         }
       }
-      finished = unrolled_steps<0, U>(dstep);
+      // blocks that end before anti-diagonal Tf skip the per-step end test
+      if (t + 2 * U + 1 < Tf) {
+        auto fast = [&](auto S_) { return dstep(S_, std::false_type{}); };
+        finished = unrolled_steps<0, U>(fast);
+      } else {
+        auto last = [&](auto S_) { return dstep(S_, std::true_type{}); };
+        finished = unrolled_steps<0, U>(last);
+      }
     }
     if constexpr (SHARED_CUT) {
       cut = fmin(cut, to_cut<R>(bcast_cut(nextcut)));
