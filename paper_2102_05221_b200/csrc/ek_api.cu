@@ -73,7 +73,10 @@ struct Ctx {
   int nsm = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // independent work forked off the calling stream
+  cudaStream_t copy = nullptr;  // chunked host-to-device uploads (ek_nn)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  static constexpr int kChunks = 8;
+  cudaEvent_t ev_chunk[kChunks] = {};
 };
 Ctx g_ctx;
 std::mutex g_mu;
@@ -110,6 +113,8 @@ int ensure_ctx() {
   CK(cudaStreamCreateWithFlags(&g_ctx.side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&g_ctx.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g_ctx.ev_join, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&g_ctx.copy, cudaStreamNonBlocking));
+  for (int k = 0; k < Ctx::kChunks; ++k) CK(cudaEventCreateWithFlags(&g_ctx.ev_chunk[k], cudaEventDisableTiming));
   // keep stream-ordered allocations cached between calls (no re-mapping per call)
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, g_ctx.dev));
@@ -563,23 +568,35 @@ static int guard_engine() {
   return g;
 }
 
+// the 1-NN LB path: dtw/cdtw with a shared cutoff on equal-length series
+static bool share_lb_path(const ek_spec* spec, int32_t variant, int32_t dense, int64_t ncand) {
+  return (variant == 1 || variant == 2) && dense && (spec->kind == K_DTW || spec->kind == K_CDTW) && ncand > 4;
+}
+
 static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, const int64_t* dqoff,
                        const int32_t* dqlen, int64_t nq, const double* dC, const int64_t* dcoff, const int32_t* dclen,
                        int64_t ncand, int32_t max_len, int32_t dense, int64_t* d_idx, double* d_dist,
-                       int64_t* d_cells, int64_t* d_comp, int64_t* d_ab, cudaStream_t st) {
+                       int64_t* d_cells, int64_t* d_comp, int64_t* d_ab, cudaStream_t st, int nchunk = 0,
+                       int64_t chunk = 0) {
+  // nchunk > 0: the candidates arrive in chunks of `chunk` series, chunk k once
+  // g_ctx.ev_chunk[k] has fired (ek_nn's overlapped upload); the LB keys of a chunk are
+  // computed as soon as it is there, everything else waits for all of them
   if (check_spec(spec)) return -1;
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
   if (nq <= 0) return 0;
   if (ncand <= 0) return fail("candidate set is empty");
   mark_reset();
   mark(st, "start");
+  const bool lb_chunks = share_lb_path(spec, variant, dense, ncand);
+  if (nchunk > 0 && !lb_chunks)
+    for (int k = 0; k < nchunk; ++k) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[k], 0));
   const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
   const int wmax = win < 0 ? max_len : win;
   const int eng = choose_engine(max_len, max_len, wmax, false);
   if (eng < 0) return fail("series length %d with window %d exceeds this build's engines", max_len, wmax);
   const bool share = variant == 1 || variant == 2;  // base / pruned_only compute every candidate exactly
   // LB_Keogh pre-filter (dtw/cdtw, equal lengths): drops candidates whose bound proves +inf
-  const bool use_lb = share && dense && (spec->kind == K_DTW || spec->kind == K_CDTW) && ncand > 4;
+  const bool use_lb = lb_chunks;
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
   const long long npairs = (long long)nq * ncand;
@@ -624,12 +641,21 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_fork, 0));
     CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr2, g_ctx.side));
     CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
-    CK(envelope_pm(dC, (const long long*)dcoff, L, (int)ncand, win < 0 ? L : win, denv.as<float2>(), scr, st));
-    mark(st, "envelope");
     DBuf dqt;
     if (dkeys.alloc(sizeof(float) * (size_t)npairs, st) || dqt.alloc(sizeof(float2) * (size_t)nq * L, st)) return -1;
-    CK(lb_matrix(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, (const float2*)denv.as<float2>(), (int)ncand,
-                 L, dqt.as<float2>(), dkeys.as<float>(), st));
+    CK(lb_qprep(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, L, dqt.as<float2>(), st));
+    const int nch = nchunk > 0 ? nchunk : 1;
+    const int64_t csz = nchunk > 0 ? chunk : ncand;
+    for (int k = 0; k < nch; ++k) {
+      const int cb = (int)std::min<int64_t>(ncand, k * csz), ce = (int)std::min<int64_t>(ncand, (k + 1) * csz);
+      if (nchunk > 0) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[k], 0));
+      if (ce <= cb) continue;
+      CK(envelope_pm(dC, (const long long*)dcoff + cb, L, ce - cb, win < 0 ? L : win, denv.as<float2>() + cb, scr, st,
+                     (int)ncand));
+      CK(lb_matrix(spec_mode(spec), (const float2*)dqt.as<float2>(), (int)nq, (const float2*)denv.as<float2>(),
+                   (int)ncand, cb, ce, L, dkeys.as<float>(), st));
+      g_launches += 2;
+    }
     mark(st, "lb_keys");
     // dkeys: the keys per (query, candidate); dskeys: the same in rank order
     if (ncand <= 16384) {
@@ -785,18 +811,42 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   CK(cudaMemcpyAsync(dq.p, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dqo.p, q_off, 8 * n_queries, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dql.p, ql.data(), 4 * n_queries, cudaMemcpyHostToDevice, st));
-  if (n_cands > 0) {
-    CK(cudaMemcpyAsync(dc.p, cands, sizeof(double) * c_total, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dco.p, c_off, 8 * n_cands, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dcl.p, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
-  }
+  // on every exit the copy stream is drained before the buffers above are released
+  struct CopyDrain {
+    ~CopyDrain() { cudaStreamSynchronize(g_ctx.copy); }
+  } drain;
   int64_t* o = dout.as<int64_t>();
   int* bad = (int*)(o + 5 * n_queries);  // validation flag rides with the results
   CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  if (check_finite(dq.as<double>(), q_total, bad, st) || check_finite(dc.as<double>(), c_total, bad, st)) return -1;
+  if (check_finite(dq.as<double>(), q_total, bad, st)) return -1;
+  // Candidates: offsets and lengths first, then the values in chunks on the copy stream,
+  // each checked for finiteness there and announced by an event, so the LB keys of early
+  // chunks are computed while later ones are still in flight (dense batches: chunk k is
+  // series [k * csz, (k + 1) * csz), contiguous in the buffer).
+  int nch = 0;
+  int64_t csz = n_cands;
+  if (n_cands > 0) {
+    CK(cudaMemcpyAsync(dco.p, c_off, 8 * n_cands, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dcl.p, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(g_ctx.ev_fork, st));  // dc / bad allocated and zeroed in stream order
+    CK(cudaStreamWaitEvent(g_ctx.copy, g_ctx.ev_fork, 0));
+    bool contiguous = dense != 0;
+    for (int64_t k = 0; k < n_cands && contiguous; ++k) contiguous = c_off[k] == k * (int64_t)mx;
+    nch = (contiguous && n_cands >= 2 * Ctx::kChunks) ? std::max(1, std::min(Ctx::kChunks, env_int("EKB_NN_CHUNKS", 4))) : 1;
+    csz = (n_cands + nch - 1) / nch;
+    for (int k = 0; k < nch; ++k) {
+      const int64_t b = std::min<int64_t>(c_total, nch == 1 ? 0 : k * csz * mx);
+      const int64_t e = nch == 1 ? c_total : std::min<int64_t>(c_total, (k + 1) * csz * mx);
+      if (e > b) {
+        CK(cudaMemcpyAsync(dc.as<double>() + b, cands + b, sizeof(double) * (e - b), cudaMemcpyHostToDevice, g_ctx.copy));
+        if (check_finite(dc.as<double>() + b, e - b, bad, g_ctx.copy)) return -1;
+      }
+      CK(cudaEventRecord(g_ctx.ev_chunk[k], g_ctx.copy));
+    }
+  }
   if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
                   dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, dense, o, (double*)(o + n_queries), o + 2 * n_queries,
-                  o + 3 * n_queries, o + 4 * n_queries, st))
+                  o + 3 * n_queries, o + 4 * n_queries, st, nch, csz))
     return -1;
   // one copy back: five result arrays and the validation flag
   std::vector<int64_t> h(5 * n_queries + 1);

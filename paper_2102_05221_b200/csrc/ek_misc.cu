@@ -163,20 +163,20 @@ __global__ void k_lb_qprep(const double* __restrict__ Q, const long long* __rest
 
 template <int MODE>
 __global__ void __launch_bounds__(128) k_lb_matrix(const float2* __restrict__ qt, int nq, const float2* __restrict__ envp,
-                                                   int ncand, int L, float* __restrict__ out) {
+                                                   int ncand, int c_begin, int c_end, int L, float* __restrict__ out) {
   constexpr int KP = 32;
   __shared__ __align__(16) float2 qs[KP][32];  // (RD(q), -RU(q))
   __shared__ __align__(16) float nus[KP][64];  // -upper
   __shared__ __align__(16) float los[KP][64];  // lower
-  const int q0 = blockIdx.y * 32, c0 = blockIdx.x * 64;
+  const int q0 = blockIdx.y * 32, c0 = c_begin + blockIdx.x * 64;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   u64 acc[4][2] = {};
-  const float PINF = __int_as_float(0x7f800000), NINF = __int_as_float(0xff800000);
+  const float NINF = __int_as_float(0xff800000);
   // fills (point-major sources, consecutive threads = consecutive candidates / queries:
   // coalesced loads, conflict-free stores): candidates cc = t % 64 at points t / 64 + 2 i,
   // queries qq = t % 32 at points t / 32 + 4 i; all of a chunk's loads are issued first
   const int cc = threadIdx.x & 63, kc = threadIdx.x >> 6, qq = threadIdx.x & 31, kq = threadIdx.x >> 5;
-  const bool c_ok = c0 + cc < ncand, q_ok = q0 + qq < nq;
+  const bool c_ok = c0 + cc < c_end, q_ok = q0 + qq < nq;
   for (int k0 = 0; k0 < L; k0 += KP) {
     float2 ev[KP / 2], qv[KP / 4];
 #pragma unroll
@@ -229,21 +229,31 @@ __global__ void __launch_bounds__(128) k_lb_matrix(const float2* __restrict__ qt
       float a, b;
       upk2(acc[u][v], a, b);
       const int c = c0 + tx * 4 + 2 * v;
-      if (c < ncand) out[(long long)q * ncand + c] = a;
-      if (c + 1 < ncand) out[(long long)q * ncand + c + 1] = b;
+      if (c < c_end) out[(long long)q * ncand + c] = a;
+      if (c + 1 < c_end) out[(long long)q * ncand + c + 1] = b;
     }
   }
 }
 
-cudaError_t lb_matrix(int mode, const double* Q, const long long* qoff, int nq, const float2* envp, int ncand, int L,
-                      float2* qt, float* out, cudaStream_t st) {
-  const dim3 grid((unsigned)((ncand + 63) / 64), (unsigned)((nq + 31) / 32));
+cudaError_t lb_qprep(int mode, const double* Q, const long long* qoff, int nq, int L, float2* qt, cudaStream_t st) {
   const unsigned pb = (unsigned)std::min<long long>(1024, ((long long)nq * L + 255) / 256);
   switch (mode) {
-    case 0: k_lb_qprep<0><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<0><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
-    case 1: k_lb_qprep<1><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<1><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
-    case 2: k_lb_qprep<2><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<2><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
-    default: k_lb_qprep<3><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); k_lb_matrix<3><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, L, out); break;
+    case 0: k_lb_qprep<0><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); break;
+    case 1: k_lb_qprep<1><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); break;
+    case 2: k_lb_qprep<2><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); break;
+    default: k_lb_qprep<3><<<pb, 256, 0, st>>>(Q, qoff, nq, L, qt); break;
+  }
+  return cudaGetLastError();
+}
+cudaError_t lb_matrix(int mode, const float2* qt, int nq, const float2* envp, int ncand, int c_begin, int c_end, int L,
+                      float* out, cudaStream_t st) {
+  if (c_end <= c_begin) return cudaSuccess;
+  const dim3 grid((unsigned)((c_end - c_begin + 63) / 64), (unsigned)((nq + 31) / 32));
+  switch (mode) {
+    case 0: k_lb_matrix<0><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
+    case 1: k_lb_matrix<1><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
+    case 2: k_lb_matrix<2><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
+    default: k_lb_matrix<3><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
   }
   return cudaGetLastError();
 }
@@ -420,7 +430,7 @@ template <int FMT, bool GLOBAL>
 __global__ void __launch_bounds__(kEnvThreads) k_envelope(const double* __restrict__ C,
                                                           const long long* __restrict__ coff, int L, int nser, int w,
                                                           float2* __restrict__ env, double* __restrict__ up, double* __restrict__ dn,
-                                                          void* __restrict__ scratch) {
+                                                          void* __restrict__ scratch, int pm_stride) {
   constexpr bool EXACT = FMT == kEnvExact;
   using T = typename std::conditional<EXACT, double, float>::type;
   extern __shared__ __align__(16) unsigned char env_sm[];
@@ -479,7 +489,7 @@ __global__ void __launch_bounds__(kEnvThreads) k_envelope(const double* __restri
       const T* th = p == pmin ? hi : hi2;
       const T* tl = p == pmin ? lo : lo2;
       const int b2 = b - (1 << p) + 1;
-      const long long o = FMT == kEnvPointMajor ? (long long)k * nser + c : (long long)c * L + k;
+      const long long o = FMT == kEnvPointMajor ? (long long)k * pm_stride + c : (long long)c * L + k;
       const T u = tmax(th[a], th[b2]), l = tmin(tl[a], tl[b2]);
       if constexpr (EXACT) {
         up[o] = u;
@@ -501,21 +511,21 @@ size_t env_scratch_bytes(int L, bool exact) {
 
 template <int FMT>
 static cudaError_t envelope_launch(const double* C, const long long* coff, int L, int nser, int w, float2* env,
-                                   double* up, double* dn, void* scratch, cudaStream_t st) {
+                                   double* up, double* dn, void* scratch, cudaStream_t st, int pm_stride = 0) {
   if (nser <= 0 || L <= 0) return cudaSuccess;
   constexpr bool EXACT = FMT == kEnvExact;
   const size_t sm = env_smem_bytes(L, EXACT);
   if (env_scratch_bytes(L, EXACT)) {
     if (!scratch) return cudaErrorInvalidValue;
-    k_envelope<FMT, true><<<(unsigned)std::min(nser, kEnvScratchBlocks), kEnvThreads, 0, st>>>(C, coff, L, nser, w,
-                                                                                              env, up, dn, scratch);
+    k_envelope<FMT, true><<<(unsigned)std::min(nser, kEnvScratchBlocks), kEnvThreads, 0, st>>>(
+        C, coff, L, nser, w, env, up, dn, scratch, pm_stride);
   } else {
     if (sm > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute((const void*)k_envelope<FMT, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
     }
-    k_envelope<FMT, false><<<(unsigned)nser, kEnvThreads, sm, st>>>(C, coff, L, nser, w, env, up, dn, nullptr);
+    k_envelope<FMT, false><<<(unsigned)nser, kEnvThreads, sm, st>>>(C, coff, L, nser, w, env, up, dn, nullptr, pm_stride);
   }
   return cudaGetLastError();
 }
@@ -524,8 +534,8 @@ cudaError_t envelope(const double* C, const long long* coff, int L, int nser, in
   return envelope_launch<kEnvPlain>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
 }
 cudaError_t envelope_pm(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
-                        cudaStream_t st) {
-  return envelope_launch<kEnvPointMajor>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
+                        cudaStream_t st, int stride) {
+  return envelope_launch<kEnvPointMajor>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st, stride);
 }
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
                            void* scratch, cudaStream_t st) {

@@ -17,8 +17,9 @@ size_t env_scratch_bytes(int L, bool exact);
 cudaError_t envelope(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
                      cudaStream_t st);
 // point-major float2 (-upper, lower) at env[k * nser + c]: the layout k_lb_matrix reads
+// (stride: the row stride of env, >= nser; a chunk of candidates passes env + its first index)
 cudaError_t envelope_pm(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
-                        cudaStream_t st);
+                        cudaStream_t st, int stride);
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
                            void* scratch, cudaStream_t st);
 
@@ -28,9 +29,11 @@ __global__ void k_rank_sort(const float* keys, int ncand, int npow2, int* order)
 // per-query stable radix sort of the rank keys (ncand <= 16384); launches k_rank_radix
 cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st, float* skeys = nullptr);
 // LB_Keogh(q, env(c)) for all pairs of a dense batch, rounded down (keys of the LB path)
-// (envp: envelope_pm of the candidates; qt: scratch of nq * L float2)
-cudaError_t lb_matrix(int mode, const double* Q, const long long* qoff, int nq, const float2* envp, int ncand, int L,
-                      float2* qt, float* out, cudaStream_t st);
+// lb_qprep: the queries point-major, qt[k * nq + q] = (RD(q), -RU(q)); lb_matrix: the keys of
+// candidates [c_begin, c_end) (envp: envelope_pm of the candidates, row stride ncand)
+cudaError_t lb_qprep(int mode, const double* Q, const long long* qoff, int nq, int L, float2* qt, cudaStream_t st);
+cudaError_t lb_matrix(int mode, const float2* qt, int nq, const float2* envp, int ncand, int c_begin, int c_end, int L,
+                      float* out, cudaStream_t st);
 // out[i] = +inf, tend[i] = 0 (pairs the LB path never visits)
 __global__ void k_fill_nn_out(double* out, int* tend, long long n);
 __global__ void k_paa(const double* src, const long long* off, const int* len, int n, int R, int D, float* dst);
