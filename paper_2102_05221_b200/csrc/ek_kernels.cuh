@@ -337,8 +337,14 @@ struct LazyCand {
   }
 };
 
+#ifndef EKB_NN_DTW_MINB
+#define EKB_NN_DTW_MINB 5  // measured: 96 registers without spills, C2 phase B -1%
+#endif
+// min resident blocks for the dtw/cdtw diagonal 1-NN kernels (0: the compiler's choice)
+__host__ __device__ constexpr int nn_minb(int kind, int eng) { return (kind == K_DTW && eng == E_DIAG4) ? EKB_NN_DTW_MINB : 0; }
+
 template <int KIND, int MODE, int ENG>
-__global__ void __launch_bounds__(128) k_nn(const double* __restrict__ Q, const long long* __restrict__ qoff,
+__global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __restrict__ Q, const long long* __restrict__ qoff,
                                             const int* __restrict__ qlen, int nq, const double* __restrict__ C,
                                             const long long* __restrict__ coff, const int* __restrict__ clen,
                                             int ncand, const int* __restrict__ order, int rank_lo, int rank_mid,
