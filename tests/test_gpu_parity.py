@@ -479,3 +479,28 @@ def test_nn_lb_long_series_scratch_envelope(gpu):
     idx, dist = gpu.nn_batch(spec, "eapruned", Q, C)[:2]
     r = eko.nn(spec, "eapruned", Q, C, threads=16)
     assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"])
+
+
+@pytest.mark.parametrize("where", [0, 37, 63])
+def test_nonfinite_in_any_upload_chunk(gpu, rng, where):
+    """The candidates go up in chunks (ek_nn); a non-finite value in any chunk raises."""
+    Q = rng.normal(size=(2, 24))
+    C = rng.normal(size=(64, 24))
+    C[where, 5] = np.nan
+    spec = gpu.DistanceSpec(kind="cdtw", window=3)
+    with pytest.raises(ValueError, match="must all be finite"):
+        gpu.nn_batch(spec, "eapruned", Q, C)
+
+
+def test_nn_lb_path_beyond_rank_limit(gpu, rng):
+    """More than 16384 candidates: the LB path keeps the keys but skips the ranking
+    (identity order); answers still equal the oracle's, ties to the lowest index."""
+    L, n = 24, 16500
+    C = np.cumsum(rng.normal(size=(n, L)), axis=1)
+    Q = C[[5, 9000, 16400]] + rng.normal(0, 1e-3, size=(3, L))
+    C[12000] = C[9000]  # an exact duplicate of a near-neighbour: the lower index must win
+    spec = gpu.DistanceSpec(kind="cdtw", window=2)
+    idx, dist = gpu.nn_batch(spec, "eapruned", Q, C)[:2]
+    r = eko.nn(spec, "eapruned", Q, C, threads=16)
+    assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"])
+    assert idx[1] == 9000
