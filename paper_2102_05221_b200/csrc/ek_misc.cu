@@ -161,23 +161,34 @@ __global__ void k_lb_qprep(const double* __restrict__ Q, const long long* __rest
   }
 }
 
+// Two 128-thread groups per block split the points (group g takes chunks g, g + 2, ...,
+// syncing on its own named barrier) and combine their sums at the end (rounded down):
+// twice the warps of a one-group tile for the same work, which hides the fill latency.
 template <int MODE>
-__global__ void __launch_bounds__(128) k_lb_matrix(const float2* __restrict__ qt, int nq, const float2* __restrict__ envp,
+__global__ void __launch_bounds__(256) k_lb_matrix(const float2* __restrict__ qt, int nq, const float2* __restrict__ envp,
                                                    int ncand, int c_begin, int c_end, int L, float* __restrict__ out) {
-  constexpr int KP = 32;
-  __shared__ __align__(16) float2 qs[KP][32];  // (RD(q), -RU(q))
-  __shared__ __align__(16) float nus[KP][64];  // -upper
-  __shared__ __align__(16) float los[KP][64];  // lower
+  constexpr int KP = 16;
+  __shared__ __align__(16) float2 qs_[2][KP][32];  // (RD(q), -RU(q))
+  __shared__ __align__(16) float nus_[2][KP][64];  // -upper
+  __shared__ __align__(16) float los_[2][KP][64];  // lower
+  const int g = threadIdx.x >> 7, t = threadIdx.x & 127;
+  float2 (&qs)[KP][32] = qs_[g];
+  float (&nus)[KP][64] = nus_[g];
+  float (&los)[KP][64] = los_[g];
+  auto gsync = [&]() {
+    if (g == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+    else asm volatile("bar.sync 2, 128;" ::: "memory");
+  };
   const int q0 = blockIdx.y * 32, c0 = c_begin + blockIdx.x * 64;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int tx = t & 15, ty = t >> 4;
   u64 acc[4][2] = {};
   const float NINF = __int_as_float(0xff800000);
   // fills (point-major sources, consecutive threads = consecutive candidates / queries:
   // coalesced loads, conflict-free stores): candidates cc = t % 64 at points t / 64 + 2 i,
   // queries qq = t % 32 at points t / 32 + 4 i; all of a chunk's loads are issued first
-  const int cc = threadIdx.x & 63, kc = threadIdx.x >> 6, qq = threadIdx.x & 31, kq = threadIdx.x >> 5;
+  const int cc = t & 63, kc = t >> 6, qq = t & 31, kq = t >> 5;
   const bool c_ok = c0 + cc < c_end, q_ok = q0 + qq < nq;
-  for (int k0 = 0; k0 < L; k0 += KP) {
+  for (int k0 = g * KP; k0 < L; k0 += 2 * KP) {
     float2 ev[KP / 2], qv[KP / 4];
 #pragma unroll
     for (int i = 0; i < KP / 2; ++i) {
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(128) k_lb_matrix(const float2* __restrict__ qt
     }
 #pragma unroll
     for (int i = 0; i < KP / 4; ++i) qs[kq + 4 * i][qq] = qv[i];
-    __syncthreads();
+    gsync();
 #pragma unroll 4
     for (int k = 0; k < KP; ++k) {
       const float4 nu = *reinterpret_cast<const float4*>(&nus[k][tx * 4]);
@@ -218,19 +229,32 @@ __global__ void __launch_bounds__(128) k_lb_matrix(const float2* __restrict__ qt
         }
       }
     }
-    __syncthreads();
+    gsync();
   }
+  // group 1 hands its sums to group 0 through the (then idle) tiles: 128 threads x 8 sums
+  // = 8 KB from nus_[1] into los_[0], so both groups must be done with them
+  u64* const part = reinterpret_cast<u64*>(&nus_[1][0][0]);
+  __syncthreads();
+  if (g == 1) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) part[(u * 2 + v) * 128 + t] = acc[u][v];
+  }
+  __syncthreads();
+  if (g == 1) return;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int q = q0 + ty * 4 + u;
     if (q >= nq) continue;
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
-      float a, b;
+      float a, b, a1, b1;
       upk2(acc[u][v], a, b);
+      upk2(part[(u * 2 + v) * 128 + t], a1, b1);
       const int c = c0 + tx * 4 + 2 * v;
-      if (c < c_end) out[(long long)q * ncand + c] = a;
-      if (c + 1 < c_end) out[(long long)q * ncand + c + 1] = b;
+      if (c < c_end) out[(long long)q * ncand + c] = __fadd_rd(a, a1);
+      if (c + 1 < c_end) out[(long long)q * ncand + c + 1] = __fadd_rd(b, b1);
     }
   }
 }
@@ -250,10 +274,10 @@ cudaError_t lb_matrix(int mode, const float2* qt, int nq, const float2* envp, in
   if (c_end <= c_begin) return cudaSuccess;
   const dim3 grid((unsigned)((c_end - c_begin + 63) / 64), (unsigned)((nq + 31) / 32));
   switch (mode) {
-    case 0: k_lb_matrix<0><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
-    case 1: k_lb_matrix<1><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
-    case 2: k_lb_matrix<2><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
-    default: k_lb_matrix<3><<<grid, 128, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
+    case 0: k_lb_matrix<0><<<grid, 256, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
+    case 1: k_lb_matrix<1><<<grid, 256, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
+    case 2: k_lb_matrix<2><<<grid, 256, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
+    default: k_lb_matrix<3><<<grid, 256, 0, st>>>(qt, nq, envp, ncand, c_begin, c_end, L, out); break;
   }
   return cudaGetLastError();
 }
