@@ -8,46 +8,6 @@
 
 namespace ekb {
 
-// Approximate squared Euclidean distance in FP32 over a 32x32 (query, candidate)
-// tile; only used to order candidates so a tight cutoff is found early.
-__global__ void __launch_bounds__(256) k_rank_dist(const double* __restrict__ Q, const long long* __restrict__ qoff,
-                                                   const int* __restrict__ qlen, int nq,
-                                                   const double* __restrict__ C, const long long* __restrict__ coff,
-                                                   const int* __restrict__ clen, int ncand, float* __restrict__ out) {
-  __shared__ float qs[32][33];
-  __shared__ float cs[32][33];
-  const int q0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps: each thread 4 queries x 1 candidate
-  int lmax = 0;
-  for (int k = 0; k < 32; ++k) {
-    if (q0 + k < nq) lmax = max(lmax, qlen[q0 + k]);
-    if (c0 + k < ncand) lmax = max(lmax, clen[c0 + k]);
-  }
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int kb = 0; kb < lmax; kb += 32) {
-    for (int r = ty; r < 32; r += 8) {
-      const int q = q0 + r, c = c0 + r, k = kb + tx;
-      qs[r][tx] = (q < nq && k < qlen[q]) ? (float)Q[qoff[q] + k] : 0.f;
-      cs[r][tx] = (c < ncand && k < clen[c]) ? (float)C[coff[c] + k] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const float cv = cs[tx][k];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float d = qs[ty + 8 * u][k] - cv;
-        acc[u] += d * d;
-      }
-    }
-    __syncthreads();
-  }
-  for (int u = 0; u < 4; ++u) {
-    const int q = q0 + ty + 8 * u, c = c0 + tx;
-    if (q < nq && c < ncand) out[(long long)q * ncand + c] = acc[u];
-  }
-}
-
 // Piecewise aggregate approximation for the ranking: dst[s * D + k] = sum of series s
 // over points [kR, kR + R) (zero past its end), in FP32.  Ranking only.
 __global__ void k_paa(const double* __restrict__ src, const long long* __restrict__ off,

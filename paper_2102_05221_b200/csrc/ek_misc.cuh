@@ -23,8 +23,6 @@ cudaError_t envelope_pm(const double* C, const long long* coff, int L, int nser,
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
                            void* scratch, cudaStream_t st);
 
-__global__ void k_rank_dist(const double* Q, const long long* qoff, const int* qlen, int nq, const double* C,
-                            const long long* coff, const int* clen, int ncand, float* out);
 __global__ void k_rank_sort(const float* keys, int ncand, int npow2, int* order);
 // per-query stable radix sort of the rank keys (ncand <= 16384); launches k_rank_radix
 cudaError_t rank_radix(const float* keys, int nq, int ncand, int* order, cudaStream_t st, float* skeys = nullptr);
