@@ -128,7 +128,16 @@ __device__ __forceinline__ bool unrolled_steps(F& f) {
 // band it would put a live cell, computed exactly, in a guard lane; the cutoff only
 // decreases, so a path <= the final cutoff is live at every check.  On that event the
 // pair stops with ovf set and the caller redoes it with a full-band engine.
-template <int KIND, int MODE, int P, bool SHARED_CUT, bool GUARD = false, class XAcc, class YAcc, class Loader>
+//
+// VIRT0 (DTW family): the caller guarantees both virtual diagonals dlo - 1 and dhi + 1 sit in
+// slot 0 of their lanes (a symmetric band with w odd).  Only slot 0 then adds the +inf band
+// offset.  Every other out-of-band slot lies beyond a virtual diagonal, starts at +inf and
+// only ever sees +inf / NaN inputs (NaN from the +inf pads), so it stays +inf or NaN, which
+// is dead for the liveness test and never selected by an in-band cell: the "if a < v"
+// minimum never picks a NaN second argument, and an in-band cell's first argument is its
+// own diagonal.
+template <int KIND, int MODE, int P, bool SHARED_CUT, bool GUARD = false, bool VIRT0 = false, class XAcc, class YAcc,
+          class Loader>
 __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut64,
                                 const unsigned long long* cutp, const Params& prm, Loader& ld,
                                 unsigned guard = 0u) {
@@ -215,7 +224,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     for (int m = 0; m < H; ++m) {
       const int p = 2 * m;
       const R T = (m == 0) ? tin : val[p - 1];
-      const R v = cell<KIND, MODE>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm);
+      const R v = (VIRT0 && p != 0) ? cell<KIND, MODE, false>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm)
+                                    : cell<KIND, MODE>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm);
       if constexpr (BORDERED) {
         val[p] = (upd[p] || tb[p] == t) ? v : INF;
       } else if constexpr (COST_MASK) {
@@ -234,7 +244,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     for (int m = 0; m < H; ++m) {
       const int p = 2 * m + 1;
       const R L = (p == P - 1) ? lin : val[p + 1];
-      const R v = cell<KIND, MODE>(val[p], val[p - 1], L, XW(m + 1), YW(m), kk[p], st[p], prm);
+      const R v = VIRT0 ? cell<KIND, MODE, false>(val[p], val[p - 1], L, XW(m + 1), YW(m), kk[p], st[p], prm)
+                        : cell<KIND, MODE>(val[p], val[p - 1], L, XW(m + 1), YW(m), kk[p], st[p], prm);
       if constexpr (BORDERED) {
         val[p] = (upd[p] || tb[p] == t + 1) ? v : INF;
       } else if constexpr (COST_MASK) {

@@ -147,7 +147,18 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
       tend = -1;
     }
   } else if constexpr (engine_is_diag(ENG)) {
-    DiagResult r = diag_pair<KIND, MODE, engine_P(ENG), SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+    constexpr int P = engine_P(ENG);
+    DiagResult r;
+    if constexpr (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW) {
+      // both virtual diagonals in slot 0 of their lanes: only slot 0 needs the band offset
+      const int dlo = max(-w, 1 - nc), dhi = min(w, nl - 1), dbase = (dlo - 1) & ~1;
+      if (dlo - 1 == dbase && (dhi + 1 - dbase) % P == 0)
+        r = diag_pair<KIND, MODE, P, SHARED_CUT, false, true>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+      else
+        r = diag_pair<KIND, MODE, P, SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+    } else {
+      r = diag_pair<KIND, MODE, P, SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+    }
     cost = r.cost;
     tend = r.t_end;
   } else if constexpr (engine_is_strip(ENG)) {
