@@ -53,10 +53,15 @@ __host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e =
 __host__ __device__ constexpr int engine_pad(int e) {
   return engine_is_diag(e) ? diag_pad(engine_P(e)) : 40;  // stripe: rows stream past the ends by < 32
 }
-// per-warp shared-memory layout: [pad | X lmax | pad][pad | Y lmax | pad][tab lmax+1]
+// per-warp shared-memory layout: [pad | X lmax | pad][pad | Y lmax | pad][|i-j| table]; the
+// table is one-sided (lmax + 1 entries) for the strip engines, two-sided for the row-stripe
+// engines: 2 (lmax + kTabPad) + 1 entries around d = i - j = 0 (stage_table2), so a lane
+// addresses a row's weights from one per-row base with compile-time offsets
+constexpr int kTabPad = 48;  // > 2 S - 1 + the clamp margin S (ek_stripe.cuh), S <= 16
 __host__ __device__ constexpr int series_slot(int lmax, int pad) { return lmax + 2 * pad; }
 __host__ __device__ constexpr int warp_stride(int lmax, int e) {
-  return 2 * series_slot(lmax, engine_pad(e)) + (engine_is_diag(e) ? 0 : lmax + 1);
+  return 2 * series_slot(lmax, engine_pad(e)) +
+         (engine_is_diag(e) ? 0 : engine_is_strip(e) ? lmax + 1 : 2 * (lmax + kTabPad) + 1);
 }
 
 struct PairDesc {
@@ -106,6 +111,40 @@ __device__ __forceinline__ void stage_table(R* tab, int len, const Params& prm) 
       tab[k] = dmul((R)prm.nu, dadd(dij, dij));
     }
   }
+}
+
+// two-sided form: tab[k] = the entry for |d| = min(|k - half|, len - 1), k in [0, 2 half]
+template <int KIND, class R>
+__device__ __forceinline__ void stage_table2(R* tab, int len, int half, const Params& prm) {
+  const int lane = threadIdx.x & 31;
+  if constexpr (KIND == K_WDTW) {
+    for (int k = lane; k <= 2 * half; k += 32) {
+      const int d = min(abs(k - half), len - 1);
+      tab[k] = (d < prm.wt_len) ? (R)prm.wt[d] : (R)0.0;
+    }
+  } else if constexpr (KIND == K_TWE) {
+    for (int k = lane; k <= 2 * half; k += 32) {
+      R dij = (R)min(abs(k - half), len - 1);
+      tab[k] = dmul((R)prm.nu, dadd(dij, dij));
+    }
+  }
+}
+// the engines' |i-j| table: staged for ENG, returns what run_engine / stripe_pair take
+// (the strip engines: the one-sided table; the row-stripe engines: the entry of d = 0)
+template <int KIND, int ENG, class R>
+__device__ __forceinline__ const R* stage_engine_table(R* tab, int len, int lmax, const Params& prm) {
+  if constexpr (engine_is_strip(ENG)) {
+    stage_table<KIND>(tab, len, prm);
+    return tab;
+  } else {
+    stage_table2<KIND>(tab, len, lmax + kTabPad, prm);
+    return tab + lmax + kTabPad;
+  }
+}
+template <int KIND, int ENG, class R>
+__device__ __forceinline__ const R* engine_table(R* tab, int len, int lmax, const Params& prm) {
+  if constexpr (engine_is_diag(ENG)) return tab;  // the diagonal engines keep per-diagonal registers
+  else return stage_engine_table<KIND, ENG>(tab, len, lmax, prm);
 }
 
 // The band an engine actually runs: guarded engines narrow it to what 32 lanes of P
@@ -230,12 +269,12 @@ __global__ void __launch_bounds__(128) k_pairs(const double* __restrict__ series
     stage_series<KIND>(X, series + pd.xoff, pd.nl, PAD);
     stage_series<KIND>(Y, series + pd.yoff, pd.nc, PAD);
     const int tablen = max(pd.nl, pd.nc) + 1;
-    if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
+    const R* tabe = engine_table<KIND, ENG>(tab, tablen, lmax, pp);
     __syncwarp();
     double cost;
     int tend;
     run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{X, pd.nl}, pd.nl, SmemSeriesT<R>{Y, pd.nc}, pd.nc, pd.w, pd.cut,
-                                       nullptr, tab, tablen, pp, ld, cost, tend);
+                                       nullptr, tabe, tablen, pp, ld, cost, tend);
     const int cells = warp_cells<ENG>(pd.nl, pd.nc, pd.w, tend, KIND == K_ERP ? 0 : 1);
     if (lane == 0) {
       out_cost[pid] = cost;
@@ -296,9 +335,9 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
       stage_series<KIND>(X, series + off[s], nl, PAD);
       stage_series<KIND>(Y, series + off[t], nc, PAD);
       const int tablen = max(nl, nc) + 1;
-      if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
+      const R* tabe = engine_table<KIND, ENG>(tab, tablen, lmax, pp);
       __syncwarp();
-      run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, EKB_INF, nullptr, tab,
+      run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, EKB_INF, nullptr, tabe,
                                          tablen, pp, ld, cost, tend);
       my_cells += (unsigned long long)warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1);
     }
@@ -502,14 +541,12 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
         const Params pp = pair_params(prm, nl);
         LazyCand<R> ld{CB, csrc, lc, staged, !q_rows};
         const int tablen = max(nl, nc) + 1;
-        if constexpr (!engine_is_diag(ENG)) {
-          ld.load_to(lc);  // the stripe engine reads all columns up front
-          stage_table<KIND>(tab, tablen, pp);
-        }
+        if constexpr (!engine_is_diag(ENG)) ld.load_to(lc);  // the stripe engine reads all columns up front
+        const R* tabe = engine_table<KIND, ENG>(tab, tablen, lmax, pp);
         __syncwarp();
         const SmemSeriesT<R> X{q_rows ? QB : CB, nl};
         const SmemSeriesT<R> Y{q_rows ? CB : QB, nc};
-        run_engine<KIND, MODE, ENG, true>(X, nl, Y, nc, w, cut, cutbits + q, tab, tablen, pp, ld, cost, tend);
+        run_engine<KIND, MODE, ENG, true>(X, nl, Y, nc, w, cut, cutbits + q, tabe, tablen, pp, ld, cost, tend);
         if (share && lane == 0 && cost < EKB_INF) {
           // values are >= 0 (or +inf), so IEEE bits order as unsigned integers
           atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
@@ -565,12 +602,12 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
     stage_series<KIND>(X, q_rows ? Q + qoff[q] : C + coff[c], nl, PAD);
     stage_series<KIND>(Y, q_rows ? C + coff[c] : Q + qoff[q], nc, PAD);
     const int tablen = max(nl, nc) + 1;
-    if constexpr (!engine_is_diag(ENG)) stage_table<KIND>(tab, tablen, pp);
+    const R* tabe = engine_table<KIND, ENG>(tab, tablen, lmax, pp);
     __syncwarp();
     const double cut = ld_cut(cutbits + q);
     double cost;
     int tend;
-    run_engine<KIND, MODE, ENG, true>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, cut, cutbits + q, tab, tablen,
+    run_engine<KIND, MODE, ENG, true>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, cut, cutbits + q, tabe, tablen,
                                       pp, ld, cost, tend);
     const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) : 0;
     if (lane == 0) {

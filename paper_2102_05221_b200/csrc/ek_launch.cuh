@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(32) k_pairs_ref(const double* __restrict__ ser
     stage_series<KIND>(X, series + pd.xoff, nl, PAD);
     stage_series<KIND>(Y, series + pd.yoff, nc, PAD);
     const int tablen = max(nl, nc) + 1;
-    stage_table<KIND>(tab, tablen, pp);
+    const double* tabe = engine_table<KIND, ENG>(tab, tablen, lmax, pp);
     unsigned* bw = (unsigned*)bits;
     for (int k = lane; k < (nl + 1) * kRefWords / 2; k += 32) bw[k] = 0u;
     for (int k = lane; k <= nl; k += 32) vbl[k] = 0;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(32) k_pairs_ref(const double* __restrict__ ser
     }
     const RowBits rec{bits, vbl};
     const StripeResult r = stripe_pair<KIND, MODE, 16, BANDED, false, EA>(SmemSeries{X, nl}, nl, SmemSeries{Y, nc},
-                                                                           nc, w, cut, nullptr, tab, tablen, pp, rec);
+                                                                           nc, w, cut, nullptr, tabe, tablen, pp, rec);
     __syncwarp();
     if (lane == 0) {
       long long cells;

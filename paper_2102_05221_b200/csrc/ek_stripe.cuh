@@ -38,7 +38,8 @@ struct NoRec {
   __device__ __forceinline__ void vb(int, bool) const {}
 };
 
-// tab: per-pair |i-j| table in shared memory (WDTW: weights; TWE: nu*(d+d)); len >= max(nl,nc)+1.
+// tab: the entry d = i - j = 0 of the two-sided |i-j| table in shared memory (stage_table2;
+// WDTW: weights; TWE: nu*(d+d)), covering d in [-(nc + 2S), nl + S].
 template <int KIND, int MODE, int S, bool BANDED, bool SHARED_CUT, bool EA, class XAcc, class YAcc,
           class Rec = NoRec>
 __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut64,
@@ -112,13 +113,16 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
       a = i - w - jbase - 1;
       b = hi - jbase - 1;
     }
+    // tab points at d = i - j = 0 of a two-sided table (stage_table2): this row's base,
+    // clamped so garbage rows / lanes stay inside it (cells of the matrix never clamp)
+    const R* trow = tab + min(max(i - jbase - 1, -(nc + S)), nl + S);
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int j = jbase + 1 + s;
       const R up = row[s];
       DiagK<KIND, R> k{};  // off = 0.0: the stripe engine masks the band itself
-      if constexpr (KIND == K_WDTW) k.w = tab[min(abs(i - j), tablen - 1)];
-      if constexpr (TWE) k.tw = tab[min(abs(i - j), tablen - 1)];
+      if constexpr (KIND == K_WDTW) k.w = trow[-s];
+      if constexpr (TWE) k.tw = trow[-s];
       SlotS<KIND, R> stt;
       R upc = R(0);
       if constexpr (TWE) {
