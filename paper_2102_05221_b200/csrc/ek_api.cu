@@ -306,11 +306,14 @@ UBFn pick_ub(int kind, int mode) {
   return nullptr;
 }
 
+int env_int(const char* name, int dflt);
+
 // Engine for a (lines, cols, window) shape; -1 if unsupported.
 int choose_engine(int nl, int nc, int w, bool ea_rows, bool allow_p2 = false) {
   if (ea_rows) return nc <= 512 ? E_STR16_EA : E_STRIP16_EA;
   const int slots = diag_slots_needed(nl, nc, w);
-  if (allow_p2 && slots <= 64) return E_DIAG2;
+  // all-pairs: P=4 on half-warps (two pairs per warp), or P=2 on full warps (EKB_PAIR_P2=1)
+  if (allow_p2 && slots <= 64) return env_int("EKB_PAIR_P2", 0) ? E_DIAG2 : E_DIAG4H;
   if (slots <= 128) return E_DIAG4;
   if (slots <= 256) return E_DIAG8;
   const bool banded = w < nl - 1;

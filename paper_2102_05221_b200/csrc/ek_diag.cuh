@@ -136,12 +136,18 @@ __device__ __forceinline__ bool unrolled_steps(F& f) {
 // is dead for the liveness test and never selected by an in-band cell: the "if a < v"
 // minimum never picks a NaN second argument, and an in-band cell's first argument is its
 // own diagonal.
-template <int KIND, int MODE, int P, bool SHARED_CUT, bool GUARD = false, bool VIRT0 = false, class XAcc, class YAcc,
-          class Loader>
+//
+// W = 16: two pairs per warp, one per half (lanes 0-15 / 16-31), run in lockstep.  The
+// caller guarantees both halves have the same shape (nl, nc, w) and passes no cutoff (the
+// all-pairs engine): the loop bounds are then warp-uniform and nothing is ever abandoned,
+// so the liveness vote is compiled out; shuffles stay inside a half (width 16).
+template <int KIND, int MODE, int P, bool SHARED_CUT, bool GUARD = false, bool VIRT0 = false, int W = 32,
+          class XAcc, class YAcc, class Loader>
 __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut64,
                                 const unsigned long long* cutp, const Params& prm, Loader& ld,
                                 unsigned guard = 0u) {
   static_assert(P % 2 == 0 && P >= 2, "P must be even");
+  static_assert(W == 32 || (W == 16 && !SHARED_CUT && !GUARD), "half-warp pairs never abandon");
   using R = real_t<MODE>;
   const R INF = rinf<R>();
   R cut = to_cut<R>(cut64);
@@ -149,7 +155,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   constexpr bool BORDERED = (KIND == K_ERP);
   // the DTW family masks out-of-band diagonals through their cost (+inf offset)
   constexpr bool COST_MASK = (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (W - 1);
   const int dlo = max(-w, 1 - nc), dhi = min(w, nl - 1);
   const int dbase = (dlo - 1) & ~1;  // floor to even, includes the lower virtual diagonal
   const int d0 = dbase + lane * P;
@@ -216,7 +222,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     auto XW = [&](int k) -> RowD<KIND, R>& { return xw[(k + rx) % (H + 1)]; };
     auto YW = [&](int m) -> ColD<KIND, R>& { return yw[(m + ry) % H]; };
     // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
-    R tin = __shfl_up_sync(FULL, val[P - 1], 1);
+    R tin = __shfl_up_sync(FULL, val[P - 1], 1, W);
     if constexpr (BORDERED) {
       if (lane == 0) tin = INF;
     }
@@ -236,9 +242,9 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       alive |= hi_word(val[p]) <= cut_hi;
     }
     // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
-    R lin = __shfl_down_sync(FULL, val[0], 1);
+    R lin = __shfl_down_sync(FULL, val[0], 1, W);
     if constexpr (BORDERED) {
-      if (lane == 31) lin = INF;
+      if (lane == W - 1) lin = INF;
     }
 #pragma unroll
     for (int m = 0; m < H; ++m) {
@@ -258,7 +264,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
     if (CHK && t + 1 >= Tf) return true;
-    const bool vote = ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1;
+    const bool vote = W == 32 && (ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1);
     if (vote) {
       if constexpr (GUARD) {
         const unsigned live = __ballot_sync(FULL, alive);
@@ -344,7 +350,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
 #pragma unroll
   for (int p = 1; p < P; ++p)
     if (p == pf) r = val[p];
-  r = __shfl_sync(FULL, r, sf / P);
+  r = __shfl_sync(FULL, r, sf / P, W);
   res.cost = (r <= cut) ? (double)r : EKB_INF;
   return res;
 }

@@ -34,19 +34,21 @@ enum Engine : int {
   E_DIAG2 = 10,  // narrow bands (<= 64 slots) in the all-pairs kernel: twice the lanes of P=4
   E_STRIP16 = 11, E_STRIPB16 = 12,  // long series: 512-column strips (unbanded / banded)
   E_STRIP16_EA = 13,                // long series, ea rows (full computation + row minima)
-  E_COUNT = 14
+  E_DIAG4H = 14,  // all-pairs, bands <= 64 slots: P=4 on 16 lanes, two lockstep pairs per warp
+  E_COUNT = 15
 };
+__host__ __device__ constexpr int engine_W(int e) { return e == E_DIAG4H ? 16 : 32; }  // lanes per pair
 __host__ __device__ constexpr int engine_is_strip(int e) {
   return e == E_STRIP16 || e == E_STRIPB16 || e == E_STRIP16_EA;
 }
 constexpr int kStripDone = 0x40000000;  // strip engines' t_end for a completed pair
 
 __host__ __device__ constexpr int engine_is_diag(int e) {
-  return e <= E_DIAG16 || e == E_GDIAG8 || e == E_GDIAG16 || e == E_DIAG2;
+  return e <= E_DIAG16 || e == E_GDIAG8 || e == E_GDIAG16 || e == E_DIAG2 || e == E_DIAG4H;
 }
 __host__ __device__ constexpr int engine_guarded(int e) { return e == E_GDIAG8 || e == E_GDIAG16; }
 __host__ __device__ constexpr int engine_P(int e) {
-  return e == E_DIAG2 ? 2 : e == E_DIAG4 ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
+  return e == E_DIAG2 ? 2 : (e == E_DIAG4 || e == E_DIAG4H) ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
 }
 __host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e == E_STR8 ? 8 : 16; }
 // elements an engine may read beyond either end of a staged series
@@ -60,7 +62,7 @@ __host__ __device__ constexpr int engine_pad(int e) {
 constexpr int kTabPad = 48;  // > 2 S - 1 + the clamp margin S (ek_stripe.cuh), S <= 16
 __host__ __device__ constexpr int series_slot(int lmax, int pad) { return lmax + 2 * pad; }
 __host__ __device__ constexpr int warp_stride(int lmax, int e) {
-  return 2 * series_slot(lmax, engine_pad(e)) +
+  return (32 / engine_W(e)) * 2 * series_slot(lmax, engine_pad(e)) +
          (engine_is_diag(e) ? 0 : engine_is_strip(e) ? lmax + 1 : 2 * (lmax + kTabPad) + 1);
 }
 
@@ -76,28 +78,29 @@ struct PairDesc {
 
 // pads: index -1 = the kind's predecessor of element 0, [-pad, -2] = 0.0, [n, n+pad) = +inf
 // R = float (FP32 mode) stages the float64 inputs rounded to nearest.
-template <int KIND, class R>
+template <int KIND, class R, int W = 32>
 __device__ __forceinline__ void stage_pads(R* dst, int n, int pad, double first) {
-  const int lane = threadIdx.x & 31;
-  for (int k = lane + 1; k <= pad; k += 32) {
+  const int lane = threadIdx.x & (W - 1);
+  for (int k = lane + 1; k <= pad; k += W) {
     dst[-k] = (k == 1) ? pad_before<KIND, R>((R)first) : (R)0.0;
     dst[n + k - 1] = rinf<R>();
   }
 }
 
-template <int KIND, class R>
+// W: the lanes staging the series (16: a half-warp pair, E_DIAG4H)
+template <int KIND, class R, int W = 32>
 __device__ __forceinline__ void stage_series(R* dst, const double* __restrict__ src, int n, int pad) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (W - 1);
   int k = lane;
-  for (; k + 7 * 32 < n; k += 8 * 32) {  // eight loads in flight per lane before the stores
+  for (; k + 7 * W < n; k += 8 * W) {  // eight loads in flight per lane before the stores
     double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + k + 32 * u);
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + k + W * u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) dst[k + 32 * u] = (R)v[u];
+    for (int u = 0; u < 8; ++u) dst[k + W * u] = (R)v[u];
   }
-  for (; k < n; k += 32) dst[k] = (R)__ldg(src + k);
-  stage_pads<KIND>(dst, n, pad, __ldg(src));
+  for (; k < n; k += W) dst[k] = (R)__ldg(src + k);
+  stage_pads<KIND, R, W>(dst, n, pad, __ldg(src));
 }
 
 template <int KIND, class R>
@@ -192,11 +195,11 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
       // both virtual diagonals in slot 0 of their lanes: only slot 0 needs the band offset
       const int dlo = max(-w, 1 - nc), dhi = min(w, nl - 1), dbase = (dlo - 1) & ~1;
       if (dlo - 1 == dbase && (dhi + 1 - dbase) % P == 0)
-        r = diag_pair<KIND, MODE, P, SHARED_CUT, false, true>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+        r = diag_pair<KIND, MODE, P, SHARED_CUT, false, true, engine_W(ENG)>(X, nl, Y, nc, w, cut, cutp, prm, ld);
       else
-        r = diag_pair<KIND, MODE, P, SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+        r = diag_pair<KIND, MODE, P, SHARED_CUT, false, false, engine_W(ENG)>(X, nl, Y, nc, w, cut, cutp, prm, ld);
     } else {
-      r = diag_pair<KIND, MODE, P, SHARED_CUT>(X, nl, Y, nc, w, cut, cutp, prm, ld);
+      r = diag_pair<KIND, MODE, P, SHARED_CUT, false, false, engine_W(ENG)>(X, nl, Y, nc, w, cut, cutp, prm, ld);
     }
     cost = r.cost;
     tend = r.t_end;
@@ -315,6 +318,58 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
   const long long npairs = (long long)n * (n - 1) / 2;
   NoLoader ld;
   unsigned long long my_cells = 0;
+  if constexpr (engine_W(ENG) == 16) {
+    // two pairs per claim, one per half-warp, in lockstep when their shapes match; a pair
+    // of different shapes runs in two passes with both halves on the same pair
+    const int half = (threadIdx.x >> 4) & 1, hl = threadIdx.x & 15;
+    R* Xh = X + half * 2 * series_slot(lmax, PAD);
+    R* Yh = Xh + series_slot(lmax, PAD);
+    for (;;) {
+      long long p = 0;
+      if (lane == 0) p = (long long)atomicAdd((unsigned long long*)counter, 2ULL);
+      p = __shfl_sync(FULL, p, 0);
+      if (p >= npairs) break;
+      int pa[2], pb[2], ps[2], pt[2];
+      const int np = p + 1 < npairs ? 2 : 1;
+      for (int k = 0; k < np; ++k) {
+        tri_index(p + k, n, pa[k], pb[k]);
+        ps[k] = pa[k];  // make_recurrence orientation (ties keep a on the rows)
+        pt[k] = pb[k];
+        if (len[pb[k]] > len[pa[k]]) {
+          ps[k] = pb[k];
+          pt[k] = pa[k];
+        }
+      }
+      const bool same = np == 2 && len[ps[0]] == len[ps[1]] && len[pt[0]] == len[pt[1]];
+      for (int pass = 0; pass < (same ? 1 : np); ++pass) {
+        const int k = same ? half : pass;  // this half's pair
+        const int s = ps[k], t = pt[k];
+        const int nl = len[s], nc = len[t];
+        const int w = win < 0 ? nl : win;
+        double cost = EKB_INF;
+        int tend = 0;
+        if (w >= nl - nc) {  // the same for both halves (same shape)
+          const Params pp = pair_params(prm, nl);
+          __syncwarp();
+          stage_series<KIND, R, 16>(Xh, series + off[s], nl, PAD);
+          stage_series<KIND, R, 16>(Yh, series + off[t], nc, PAD);
+          __syncwarp();
+          run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{Xh, nl}, nl, SmemSeriesT<R>{Yh, nc}, nc, w, EKB_INF,
+                                             nullptr, (const R*)tab, 0, pp, ld, cost, tend);
+          // every lane of the warp sums one pair shape's band cells (both halves alike)
+          // (warp_cells sums one shape's band cells over the whole warp: x2 when both halves ran)
+          my_cells += (unsigned long long)warp_cells<E_DIAG4>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) *
+                      (same ? 2u : 1u);
+        }
+        if (hl == 0 && (same || half == 0)) {
+          D[(long long)pa[k] * n + pb[k]] = cost;
+          D[(long long)pb[k] * n + pa[k]] = cost;
+        }
+      }
+    }
+    if (lane == 0 && cells_total) atomicAdd(cells_total, my_cells);
+    return;
+  }
   for (;;) {
     long long p = 0;
     if (lane == 0) p = (long long)atomicAdd((unsigned long long*)counter, 1ULL);

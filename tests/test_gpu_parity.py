@@ -504,3 +504,20 @@ def test_nn_lb_path_beyond_rank_limit(gpu, rng):
     r = eko.nn(spec, "eapruned", Q, C, threads=16)
     assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"])
     assert idx[1] == 9000
+
+
+@pytest.mark.parametrize("kind,window,n", [("erp", 25, 33), ("cdtw", 12, 40), ("cdtw", 29, 17), ("erp", 3, 8)])
+def test_pairwise_half_warp_pairs(gpu, rng, kind, window, n):
+    """Bands of <= 64 diagonal slots run two pairs per warp in lockstep (E_DIAG4H): equal
+    lengths (the lockstep path), an odd number of pairs (a lone last pair), and a ragged
+    set (pairs of different shapes run one after the other); bit-exact with the oracle."""
+    spec = (gpu.DistanceSpec(kind="erp", window=window, erp_gap=0.3) if kind == "erp"
+            else gpu.DistanceSpec(kind="cdtw", window=window))
+    X = np.cumsum(rng.normal(size=(n, 90)), axis=1)
+    D, cells = gpu.pairwise(spec, X)
+    Do, cells_o = eko.pairwise(spec, X, threads=8)
+    assert np.array_equal(D, Do)
+    Xr = [np.cumsum(rng.normal(size=int(m))) for m in rng.integers(60, 91, size=n)]
+    D, _ = gpu.pairwise(spec, Xr)
+    Do, _ = eko.pairwise(spec, Xr, threads=8)
+    assert np.array_equal(D, Do)
