@@ -319,7 +319,8 @@ int choose_engine(int nl, int nc, int w, bool ea_rows, bool allow_p2 = false) {
   const bool banded = w < nl - 1;
   if (!banded) {
     if (nc <= 128) return E_STR4;
-    if (nc <= 256) return E_STR8;
+    // all-pairs: S=16 on half-warps (two pairs per warp), or S=8 on full warps (EKB_PAIR_S8=1)
+    if (nc <= 256) return (allow_p2 && !env_int("EKB_PAIR_S8", 0)) ? E_STR16H : E_STR8;
     if (nc <= 512) return E_STR16;
   }
   if (slots <= 512) return E_DIAG16;

@@ -35,9 +35,10 @@ enum Engine : int {
   E_STRIP16 = 11, E_STRIPB16 = 12,  // long series: 512-column strips (unbanded / banded)
   E_STRIP16_EA = 13,                // long series, ea rows (full computation + row minima)
   E_DIAG4H = 14,  // all-pairs, bands <= 64 slots: P=4 on 16 lanes, two lockstep pairs per warp
-  E_COUNT = 15
+  E_STR16H = 15,  // all-pairs, unbanded, <= 256 columns: S=16 on 16 lanes, two pairs per warp
+  E_COUNT = 16
 };
-__host__ __device__ constexpr int engine_W(int e) { return e == E_DIAG4H ? 16 : 32; }  // lanes per pair
+__host__ __device__ constexpr int engine_W(int e) { return (e == E_DIAG4H || e == E_STR16H) ? 16 : 32; }
 __host__ __device__ constexpr int engine_is_strip(int e) {
   return e == E_STRIP16 || e == E_STRIPB16 || e == E_STRIP16_EA;
 }
@@ -51,7 +52,8 @@ __host__ __device__ constexpr int engine_P(int e) {
   return e == E_DIAG2 ? 2 : (e == E_DIAG4 || e == E_DIAG4H) ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
 }
 __host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e == E_STR8 ? 8 : 16; }
-// elements an engine may read beyond either end of a staged series
+// elements an engine may read beyond either end of a staged series (stripe: rows stream past
+// the ends by < 2 W)
 __host__ __device__ constexpr int engine_pad(int e) {
   return engine_is_diag(e) ? diag_pad(engine_P(e)) : 40;  // stripe: rows stream past the ends by < 32
 }
@@ -61,9 +63,9 @@ __host__ __device__ constexpr int engine_pad(int e) {
 // addresses a row's weights from one per-row base with compile-time offsets
 constexpr int kTabPad = 48;  // > 2 S - 1 + the clamp margin S (ek_stripe.cuh), S <= 16
 __host__ __device__ constexpr int series_slot(int lmax, int pad) { return lmax + 2 * pad; }
-__host__ __device__ constexpr int warp_stride(int lmax, int e) {
-  return (32 / engine_W(e)) * 2 * series_slot(lmax, engine_pad(e)) +
-         (engine_is_diag(e) ? 0 : engine_is_strip(e) ? lmax + 1 : 2 * (lmax + kTabPad) + 1);
+__host__ __device__ constexpr int warp_stride(int lmax, int e) {  // (W = 16: two such blocks)
+  return (32 / engine_W(e)) * (2 * series_slot(lmax, engine_pad(e)) +
+                               (engine_is_diag(e) ? 0 : engine_is_strip(e) ? lmax + 1 : 2 * (lmax + kTabPad) + 1));
 }
 
 struct PairDesc {
@@ -117,16 +119,16 @@ __device__ __forceinline__ void stage_table(R* tab, int len, const Params& prm) 
 }
 
 // two-sided form: tab[k] = the entry for |d| = min(|k - half|, len - 1), k in [0, 2 half]
-template <int KIND, class R>
+template <int KIND, class R, int W = 32>
 __device__ __forceinline__ void stage_table2(R* tab, int len, int half, const Params& prm) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (W - 1);
   if constexpr (KIND == K_WDTW) {
-    for (int k = lane; k <= 2 * half; k += 32) {
+    for (int k = lane; k <= 2 * half; k += W) {
       const int d = min(abs(k - half), len - 1);
       tab[k] = (d < prm.wt_len) ? (R)prm.wt[d] : (R)0.0;
     }
   } else if constexpr (KIND == K_TWE) {
-    for (int k = lane; k <= 2 * half; k += 32) {
+    for (int k = lane; k <= 2 * half; k += W) {
       R dij = (R)min(abs(k - half), len - 1);
       tab[k] = dmul((R)prm.nu, dadd(dij, dij));
     }
@@ -140,7 +142,7 @@ __device__ __forceinline__ const R* stage_engine_table(R* tab, int len, int lmax
     stage_table<KIND>(tab, len, prm);
     return tab;
   } else {
-    stage_table2<KIND>(tab, len, lmax + kTabPad, prm);
+    stage_table2<KIND, R, engine_W(ENG)>(tab, len, lmax + kTabPad, prm);
     return tab + lmax + kTabPad;
   }
 }
@@ -213,7 +215,8 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
   } else {
     constexpr bool BANDED = ENG == E_STRB16 || ENG == E_STR16_EA;
     constexpr bool EA = ENG == E_STR16_EA;
-    StripeResult r = stripe_pair<KIND, MODE, engine_S(ENG), BANDED, SHARED_CUT, EA>(X, nl, Y, nc, w, cut, cutp,
+    StripeResult r = stripe_pair<KIND, MODE, engine_S(ENG), BANDED, SHARED_CUT, EA, XAcc, YAcc, NoRec, engine_W(ENG)>(
+        X, nl, Y, nc, w, cut, cutp,
                                                                                      tab, tablen, prm);
     cost = r.cost;
     tend = r.t_end;
@@ -322,8 +325,9 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
     // two pairs per claim, one per half-warp, in lockstep when their shapes match; a pair
     // of different shapes runs in two passes with both halves on the same pair
     const int half = (threadIdx.x >> 4) & 1, hl = threadIdx.x & 15;
-    R* Xh = X + half * 2 * series_slot(lmax, PAD);
+    R* Xh = X + half * (warp_stride(lmax, ENG) / 2);  // each half: [X][Y][|i-j| table]
     R* Yh = Xh + series_slot(lmax, PAD);
+    R* tabh = Yh - PAD + series_slot(lmax, PAD);
     for (;;) {
       long long p = 0;
       if (lane == 0) p = (long long)atomicAdd((unsigned long long*)counter, 2ULL);
@@ -353,12 +357,14 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
           __syncwarp();
           stage_series<KIND, R, 16>(Xh, series + off[s], nl, PAD);
           stage_series<KIND, R, 16>(Yh, series + off[t], nc, PAD);
+          const int tablen = max(nl, nc) + 1;
+          const R* tabe = engine_table<KIND, ENG>(tabh, tablen, lmax, pp);
           __syncwarp();
           run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{Xh, nl}, nl, SmemSeriesT<R>{Yh, nc}, nc, w, EKB_INF,
-                                             nullptr, (const R*)tab, 0, pp, ld, cost, tend);
-          // every lane of the warp sums one pair shape's band cells (both halves alike)
-          // (warp_cells sums one shape's band cells over the whole warp: x2 when both halves ran)
-          my_cells += (unsigned long long)warp_cells<E_DIAG4>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) *
+                                             nullptr, tabe, tablen, pp, ld, cost, tend);
+          // nothing abandons here (no cutoff): the whole band of this shape, summed over the
+          // warp (x2 when both halves ran a pair of it)
+          my_cells += (unsigned long long)warp_cells<E_DIAG4>(nl, nc, w, nl + nc, KIND == K_ERP ? 0 : 1) *
                       (same ? 2u : 1u);
         }
         if (hl == 0 && (same || half == 0)) {

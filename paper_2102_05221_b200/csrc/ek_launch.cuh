@@ -203,6 +203,10 @@ TriFn get_triangle(int mode, int eng) {
     EKB_ENG_CASES(1, k_triangle)
     EKB_ENG_CASES(2, k_triangle)
     EKB_ENG_CASES(3, k_triangle)
+    case 0 * 16 + E_STR16H: return k_triangle<KIND, 0, E_STR16H>;
+    case 1 * 16 + E_STR16H: return k_triangle<KIND, 1, E_STR16H>;
+    case 2 * 16 + E_STR16H: return k_triangle<KIND, 2, E_STR16H>;
+    case 3 * 16 + E_STR16H: return k_triangle<KIND, 3, E_STR16H>;
     case 0 * 16 + E_DIAG4H: return k_triangle<KIND, 0, E_DIAG4H>;
     case 1 * 16 + E_DIAG4H: return k_triangle<KIND, 1, E_DIAG4H>;
     case 2 * 16 + E_DIAG4H: return k_triangle<KIND, 2, E_DIAG4H>;

@@ -40,15 +40,19 @@ struct NoRec {
 
 // tab: the entry d = i - j = 0 of the two-sided |i-j| table in shared memory (stage_table2;
 // WDTW: weights; TWE: nu*(d+d)), covering d in [-(nc + 2S), nl + S].
+// W = 16: two pairs per warp (one per half-warp) in lockstep, all-pairs only (no cutoff,
+// no ea rows, no recorder): the caller guarantees equal shapes, so the step count is
+// warp-uniform and the abandon vote is compiled out; shuffles stay inside a half.
 template <int KIND, int MODE, int S, bool BANDED, bool SHARED_CUT, bool EA, class XAcc, class YAcc,
-          class Rec = NoRec>
+          class Rec = NoRec, int W = 32>
 __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc, int w, double cut64,
                                     const unsigned long long* cutp, const real_t<MODE>* tab, int tablen,
                                     const Params& prm, const Rec& rec = Rec{}) {
+  static_assert(W == 32 || (W == 16 && !SHARED_CUT && !EA && !Rec::on), "half-warp pairs never abandon");
   using R = real_t<MODE>;
   const R INF = rinf<R>();
   R cut = to_cut<R>(cut64);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (W - 1);
   constexpr bool BORDERED = (KIND == K_ERP);
   constexpr bool TWE = (KIND == K_TWE);
   const int r0 = BORDERED ? 0 : 1;  // ERP evaluates the top border row through the recurrence
@@ -159,12 +163,12 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
     }
     const int i0 = r0 + 2 * (t - lane), i1 = i0 + 1;
     // the left neighbour's last column for rows i0, i1 (computed at step t-1)
-    R lb0 = __shfl_up_sync(FULL, last0, 1);
-    R lb1 = __shfl_up_sync(FULL, last1, 1);
-    R lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1) : R(0);
-    R lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1) : R(0);
-    R rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1) : INF;
-    R rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1) : INF;
+    R lb0 = __shfl_up_sync(FULL, last0, 1, W);
+    R lb1 = __shfl_up_sync(FULL, last1, 1, W);
+    R lbpc0 = TWE ? __shfl_up_sync(FULL, lastpc0, 1, W) : R(0);
+    R lbpc1 = TWE ? __shfl_up_sync(FULL, lastpc1, 1, W) : R(0);
+    R rm0 = EA ? __shfl_up_sync(FULL, rmo0, 1, W) : INF;
+    R rm1 = EA ? __shfl_up_sync(FULL, rmo1, 1, W) : INF;
     const R x0 = cx(i0 - 1), x1 = cx(i1 - 1);
     const RowD<KIND, R> rd0 = make_row<KIND, MODE>(x0, xprev, prm);
     const RowD<KIND, R> rd1 = make_row<KIND, MODE>(x1, x0, prm);
@@ -227,7 +231,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
       }
     }
     if constexpr (!EA) {
-      if (t & 1) {
+      if (W == 32 && (t & 1)) {
         if (!__any_sync(FULL, alive || alive2)) { dead = true; break; }
       }
       alive2 = alive;
@@ -249,7 +253,7 @@ __device__ StripeResult stripe_pair(const XAcc& X, int nl, const YAcc& Y, int nc
   for (int s = 1; s < S; ++s)
     if (s == sf) r = val[s];
   if (last_is_i0) r = fin;
-  r = __shfl_sync(FULL, r, lf);
+  r = __shfl_sync(FULL, r, lf, W);
   if constexpr (EA) {
     const bool flagged = __any_sync(FULL, ea_flag);
     res.cost = flagged ? INF : r;

@@ -521,3 +521,21 @@ def test_pairwise_half_warp_pairs(gpu, rng, kind, window, n):
     D, _ = gpu.pairwise(spec, Xr)
     Do, _ = eko.pairwise(spec, Xr, threads=8)
     assert np.array_equal(D, Do)
+
+
+@pytest.mark.parametrize("kind", ["wdtw", "dtw", "twe", "msm", "erp"])
+def test_pairwise_half_warp_stripe(gpu, rng, kind):
+    """Unbanded all-pairs of 129..256 columns run two pairs per warp on the S=16 row stripe
+    (E_STR16H): dense (lockstep) and ragged (one pair at a time) sets, bit-exact."""
+    spec = {"wdtw": gpu.DistanceSpec(kind="wdtw", wdtw_g=0.05), "dtw": gpu.DistanceSpec(kind="dtw"),
+            "twe": gpu.DistanceSpec(kind="twe", twe_nu=0.01, twe_lambda=0.5),
+            "msm": gpu.DistanceSpec(kind="msm", msm_c=0.5),
+            "erp": gpu.DistanceSpec(kind="erp", window=400, erp_gap=0.1)}[kind]
+    X = np.cumsum(rng.normal(size=(9, 200)), axis=1)
+    D, _ = gpu.pairwise(spec, X)
+    Do, _ = eko.pairwise(spec, X, threads=8)
+    assert np.array_equal(D, Do)
+    Xr = [np.cumsum(rng.normal(size=int(m))) for m in rng.integers(150, 257, size=7)]
+    D, _ = gpu.pairwise(spec, Xr)
+    Do, _ = eko.pairwise(spec, Xr, threads=8)
+    assert np.array_equal(D, Do)
