@@ -1018,7 +1018,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   DBuf dseed, dukeys, dsord;
   long long ns = 0;
   if (share) {
-    const long long nsamp = std::min<long long>(nwin, 4096);
+    const long long nsamp = std::min<long long>(nwin, env_int("EKB_SUBSEQ_SAMPLES", 6144));
     const long long stride = std::max<long long>(1, nwin / nsamp);
     if (dukeys.alloc(sizeof(float) * nsamp, st) || dsord.alloc(sizeof(int) * nsamp, st)) return -1;
     if (normalize && use_lb &&  // exact statistics of the sampled windows
@@ -1030,16 +1030,20 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                      (const double*)dqn.as<double>(), (int)lq, dref, stride, (int)normalize, wst, nsamp,
                      dukeys.as<float>(), dcut.as<unsigned long long>()))
       return -1;
-    int np2 = 1;
-    while (np2 < nsamp) np2 <<= 1;
-    if (launch_plain(k_rank_sort, dim3(1), dim3(1024), (size_t)np2 * 8, st, (const float*)dukeys.as<float>(),
-                     (int)nsamp, np2, dsord.as<int>()))
-      return -1;
-    ns = std::min<long long>(16, nsamp);
+    ns = std::min<long long>(env_int("EKB_SUBSEQ_SEEDS", 32), nsamp);
     if (dseed.alloc(sizeof(long long) * ns, st)) return -1;
-    if (launch_plain(k_seed_list<0>, dim3(1), dim3(32), 0, st, (const int*)dsord.as<int>(), (int)ns, stride,
-                     dseed.as<long long>()))
+    if (env_int("EKB_SUBSEQ_SORT", 0)) {  // the global best ns samples (a one-block sort)
+      int np2 = 1;
+      while (np2 < nsamp) np2 <<= 1;
+      if (launch_plain(k_rank_sort, dim3(1), dim3(1024), (size_t)np2 * 8, st, (const float*)dukeys.as<float>(),
+                       (int)nsamp, np2, dsord.as<int>()) ||
+          launch_plain(k_seed_list<0>, dim3(1), dim3(32), 0, st, (const int*)dsord.as<int>(), (int)ns, stride,
+                       dseed.as<long long>()))
+        return -1;
+    } else if (launch_plain(k_seed_segmin<0>, dim3((unsigned)ns), dim3(256), 0, st, (const float*)dukeys.as<float>(),
+                            nsamp, (int)ns, stride, dseed.as<long long>())) {
       return -1;
+    }
   }
   mark(st, "seed_bounds");
   // LB_Keogh envelope of the query (search.py:185-187) and the test order
