@@ -439,7 +439,7 @@ def run_ours(args):
         ms = float(np.mean(step_ms))
         ms_max = dist_max(ms, dev)
         value = world * r.units / (ms_max / 1e3)
-        kern = [k for k in phases[0] if k.startswith(("nn_phase", "triangle", "subseq_phase"))]
+        kern = [k for k in phases[0] if k.startswith(("nn_phase", "nn_fix", "triangle", "subseq_phase"))]
         kern_ms = float(np.mean([sum(p[k] for k in kern) for p in phases]))
         mean_cells = float(np.mean(cells))
         ops = mean_cells * OPS_PER_CELL[r.kind]

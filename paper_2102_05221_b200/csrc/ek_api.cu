@@ -564,8 +564,8 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
 // guarded engine for wide bands (EKB_GUARD=0/8/16 overrides, for tuning)
 static int guard_engine_impl() {
   const char* e = getenv("EKB_GUARD");
-  const int g = e ? atoi(e) : 8;
-  return g == 16 ? E_GDIAG16 : g == 8 ? E_GDIAG8 : -1;
+  const int g = e ? atoi(e) : 4;  // P=4 (+-62) with the P=8 / full-band redo cascade
+  return g == 16 ? E_GDIAG16 : g == 8 ? E_GDIAG8 : g == 4 ? E_GDIAG4 : -1;
 }
 static int guard_engine() {
   static const int g = guard_engine_impl();
@@ -621,8 +621,14 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   if (share && kind_tag(spec->kind) != K_ERP && (!engine_is_diag(eng) || eng == E_DIAG16) && guard_engine() >= 0 &&
       diag_slots_needed(max_len, max_len, wmax) > 384)
     engB = guard_engine();
-  DBuf dovf;
+  // A P=4 guarded band (+-62) serves the tail ranks; the first segment's ranks (where the
+  // long, wide-warping DPs concentrate) keep the P=8 band, and its overflows skip straight to
+  // the full-band redo (list 2).  A P=4 overflow is redone with the P=8 band first.
+  const bool g4 = engB == E_GDIAG4 && diag_slots_needed(max_len, max_len, wmax) > 256;
+  DBuf dovf, dovf2;
   if (engB != eng && dovf.alloc(sizeof(int2) * (size_t)npairs, st)) return -1;
+  if (g4 && dovf2.alloc(sizeof(int2) * (size_t)npairs, st)) return -1;
+  int* const ovf2_count = dcnt.as<int>() + 10;  // ints 10, 11: second-level overflows and their counter
   // 0-1. candidate order.  LB path: envelopes, the LB_Keogh(q, env(c)) key of every pair
   //      (k_lb_matrix, rounded down) and the candidates ranked by it; the query envelopes
   //      for the survivors' reverse bound on a side stream.  Otherwise an approximate
@@ -749,25 +755,40 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     const int K1 = one_launch ? K1_lb : sgi == 0 ? 1 : 8;
     if (lo >= hi) continue;
     const long long items = (long long)nq * ((mid - lo + K1 - 1) / K1 + (hi - mid + K2 - 1) / K2);
-    if (launch_persistent(fnB, 32 * wpb, smemB, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
+    const bool seg1_wide = g4 && !one_launch && sgi == 0 && env_int("EKB_SEG1_G8", 1);
+    const NNFn fseg = seg1_wide ? pick_nn(spec->kind, spec_mode(spec), E_GDIAG8) : fnB;
+    const size_t smseg = seg1_wide ? pair_smem(max_len, E_GDIAG8, wpb, elem_size(spec)) : smemB;
+    if (launch_persistent(fseg, 32 * wpb, smseg, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
                           (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), lo, mid,
                           hi, K1, K2, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
                           dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 64 + 32 * sgi,
                           (const float*)(use_lb ? dskeys.as<float>() : nullptr),
-                          (const float2*)denvq.as<float2>(), dovf.as<int2>(), ovf_count))
+                          (const float2*)denvq.as<float2>(), seg1_wide ? dovf2.as<int2>() : dovf.as<int2>(),
+                          seg1_wide ? ovf2_count : ovf_count))
       return -1;
   }
   mark(st, "nn_phaseB");
-  if (engB != eng) {  // redo guarded-band overflows with the full-band engine
-    const NNFixFn ff = pick_nn_fix(spec->kind, spec_mode(spec), eng);
-    Params fprm = ph.prm;
-    DBuf dstrip2;
-    if (strip_scratch(ff, eng, 32 * wpb, smem, max_len, fprm, dstrip2, st)) return -1;
-    if (launch_persistent(ff, 32 * wpb, smem, st, npairs, dQ, (const long long*)dqoff, (const int*)dqlen, dC,
-                          (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int2*)dovf.as<int2>(),
-                          (const int*)ovf_count, win, (int)max_len, fprm, dcut.as<unsigned long long>(),
-                          dout.as<double>(), dtend.as<int>(), ovf_count + 1))
-      return -1;
+  if (engB != eng) {
+    // redo guarded-band overflows: a P=4 band's with the P=8 guarded band first, whose own
+    // overflows then go to the full-band engine
+    const bool two = g4;
+    for (int lvl = two ? 0 : 1; lvl < 2; ++lvl) {
+      const int fe = lvl == 0 ? E_GDIAG8 : eng;
+      const NNFixFn ff = pick_nn_fix(spec->kind, spec_mode(spec), fe);
+      const int fwpb = pick_wpb(max_len, fe, 4, 0, elem_size(spec));
+      const size_t fsmem = pair_smem(max_len, fe, fwpb, elem_size(spec));
+      Params fprm = ph.prm;
+      DBuf dstrip2;
+      if (strip_scratch(ff, fe, 32 * fwpb, fsmem, max_len, fprm, dstrip2, st)) return -1;
+      const bool from2 = lvl == 1 && two;
+      const int2* lst = from2 ? (const int2*)dovf2.as<int2>() : (const int2*)dovf.as<int2>();
+      int* cnt = from2 ? ovf2_count : ovf_count;
+      if (launch_persistent(ff, 32 * fwpb, fsmem, st, npairs, dQ, (const long long*)dqoff, (const int*)dqlen, dC,
+                            (const long long*)dcoff, (const int*)dclen, (int)ncand, lst, (const int*)cnt, win,
+                            (int)max_len, fprm, dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
+                            cnt + 1, dovf2.as<int2>(), ovf2_count))
+        return -1;
+    }
     mark(st, "nn_fix");
   }
   // 4. lexicographic (distance, index) minimum + accounting

@@ -36,7 +36,8 @@ enum Engine : int {
   E_STRIP16_EA = 13,                // long series, ea rows (full computation + row minima)
   E_DIAG4H = 14,  // all-pairs, bands <= 64 slots: P=4 on 16 lanes, two lockstep pairs per warp
   E_STR16H = 15,  // all-pairs, unbanded, <= 256 columns: S=16 on 16 lanes, two pairs per warp
-  E_COUNT = 16
+  E_GDIAG4 = 16,  // guarded diagonal P=4 (+-62)
+  E_COUNT = 17
 };
 __host__ __device__ constexpr int engine_W(int e) { return (e == E_DIAG4H || e == E_STR16H) ? 16 : 32; }
 __host__ __device__ constexpr int engine_is_strip(int e) {
@@ -45,11 +46,11 @@ __host__ __device__ constexpr int engine_is_strip(int e) {
 constexpr int kStripDone = 0x40000000;  // strip engines' t_end for a completed pair
 
 __host__ __device__ constexpr int engine_is_diag(int e) {
-  return e <= E_DIAG16 || e == E_GDIAG8 || e == E_GDIAG16 || e == E_DIAG2 || e == E_DIAG4H;
+  return e <= E_DIAG16 || e == E_GDIAG8 || e == E_GDIAG16 || e == E_DIAG2 || e == E_DIAG4H || e == E_GDIAG4;
 }
-__host__ __device__ constexpr int engine_guarded(int e) { return e == E_GDIAG8 || e == E_GDIAG16; }
+__host__ __device__ constexpr int engine_guarded(int e) { return e == E_GDIAG8 || e == E_GDIAG16 || e == E_GDIAG4; }
 __host__ __device__ constexpr int engine_P(int e) {
-  return e == E_DIAG2 ? 2 : (e == E_DIAG4 || e == E_DIAG4H) ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
+  return e == E_DIAG2 ? 2 : (e == E_DIAG4 || e == E_DIAG4H || e == E_GDIAG4) ? 4 : (e == E_DIAG8 || e == E_GDIAG8) ? 8 : 16;
 }
 __host__ __device__ constexpr int engine_S(int e) { return e == E_STR4 ? 4 : e == E_STR8 ? 8 : 16; }
 // elements an engine may read beyond either end of a staged series (stripe: rows stream past
@@ -627,8 +628,9 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
   }
 }
 
-// Redo of the pairs a guarded band gave up on (k_nn's ovf_list, *ovf_count of them)
-// with a full-band engine and the query's shared cutoff.
+// Redo of the pairs a guarded band gave up on (`list`, *count of them) with a wider engine
+// and the query's shared cutoff: a wider guarded band, whose own overflows go to ovf_list /
+// ovf_count for the next redo, or the full band.
 template <int KIND, int MODE, int ENG>
 __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, const long long* __restrict__ qoff,
                                                 const int* __restrict__ qlen, const double* __restrict__ C,
@@ -636,7 +638,8 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
                                                 int ncand, const int2* __restrict__ list,
                                                 const int* __restrict__ count, int win, int lmax, Params prm,
                                                 unsigned long long* cutbits, double* __restrict__ out,
-                                                int* __restrict__ tend_out, int* __restrict__ counter) {
+                                                int* __restrict__ tend_out, int* __restrict__ counter,
+                                                int2* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
   const int wib = threadIdx.x >> 5;
@@ -670,8 +673,12 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
     int tend;
     run_engine<KIND, MODE, ENG, true>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, cut, cutbits + q, tabe, tablen,
                                       pp, ld, cost, tend);
-    const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1) : 0;
+    const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, engine_band<ENG>(nl, nc, w), tend, KIND == K_ERP ? 0 : 1) : 0;
     if (lane == 0) {
+      if (tend < 0) {  // a guarded redo overflowed too: the next, wider engine takes it
+        ovf_list[atomicAdd(ovf_count, 1)] = make_int2(q, c);
+        cost = EKB_INF;
+      }
       if (cost < EKB_INF) atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
       out[(long long)q * ncand + c] = cost;
       tend_out[(long long)q * ncand + c] = cells;

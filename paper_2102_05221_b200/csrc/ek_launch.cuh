@@ -13,7 +13,8 @@ using NNFn = void (*)(const double*, const long long*, const int*, int, const do
                       const int*, int, const int*, int, int, int, int, int, int, int, Params, int, unsigned long long*,
                       double*, int*, int*, const float*, const float2*, int2*, int*);
 using NNFixFn = void (*)(const double*, const long long*, const int*, const double*, const long long*, const int*,
-                         int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*);
+                         int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*,
+                         int2*, int*);
 using RefFn = void (*)(const double*, const PairDesc*, int, int, Params, double*, long long*);
 using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, Params, unsigned long long*, int);
@@ -155,85 +156,89 @@ __global__ void __launch_bounds__(32) k_pairs_ref(const double* __restrict__ ser
 
 template <int KIND>
 RefFn get_pairs_ref(int mode, int eng) {
-  switch (mode * 16 + eng) {
-    case 0 * 16 + E_STR16: return k_pairs_ref<KIND, 0, E_STR16>;
-    case 1 * 16 + E_STR16: return k_pairs_ref<KIND, 1, E_STR16>;
-    case 0 * 16 + E_STRB16: return k_pairs_ref<KIND, 0, E_STRB16>;
-    case 1 * 16 + E_STRB16: return k_pairs_ref<KIND, 1, E_STRB16>;
-    case 0 * 16 + E_STR16_EA: return k_pairs_ref<KIND, 0, E_STR16_EA>;
-    case 1 * 16 + E_STR16_EA: return k_pairs_ref<KIND, 1, E_STR16_EA>;
+  switch (mode * 32 + eng) {
+    case 0 * 32 + E_STR16: return k_pairs_ref<KIND, 0, E_STR16>;
+    case 1 * 32 + E_STR16: return k_pairs_ref<KIND, 1, E_STR16>;
+    case 0 * 32 + E_STRB16: return k_pairs_ref<KIND, 0, E_STRB16>;
+    case 1 * 32 + E_STRB16: return k_pairs_ref<KIND, 1, E_STRB16>;
+    case 0 * 32 + E_STR16_EA: return k_pairs_ref<KIND, 0, E_STR16_EA>;
+    case 1 * 32 + E_STR16_EA: return k_pairs_ref<KIND, 1, E_STR16_EA>;
   }
   return nullptr;
 }
 
 #define EKB_ENG_CASES(M, FN)                                                                         \
-  case (M)*16 + E_DIAG4: return FN<KIND, M, E_DIAG4>;                                               \
-  case (M)*16 + E_DIAG8: return FN<KIND, M, E_DIAG8>;                                               \
-  case (M)*16 + E_DIAG16: return FN<KIND, M, E_DIAG16>;                                             \
-  case (M)*16 + E_STR4: return FN<KIND, M, E_STR4>;                                                 \
-  case (M)*16 + E_STR8: return FN<KIND, M, E_STR8>;                                                 \
-  case (M)*16 + E_STR16: return FN<KIND, M, E_STR16>;                                               \
-  case (M)*16 + E_STRB16: return FN<KIND, M, E_STRB16>;                                             \
-  case (M)*16 + E_STRIP16: return FN<KIND, M, E_STRIP16>;                                           \
-  case (M)*16 + E_STRIPB16: return FN<KIND, M, E_STRIPB16>;
+  case (M)*32 + E_DIAG4: return FN<KIND, M, E_DIAG4>;                                               \
+  case (M)*32 + E_DIAG8: return FN<KIND, M, E_DIAG8>;                                               \
+  case (M)*32 + E_DIAG16: return FN<KIND, M, E_DIAG16>;                                             \
+  case (M)*32 + E_STR4: return FN<KIND, M, E_STR4>;                                                 \
+  case (M)*32 + E_STR8: return FN<KIND, M, E_STR8>;                                                 \
+  case (M)*32 + E_STR16: return FN<KIND, M, E_STR16>;                                               \
+  case (M)*32 + E_STRB16: return FN<KIND, M, E_STRB16>;                                             \
+  case (M)*32 + E_STRIP16: return FN<KIND, M, E_STRIP16>;                                           \
+  case (M)*32 + E_STRIPB16: return FN<KIND, M, E_STRIPB16>;
 
 template <int KIND>
 PairsFn get_pairs(int mode, int eng) {
-  switch (mode * 16 + eng) {
+  switch (mode * 32 + eng) {
     EKB_ENG_CASES(0, k_pairs)
     EKB_ENG_CASES(1, k_pairs)
     EKB_ENG_CASES(2, k_pairs)
     EKB_ENG_CASES(3, k_pairs)
-    case 0 * 16 + E_STR16_EA: return k_pairs<KIND, 0, E_STR16_EA>;
-    case 1 * 16 + E_STR16_EA: return k_pairs<KIND, 1, E_STR16_EA>;
-    case 2 * 16 + E_STR16_EA: return k_pairs<KIND, 2, E_STR16_EA>;
-    case 3 * 16 + E_STR16_EA: return k_pairs<KIND, 3, E_STR16_EA>;
-    case 0 * 16 + E_STRIP16_EA: return k_pairs<KIND, 0, E_STRIP16_EA>;
-    case 1 * 16 + E_STRIP16_EA: return k_pairs<KIND, 1, E_STRIP16_EA>;
-    case 2 * 16 + E_STRIP16_EA: return k_pairs<KIND, 2, E_STRIP16_EA>;
-    case 3 * 16 + E_STRIP16_EA: return k_pairs<KIND, 3, E_STRIP16_EA>;
+    case 0 * 32 + E_STR16_EA: return k_pairs<KIND, 0, E_STR16_EA>;
+    case 1 * 32 + E_STR16_EA: return k_pairs<KIND, 1, E_STR16_EA>;
+    case 2 * 32 + E_STR16_EA: return k_pairs<KIND, 2, E_STR16_EA>;
+    case 3 * 32 + E_STR16_EA: return k_pairs<KIND, 3, E_STR16_EA>;
+    case 0 * 32 + E_STRIP16_EA: return k_pairs<KIND, 0, E_STRIP16_EA>;
+    case 1 * 32 + E_STRIP16_EA: return k_pairs<KIND, 1, E_STRIP16_EA>;
+    case 2 * 32 + E_STRIP16_EA: return k_pairs<KIND, 2, E_STRIP16_EA>;
+    case 3 * 32 + E_STRIP16_EA: return k_pairs<KIND, 3, E_STRIP16_EA>;
   }
   return nullptr;
 }
 
 template <int KIND>
 TriFn get_triangle(int mode, int eng) {
-  switch (mode * 16 + eng) {
+  switch (mode * 32 + eng) {
     EKB_ENG_CASES(0, k_triangle)
     EKB_ENG_CASES(1, k_triangle)
     EKB_ENG_CASES(2, k_triangle)
     EKB_ENG_CASES(3, k_triangle)
-    case 0 * 16 + E_STR16H: return k_triangle<KIND, 0, E_STR16H>;
-    case 1 * 16 + E_STR16H: return k_triangle<KIND, 1, E_STR16H>;
-    case 2 * 16 + E_STR16H: return k_triangle<KIND, 2, E_STR16H>;
-    case 3 * 16 + E_STR16H: return k_triangle<KIND, 3, E_STR16H>;
-    case 0 * 16 + E_DIAG4H: return k_triangle<KIND, 0, E_DIAG4H>;
-    case 1 * 16 + E_DIAG4H: return k_triangle<KIND, 1, E_DIAG4H>;
-    case 2 * 16 + E_DIAG4H: return k_triangle<KIND, 2, E_DIAG4H>;
-    case 3 * 16 + E_DIAG4H: return k_triangle<KIND, 3, E_DIAG4H>;
-    case 0 * 16 + E_DIAG2: return k_triangle<KIND, 0, E_DIAG2>;
-    case 1 * 16 + E_DIAG2: return k_triangle<KIND, 1, E_DIAG2>;
-    case 2 * 16 + E_DIAG2: return k_triangle<KIND, 2, E_DIAG2>;
-    case 3 * 16 + E_DIAG2: return k_triangle<KIND, 3, E_DIAG2>;
+    case 0 * 32 + E_STR16H: return k_triangle<KIND, 0, E_STR16H>;
+    case 1 * 32 + E_STR16H: return k_triangle<KIND, 1, E_STR16H>;
+    case 2 * 32 + E_STR16H: return k_triangle<KIND, 2, E_STR16H>;
+    case 3 * 32 + E_STR16H: return k_triangle<KIND, 3, E_STR16H>;
+    case 0 * 32 + E_DIAG4H: return k_triangle<KIND, 0, E_DIAG4H>;
+    case 1 * 32 + E_DIAG4H: return k_triangle<KIND, 1, E_DIAG4H>;
+    case 2 * 32 + E_DIAG4H: return k_triangle<KIND, 2, E_DIAG4H>;
+    case 3 * 32 + E_DIAG4H: return k_triangle<KIND, 3, E_DIAG4H>;
+    case 0 * 32 + E_DIAG2: return k_triangle<KIND, 0, E_DIAG2>;
+    case 1 * 32 + E_DIAG2: return k_triangle<KIND, 1, E_DIAG2>;
+    case 2 * 32 + E_DIAG2: return k_triangle<KIND, 2, E_DIAG2>;
+    case 3 * 32 + E_DIAG2: return k_triangle<KIND, 3, E_DIAG2>;
   }
   return nullptr;
 }
 
 template <int KIND>
 NNFn get_nn(int mode, int eng) {
-  switch (mode * 16 + eng) {
+  switch (mode * 32 + eng) {
     EKB_ENG_CASES(0, k_nn)
     EKB_ENG_CASES(1, k_nn)
     EKB_ENG_CASES(2, k_nn)
     EKB_ENG_CASES(3, k_nn)
-    case 0 * 16 + E_GDIAG8: return k_nn<KIND, 0, E_GDIAG8>;
-    case 1 * 16 + E_GDIAG8: return k_nn<KIND, 1, E_GDIAG8>;
-    case 2 * 16 + E_GDIAG8: return k_nn<KIND, 2, E_GDIAG8>;
-    case 3 * 16 + E_GDIAG8: return k_nn<KIND, 3, E_GDIAG8>;
-    case 0 * 16 + E_GDIAG16: return k_nn<KIND, 0, E_GDIAG16>;
-    case 1 * 16 + E_GDIAG16: return k_nn<KIND, 1, E_GDIAG16>;
-    case 2 * 16 + E_GDIAG16: return k_nn<KIND, 2, E_GDIAG16>;
-    case 3 * 16 + E_GDIAG16: return k_nn<KIND, 3, E_GDIAG16>;
+    case 0 * 32 + E_GDIAG4: return k_nn<KIND, 0, E_GDIAG4>;
+    case 1 * 32 + E_GDIAG4: return k_nn<KIND, 1, E_GDIAG4>;
+    case 2 * 32 + E_GDIAG4: return k_nn<KIND, 2, E_GDIAG4>;
+    case 3 * 32 + E_GDIAG4: return k_nn<KIND, 3, E_GDIAG4>;
+    case 0 * 32 + E_GDIAG8: return k_nn<KIND, 0, E_GDIAG8>;
+    case 1 * 32 + E_GDIAG8: return k_nn<KIND, 1, E_GDIAG8>;
+    case 2 * 32 + E_GDIAG8: return k_nn<KIND, 2, E_GDIAG8>;
+    case 3 * 32 + E_GDIAG8: return k_nn<KIND, 3, E_GDIAG8>;
+    case 0 * 32 + E_GDIAG16: return k_nn<KIND, 0, E_GDIAG16>;
+    case 1 * 32 + E_GDIAG16: return k_nn<KIND, 1, E_GDIAG16>;
+    case 2 * 32 + E_GDIAG16: return k_nn<KIND, 2, E_GDIAG16>;
+    case 3 * 32 + E_GDIAG16: return k_nn<KIND, 3, E_GDIAG16>;
   }
   return nullptr;
 }
@@ -241,35 +246,39 @@ NNFn get_nn(int mode, int eng) {
 // full-band engines that redo guarded-band overflows
 template <int KIND>
 NNFixFn get_nn_fix(int mode, int eng) {
-  switch (mode * 16 + eng) {
-    case 0 * 16 + E_STR4: return k_nn_fix<KIND, 0, E_STR4>;
-    case 1 * 16 + E_STR4: return k_nn_fix<KIND, 1, E_STR4>;
-    case 0 * 16 + E_STR8: return k_nn_fix<KIND, 0, E_STR8>;
-    case 1 * 16 + E_STR8: return k_nn_fix<KIND, 1, E_STR8>;
-    case 0 * 16 + E_STR16: return k_nn_fix<KIND, 0, E_STR16>;
-    case 1 * 16 + E_STR16: return k_nn_fix<KIND, 1, E_STR16>;
-    case 0 * 16 + E_DIAG16: return k_nn_fix<KIND, 0, E_DIAG16>;
-    case 1 * 16 + E_DIAG16: return k_nn_fix<KIND, 1, E_DIAG16>;
-    case 0 * 16 + E_STRB16: return k_nn_fix<KIND, 0, E_STRB16>;
-    case 1 * 16 + E_STRB16: return k_nn_fix<KIND, 1, E_STRB16>;
-    case 0 * 16 + E_STRIP16: return k_nn_fix<KIND, 0, E_STRIP16>;
-    case 1 * 16 + E_STRIP16: return k_nn_fix<KIND, 1, E_STRIP16>;
-    case 0 * 16 + E_STRIPB16: return k_nn_fix<KIND, 0, E_STRIPB16>;
-    case 1 * 16 + E_STRIPB16: return k_nn_fix<KIND, 1, E_STRIPB16>;
-    case 2 * 16 + E_STR4: return k_nn_fix<KIND, 2, E_STR4>;
-    case 3 * 16 + E_STR4: return k_nn_fix<KIND, 3, E_STR4>;
-    case 2 * 16 + E_STR8: return k_nn_fix<KIND, 2, E_STR8>;
-    case 3 * 16 + E_STR8: return k_nn_fix<KIND, 3, E_STR8>;
-    case 2 * 16 + E_STR16: return k_nn_fix<KIND, 2, E_STR16>;
-    case 3 * 16 + E_STR16: return k_nn_fix<KIND, 3, E_STR16>;
-    case 2 * 16 + E_DIAG16: return k_nn_fix<KIND, 2, E_DIAG16>;
-    case 3 * 16 + E_DIAG16: return k_nn_fix<KIND, 3, E_DIAG16>;
-    case 2 * 16 + E_STRB16: return k_nn_fix<KIND, 2, E_STRB16>;
-    case 3 * 16 + E_STRB16: return k_nn_fix<KIND, 3, E_STRB16>;
-    case 2 * 16 + E_STRIP16: return k_nn_fix<KIND, 2, E_STRIP16>;
-    case 3 * 16 + E_STRIP16: return k_nn_fix<KIND, 3, E_STRIP16>;
-    case 2 * 16 + E_STRIPB16: return k_nn_fix<KIND, 2, E_STRIPB16>;
-    case 3 * 16 + E_STRIPB16: return k_nn_fix<KIND, 3, E_STRIPB16>;
+  switch (mode * 32 + eng) {
+    case 0 * 32 + E_GDIAG8: return k_nn_fix<KIND, 0, E_GDIAG8>;
+    case 1 * 32 + E_GDIAG8: return k_nn_fix<KIND, 1, E_GDIAG8>;
+    case 2 * 32 + E_GDIAG8: return k_nn_fix<KIND, 2, E_GDIAG8>;
+    case 3 * 32 + E_GDIAG8: return k_nn_fix<KIND, 3, E_GDIAG8>;
+    case 0 * 32 + E_STR4: return k_nn_fix<KIND, 0, E_STR4>;
+    case 1 * 32 + E_STR4: return k_nn_fix<KIND, 1, E_STR4>;
+    case 0 * 32 + E_STR8: return k_nn_fix<KIND, 0, E_STR8>;
+    case 1 * 32 + E_STR8: return k_nn_fix<KIND, 1, E_STR8>;
+    case 0 * 32 + E_STR16: return k_nn_fix<KIND, 0, E_STR16>;
+    case 1 * 32 + E_STR16: return k_nn_fix<KIND, 1, E_STR16>;
+    case 0 * 32 + E_DIAG16: return k_nn_fix<KIND, 0, E_DIAG16>;
+    case 1 * 32 + E_DIAG16: return k_nn_fix<KIND, 1, E_DIAG16>;
+    case 0 * 32 + E_STRB16: return k_nn_fix<KIND, 0, E_STRB16>;
+    case 1 * 32 + E_STRB16: return k_nn_fix<KIND, 1, E_STRB16>;
+    case 0 * 32 + E_STRIP16: return k_nn_fix<KIND, 0, E_STRIP16>;
+    case 1 * 32 + E_STRIP16: return k_nn_fix<KIND, 1, E_STRIP16>;
+    case 0 * 32 + E_STRIPB16: return k_nn_fix<KIND, 0, E_STRIPB16>;
+    case 1 * 32 + E_STRIPB16: return k_nn_fix<KIND, 1, E_STRIPB16>;
+    case 2 * 32 + E_STR4: return k_nn_fix<KIND, 2, E_STR4>;
+    case 3 * 32 + E_STR4: return k_nn_fix<KIND, 3, E_STR4>;
+    case 2 * 32 + E_STR8: return k_nn_fix<KIND, 2, E_STR8>;
+    case 3 * 32 + E_STR8: return k_nn_fix<KIND, 3, E_STR8>;
+    case 2 * 32 + E_STR16: return k_nn_fix<KIND, 2, E_STR16>;
+    case 3 * 32 + E_STR16: return k_nn_fix<KIND, 3, E_STR16>;
+    case 2 * 32 + E_DIAG16: return k_nn_fix<KIND, 2, E_DIAG16>;
+    case 3 * 32 + E_DIAG16: return k_nn_fix<KIND, 3, E_DIAG16>;
+    case 2 * 32 + E_STRB16: return k_nn_fix<KIND, 2, E_STRB16>;
+    case 3 * 32 + E_STRB16: return k_nn_fix<KIND, 3, E_STRB16>;
+    case 2 * 32 + E_STRIP16: return k_nn_fix<KIND, 2, E_STRIP16>;
+    case 3 * 32 + E_STRIP16: return k_nn_fix<KIND, 3, E_STRIP16>;
+    case 2 * 32 + E_STRIPB16: return k_nn_fix<KIND, 2, E_STRIPB16>;
+    case 3 * 32 + E_STRIPB16: return k_nn_fix<KIND, 3, E_STRIPB16>;
   }
   return nullptr;
 }
