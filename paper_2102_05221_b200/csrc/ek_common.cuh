@@ -208,4 +208,18 @@ EKB_DI R pad_before(R first) {
   return KIND == K_MSM ? first : (R)0.0;
 }
 
+// LB pre-tests (ek_lb.cuh) and the diagonal-distance liveness bound (ek_diag.cuh): a bound
+// above lb_threshold(cut) proves the DP value exceeds cut.
+// bound > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header).
+// FP32 mode: the bound is exact for the float-rounded series the DP sees (rounding is
+// monotone, so the outward float envelope still encloses them), and the float DP value
+// of any path is >= its exact cost * (1 - u)^(2n+3), u = 2^-24 (each term passes
+// through <= 2n+3 roundings); hence the wider margin (1 + (2n+8) 2^-24), rounded up.
+template <int MODE>
+__device__ __forceinline__ double lb_threshold(double cut, int n) {
+  if constexpr ((MODE & M_F32) != 0) return __dmul_ru(cut, 1.0 + (double)(2 * n + 8) * 0x1p-24);
+  return cut * (1.0 + 2.3283064365386963e-10);
+}
+__device__ __forceinline__ double lb_threshold(double cut) { return lb_threshold<0>(cut, 0); }
+
 }  // namespace ekb

@@ -39,6 +39,9 @@ namespace ekb {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef EKB_DBOUND
+#define EKB_DBOUND 1  // MSM / TWE diagonal-distance bound in the liveness test
+#endif
 #ifndef EKB_ROT_MAX_H
 #define EKB_ROT_MAX_H 2  // register windows rotate at compile time up to H = P/2 = 2 (U = 6 unrolled steps)
 #endif
@@ -200,6 +203,27 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
 
   const int Tf = nl + nc;
   int cut_hi = hi_word(cut);
+  // MSM / TWE: a cell on diagonal d still needs |d - (nl - nc)| diagonal-changing moves to
+  // reach the last cell, and each costs at least cmin (MSM: the split/merge cost c; TWE:
+  // nu + lambda, a deletion's least cost).  Its path's final value is then at least
+  // val + |d - dfin| cmin (less the rounding of the remaining additions, which the pre-test
+  // margin of lb_threshold covers), so the cell is alive only while val <= cut' - k cmin:
+  // one threshold per slot (its diagonal is fixed), refreshed with the cutoff.
+  constexpr bool DBOUND = (KIND == K_MSM || KIND == K_TWE) && EKB_DBOUND;
+  int thr_hi[DBOUND ? P : 1];
+  double cmin = 0.0;
+  if constexpr (DBOUND) cmin = KIND == K_MSM ? prm.msm_c : __dadd_rd(prm.nu, prm.lam);
+  auto set_thr = [&](double c64) {
+    if constexpr (DBOUND) {
+      const double cm = lb_threshold<MODE>(c64, Tf);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int k = abs(d0 + p - (nl - nc));
+        thr_hi[p] = hi_word(to_cut<R>(__dsub_ru(cm, __dmul_rd((double)k, cmin))));
+      }
+    }
+  };
+  set_thr(cut64);
   bool dead = false;
   bool ovf = false;
 
@@ -239,7 +263,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       } else {
         val[p] = upd[p] ? v : INF;
       }
-      alive |= hi_word(val[p]) <= cut_hi;
+      alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
     }
     // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
     R lin = __shfl_down_sync(FULL, val[0], 1, W);
@@ -259,7 +283,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       } else {
         val[p] = upd[p] ? v : INF;
       }
-      alive |= hi_word(val[p]) <= cut_hi;
+      alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
     }
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
@@ -331,8 +355,13 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       }
     }
     if constexpr (SHARED_CUT) {
-      cut = fmin(cut, to_cut<R>(bcast_cut(nextcut)));
+      const double c64 = bcast_cut(nextcut);
+      cut = fmin(cut, to_cut<R>(c64));
       cut_hi = hi_word(cut);
+      if constexpr (DBOUND) {
+        cut64 = fmin(cut64, c64);
+        set_thr(cut64);
+      }
     }
   }
 

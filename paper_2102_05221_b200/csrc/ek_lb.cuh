@@ -113,16 +113,6 @@ __device__ __forceinline__ bool warp_lb_reverse(const R* cs, const float2* __res
   return true;
 }
 
-// bound > cutoff * (1 + 2^-32) proves the DP value exceeds the cutoff (see header).
-// FP32 mode: the bound is exact for the float-rounded series the DP sees (rounding is
-// monotone, so the outward float envelope still encloses them), and the float DP value
-// of any path is >= its exact cost * (1 - u)^(2n+3), u = 2^-24 (each term passes
-// through <= 2n+3 roundings); hence the wider margin (1 + (2n+8) 2^-24), rounded up.
-template <int MODE>
-__device__ __forceinline__ double lb_threshold(double cut, int n) {
-  if constexpr ((MODE & M_F32) != 0) return __dmul_ru(cut, 1.0 + (double)(2 * n + 8) * 0x1p-24);
-  return cut * (1.0 + 2.3283064365386963e-10);
-}
-__device__ __forceinline__ double lb_threshold(double cut) { return lb_threshold<0>(cut, 0); }
+// lb_threshold (the pre-tests' cutoff margin) lives in ek_common.cuh
 
 }  // namespace ekb
