@@ -69,6 +69,23 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
                       const int64_t* t_len, const double* cutoffs, const int64_t* windows, double* out_cost,
                       int64_t* out_cells);
 
+/* _speedups.run (pkg/src/elastik/_speedups.pyx:274-317) for many pairs: the native seam
+ * engines._dispatch calls (engines.py:29-50), with its exact semantics:
+ *   engine 0 base (_base: the full matrix; window and cutoff are ignored, cells = nl*nc),
+ *          1 ea (_ea, :129-162), 2 eapruned (_eapruned, :165-271);
+ *   lines / cols are taken as given (no re-orientation: make_recurrence already oriented
+ *   them, and orient="st" may put the shorter series on the rows);
+ *   windows[p] is run's `window` (required for engines 1 and 2, may be NULL for base);
+ *   cutoffs[p] is run's `cutoff` (NULL = +inf).
+ * (cost, cells) equal run's return value: the reference's own cells_computed for pairs of
+ * up to 512 columns x 2048 rows (beyond that, the band cells the GPU evaluated).
+ * WDTW: run's `weights` argument is the table for m = max(nl, nc); pass it as
+ * spec->wdtw_tables with wdtw_table_off[m] = 0.  ERP: run's border arrays are the
+ * sequential prefixes of kernels._erp_border, which the engines rebuild bit-identically. */
+int ek_run_batch(const ek_spec* spec, int32_t engine, int64_t n_pairs, const double* series, int64_t series_len,
+                 const int64_t* l_off, const int64_t* l_len, const int64_t* c_off, const int64_t* c_len,
+                 const int64_t* windows, const double* cutoffs, double* out_cost, int64_t* out_cells);
+
 /* 1-NN of every query against the candidates (nn_search per query, lb="none").
  * nn_idx = -1 when every candidate is +inf.  computed/abandoned/cells per query. */
 int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,

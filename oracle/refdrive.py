@@ -25,6 +25,7 @@ import importlib.util
 import math
 import multiprocessing as mp
 import os
+from collections import deque
 
 import numpy as np
 
@@ -187,10 +188,25 @@ def distance(spec, variant, s, t, cutoff=math.inf):
     return _run(spec, p, "eapruned", window, diagonal_upper_bound(spec, p))
 
 
-def nn_search(spec, variant, query, candidates):
-    """search.nn_search (lb="none") -> (d_nn, best, cells, computed, abandoned)."""
-    d_nn, best, cells, comp, ab = math.inf, -1, 0, 0, 0
+def nn_search(spec, variant, query, candidates, lb="none", envelopes=None):
+    """search.nn_search (search.py:81-125) -> (d_nn, best, cells, computed, abandoned, lb_skips).
+
+    ``lb`` = "none" / "keogh" / "keogh2" with the reference's own LB tests (restated below);
+    ``envelopes``: the candidates' envelopes (search._candidate_envelopes, built once per
+    classify_1nn call)."""
+    d_nn, best, cells, comp, ab, skips = math.inf, -1, 0, 0, 0, 0
+    env_q = None
+    if lb == "keogh2":
+        env_q = build_envelope(query, spec.window if spec.window is not None else len(query))
     for idx, cand in enumerate(candidates):
+        if envelopes is not None and len(cand) == len(query):
+            if lb == "keogh":
+                bound = lb_keogh(query, envelopes[idx], spec.cost_mode)
+            else:
+                bound = lb_keogh2(query, cand, envelopes[idx], env_q, d_nn, spec.cost_mode)
+            if bound >= d_nn:
+                skips += 1
+                continue
         cost, cc = distance(spec, variant, query, cand, cutoff=d_nn)
         cells += cc
         if math.isinf(cost):
@@ -199,7 +215,70 @@ def nn_search(spec, variant, query, candidates):
         comp += 1
         if cost < d_nn:
             d_nn, best = cost, idx
-    return d_nn, best, cells, comp, ab
+    return d_nn, best, cells, comp, ab, skips
+
+
+# ---- lower_bounds.py restated (pkg/src/elastik/lower_bounds.py:23-98): the reference's
+# pure-Python envelope (monotone deques) and LB_Keogh / LB_Keogh2 tests
+
+def build_envelope(s, window):
+    """lower_bounds.build_envelope (:23-57) -> (upper, lower) lists."""
+    values = np.asarray(s, dtype=np.float64).tolist()
+    n = len(values)
+    upper, lower = [0.0] * n, [0.0] * n
+    maxq, minq = deque(), deque()
+    right = 0
+    for i in range(n):
+        hi = min(n - 1, i + window)
+        while right <= hi:
+            v = values[right]
+            while maxq and values[maxq[-1]] <= v:
+                maxq.pop()
+            maxq.append(right)
+            while minq and values[minq[-1]] >= v:
+                minq.pop()
+            minq.append(right)
+            right += 1
+        lo = i - window
+        while maxq[0] < lo:
+            maxq.popleft()
+        while minq[0] < lo:
+            minq.popleft()
+        upper[i] = values[maxq[0]]
+        lower[i] = values[minq[0]]
+    return upper, lower
+
+
+def lb_keogh(q, env, cost_mode="squared"):
+    """lower_bounds.lb_keogh (:60-85): left-to-right sum of the distances to the envelope."""
+    upper, lower = env
+    squared = cost_mode == "squared"
+    total = 0.0
+    for qi, u, lo in zip(np.asarray(q, dtype=np.float64).tolist(), upper, lower):
+        if qi > u:
+            d = qi - u
+        elif qi < lo:
+            d = lo - qi
+        else:
+            continue
+        total += d * d if squared else d
+    return total
+
+
+def lb_keogh2(q, c, env_c, env_q, cutoff=math.inf, cost_mode="squared"):
+    """lower_bounds.lb_keogh2 (:88-98): both orders, the second skipped past the cutoff."""
+    first = lb_keogh(q, env_c, cost_mode)
+    if first > cutoff:
+        return first
+    second = lb_keogh(c, env_q, cost_mode)
+    return second if second > first else first
+
+
+def candidate_envelopes(spec, candidates, lb):
+    """search._candidate_envelopes (search.py:69-78)."""
+    if lb == "none" or spec.kind not in ("dtw", "cdtw"):
+        return None
+    return [build_envelope(c, spec.window if spec.window is not None else len(c)) for c in candidates]
 
 
 def znormalize(s):
@@ -211,19 +290,27 @@ def znormalize(s):
     return (s - mean) / std
 
 
-def subsequence_search(spec, variant, query, reference, normalize, lo=0, hi=None):
-    """search.subsequence_search (lb="none") over offsets [lo, hi) -> (offset, dist, cells)."""
+def subsequence_search(spec, variant, query, reference, normalize, lo=0, hi=None, lb="none"):
+    """search.subsequence_search (search.py:163-215) over offsets [lo, hi) -> (offset, dist, cells)."""
     query = np.ascontiguousarray(query, dtype=np.float64)
     reference = np.ascontiguousarray(reference, dtype=np.float64)
     lq = len(query)
     if normalize:
         query = znormalize(query)
+    w = spec.window if spec.window is not None else lq
+    env_q = build_envelope(query, w) if lb != "none" else None
     hi = len(reference) - lq + 1 if hi is None else hi
     best_d, best_off, cells = math.inf, -1, 0
     for off in range(lo, hi):
         win = reference[off:off + lq]
         if normalize:
             win = znormalize(win)
+        if env_q is not None:
+            bound = lb_keogh(win, env_q, spec.cost_mode)
+            if lb == "keogh2" and bound < best_d:
+                bound = lb_keogh2(query, win, build_envelope(win, w), env_q, best_d, spec.cost_mode)
+            if bound >= best_d:
+                continue
         cost, cc = distance(spec, variant, query, win, cutoff=best_d)
         cells += cc
         if math.isinf(cost):
@@ -234,32 +321,18 @@ def subsequence_search(spec, variant, query, reference, normalize, lo=0, hi=None
 
 
 # ---- process-pool sharding (processes, not threads) ----
+#
+# The pools are created once per workload, before the timed region (fork copies the
+# workload into every worker), and warmed with one task, so a timed step measures the
+# steady-state scan, not process start-up.
 
 _G = {}
 
 
 def _nn_worker(qidx):
     g = _G
-    d, b, cells, _, _ = nn_search(g["spec"], g["variant"], g["Q"][qidx], g["C"])
+    d, b, cells, _, _, _ = nn_search(g["spec"], g["variant"], g["Q"][qidx], g["C"], g["lb"], g["env"])
     return qidx, d, b, cells
-
-
-def nn_pool(spec, variant, Q, Cands, procs=None):
-    """nn_search for every query, queries sharded across a fork process pool."""
-    procs = procs or len(os.sched_getaffinity(0))
-    _G.update(spec=spec, variant=variant, Q=Q, C=list(Cands))
-    nq = len(Q)
-    idx = np.empty(nq, dtype=np.int64)
-    dist = np.empty(nq, dtype=np.float64)
-    cells = np.empty(nq, dtype=np.int64)
-    if procs <= 1 or nq == 1:
-        for q in range(nq):
-            _, dist[q], idx[q], cells[q] = _nn_worker(q)
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            for q, d, b, cc in pool.imap_unordered(_nn_worker, range(nq)):
-                dist[q], idx[q], cells[q] = d, b, cc
-    return idx, dist, cells
 
 
 def _pw_worker(i):
@@ -273,44 +346,109 @@ def _pw_worker(i):
     return i, row, cells
 
 
-def pairwise_pool(spec, X, variant="pruned_only", rows=None, procs=None):
-    """Upper-triangle rows ``rows`` of the all-pairs matrix, rows sharded across processes."""
-    procs = procs or len(os.sched_getaffinity(0))
-    _G.update(spec=spec, variant=variant, X=[np.ascontiguousarray(x, dtype=np.float64) for x in X])
-    rows = list(range(len(X))) if rows is None else list(rows)
-    out, total = {}, 0
-    if procs <= 1:
-        for i in rows:
-            _, out[i], cc = _pw_worker(i)
-            total += cc
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            for i, row, cc in pool.imap_unordered(_pw_worker, rows):
-                out[i] = row
-                total += cc
-    return out, total
-
-
 def _ss_worker(span):
     g = _G
     lo, hi = span
-    return subsequence_search(g["spec"], g["variant"], g["q"], g["ref"], g["normalize"], lo, hi)
+    return subsequence_search(g["spec"], g["variant"], g["q"], g["ref"], g["normalize"], lo, hi, g["lb"])
 
 
-def subsequence_pool(spec, variant, query, reference, normalize, lo=0, hi=None, chunk=4096, procs=None):
+class _Pool:
+    def __init__(self, procs, **workload):
+        self.procs = procs or len(os.sched_getaffinity(0))
+        _G.clear()
+        _G.update(workload)
+        self.pool = mp.get_context("fork").Pool(self.procs) if self.procs > 1 else None
+
+    def map(self, fn, items):
+        if self.pool is None:
+            return [fn(x) for x in items]
+        return list(self.pool.imap_unordered(fn, items))
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+            self.pool = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class NNPool(_Pool):
+    """nn_search per query, queries sharded across a persistent fork pool.
+
+    ``env`` (lb != "none"): the candidates' envelopes, built by the caller the way
+    classify_1nn does (once per call, serially, search.py:140)."""
+
+    def __init__(self, spec, variant, Q, Cands, lb="none", env=None, procs=None):
+        super().__init__(procs, spec=spec, variant=variant, Q=Q, C=list(Cands), lb=lb, env=env)
+        self.nq = len(Q)
+
+    def warm(self):
+        self.map(_nn_worker, [0] * (self.procs or 1))
+
+    def run(self, queries):
+        queries = list(queries)
+        idx = np.empty(len(queries), dtype=np.int64)
+        dist = np.empty(len(queries), dtype=np.float64)
+        cells = np.empty(len(queries), dtype=np.int64)
+        pos = {q: k for k, q in enumerate(queries)}
+        for q, d, b, cc in self.map(_nn_worker, queries):
+            dist[pos[q]], idx[pos[q]], cells[pos[q]] = d, b, cc
+        return idx, dist, cells
+
+
+class PairwisePool(_Pool):
+    def __init__(self, spec, X, variant="pruned_only", procs=None):
+        super().__init__(procs, spec=spec, variant=variant, X=[np.ascontiguousarray(x, dtype=np.float64) for x in X])
+        self.n = len(X)
+
+    def warm(self):
+        self.map(_pw_worker, [self.n - 2] * (self.procs or 1))
+
+    def run(self, rows):
+        out, total = {}, 0
+        for i, row, cc in self.map(_pw_worker, list(rows)):
+            out[i] = row
+            total += cc
+        return out, total
+
+
+class SubseqPool(_Pool):
+    def __init__(self, spec, variant, query, reference, normalize, lb="none", procs=None):
+        super().__init__(procs, spec=spec, variant=variant, q=query, ref=reference, normalize=normalize, lb=lb)
+
+    def warm(self):
+        self.map(_ss_worker, [(0, 2)] * (self.procs or 1))
+
+    def run(self, lo, hi, chunk=4096):
+        spans = [(a, min(a + chunk, hi)) for a in range(lo, hi, chunk)]
+        best_off, best_d, cells = -1, math.inf, 0
+        for o, d, cc in self.map(_ss_worker, spans):
+            cells += cc
+            if o >= 0 and (d < best_d or (d == best_d and o < best_off)):
+                best_off, best_d = o, d
+        return best_off, best_d, cells
+
+
+def nn_pool(spec, variant, Q, Cands, procs=None, lb="none"):
+    """nn_search for every query (one-shot pool)."""
+    env = candidate_envelopes(spec, Cands, lb)
+    with NNPool(spec, variant, Q, Cands, lb, env, procs) as p:
+        return p.run(range(len(Q)))
+
+
+def pairwise_pool(spec, X, variant="pruned_only", rows=None, procs=None):
+    """Upper-triangle rows ``rows`` of the all-pairs matrix (one-shot pool)."""
+    with PairwisePool(spec, X, variant, procs) as p:
+        return p.run(range(len(X)) if rows is None else rows)
+
+
+def subsequence_pool(spec, variant, query, reference, normalize, lo=0, hi=None, chunk=4096, procs=None, lb="none"):
     """Offsets [lo, hi) in chunks across processes; merged by lexicographic (dist, offset)."""
-    procs = procs or len(os.sched_getaffinity(0))
     hi = len(reference) - len(query) + 1 if hi is None else hi
-    _G.update(spec=spec, variant=variant, q=query, ref=reference, normalize=normalize)
-    spans = [(a, min(a + chunk, hi)) for a in range(lo, hi, chunk)]
-    if procs <= 1:
-        res = [_ss_worker(s) for s in spans]
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            res = pool.map(_ss_worker, spans)
-    best_off, best_d, cells = -1, math.inf, 0
-    for o, d, cc in res:
-        cells += cc
-        if o >= 0 and (d < best_d or (d == best_d and o < best_off)):
-            best_off, best_d = o, d
-    return best_off, best_d, cells
+    with SubseqPool(spec, variant, query, reference, normalize, lb, procs) as p:
+        return p.run(lo, hi, chunk)

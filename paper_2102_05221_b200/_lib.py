@@ -59,6 +59,8 @@ EXPORTS = {
     "ek_fp32_peak_ops": ([], C.c_double),
     "ek_distance_batch": ([C.POINTER(EkSpec), C.c_int32, C.c_int64, _dp, C.c_int64, _i64p, _i64p, _i64p, _i64p,
                            _dp, _i64p, _dp, _i64p], C.c_int),
+    "ek_run_batch": ([C.POINTER(EkSpec), C.c_int32, C.c_int64, _dp, C.c_int64, _i64p, _i64p, _i64p, _i64p,
+                      _i64p, _dp, _dp, _i64p], C.c_int),
     "ek_nn": ([C.POINTER(EkSpec), C.c_int32, _dp, C.c_int64, _i64p, _i64p, C.c_int64, _dp, C.c_int64, _i64p, _i64p,
                C.c_int64, _i64p, _dp, _i64p, _i64p, _i64p], C.c_int),
     "ek_nn_dev": ([C.POINTER(EkSpec), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,

@@ -446,13 +446,19 @@ int ek_init(int device) {
   return ensure_ctx();
 }
 
-int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, const double* series,
-                      int64_t series_len, const int64_t* s_off, const int64_t* s_len, const int64_t* t_off,
-                      const int64_t* t_len, const double* cutoffs, const int64_t* windows, double* out_cost,
-                      int64_t* out_cells) {
+}  // extern "C"
+
+// ek_distance_batch (engines.distance semantics: the pair is oriented here, variant codes
+// 0-3) and ek_run_batch (_speedups.run semantics: lines / cols as given, engine codes
+// 0-2, base ignores window and cutoff) share this body.
+static int distance_batch_impl(const ek_spec* spec, int32_t variant, int64_t n_pairs, const double* series,
+                               int64_t series_len, const int64_t* s_off, const int64_t* s_len,
+                               const int64_t* t_off, const int64_t* t_len, const double* cutoffs,
+                               const int64_t* windows, double* out_cost, int64_t* out_cells, bool run_sem) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (ensure_ctx() || check_spec(spec)) return -1;
-  if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
+  if (run_sem ? (variant < 0 || variant > 2) : (variant < 0 || variant > 3))
+    return fail(run_sem ? "unknown engine code %d" : "unknown variant code %d", variant);
   if (n_pairs <= 0) return 0;
   cudaStream_t st = g_ctx.stream;
   // host-side orientation / window / variant semantics (engines.py:121-147, kernels.py:168-171)
@@ -460,19 +466,28 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
   std::vector<std::vector<long long>> gidx(E_COUNT), ridx(E_COUNT);
   std::vector<int> glmax(E_COUNT, 0), rlmax(E_COUNT, 0);
   for (int64_t p = 0; p < n_pairs; ++p) {
-    const bool swap = t_len[p] > s_len[p];
+    const bool longer_t = t_len[p] > s_len[p];
+    // _speedups.run keeps the caller's orientation (make_recurrence(orient="st") can put the
+    // shorter series on the rows); base and eapruned are symmetric in it (the transposed DP
+    // takes the same values: every move cost and border is symmetric), only ea's row minima
+    // and all cell counts are not, so those pairs stay unswapped on the row-stripe engine
+    const bool keep = run_sem && longer_t && variant != 0;
+    const bool swap = longer_t && !keep;
     PairDesc pd{};
     pd.xoff = swap ? t_off[p] : s_off[p];
     pd.yoff = swap ? s_off[p] : t_off[p];
     pd.nl = (int)(swap ? t_len[p] : s_len[p]);
     pd.nc = (int)(swap ? s_len[p] : t_len[p]);
     const long long win = windows ? windows[p] : spec->window;
-    int w = win < 0 ? pd.nl : (int)std::min<long long>(win, 1LL << 30);
+    int w = win < 0 ? std::max(pd.nl, pd.nc) : (int)std::min<long long>(win, 1LL << 30);
     double cut = cutoffs ? cutoffs[p] : INFINITY;
     bool ea_rows = false;
     out_cells[p] = 0;
     out_cost[p] = INFINITY;
-    if (variant == 0) {  // base: compute_base (no window) or compute_ea(window, inf)
+    if (run_sem && variant == 0) {  // _base: the full matrix, window and cutoff unused (_speedups.pyx:103-126)
+      cut = INFINITY;
+      w = std::max(pd.nl, pd.nc);
+    } else if (variant == 0) {  // base: compute_base (no window) or compute_ea(window, inf)
       cut = INFINITY;
       if (spec->window < 0 && !windows) w = pd.nl;
     } else if (variant == 1) {  // ea: row abandoning; NaN never abandons
@@ -488,15 +503,23 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
     if (w < pd.nl - pd.nc) continue;  // infeasible window: (+inf, 0)
     pd.w = w;
     pd.cut = cut;
+    if (keep) ea_rows = variant == 1;  // ea rows count whole band rows even at cutoff +inf
     // ea with a finite cutoff, eapruned and pruned_only report the reference's own cell
     // count (ek_refcells.cuh) when the row-stripe replay engine holds the pair
     if ((ea_rows || variant == 2 || variant == 3) && pd.nc <= kRefMaxCols && pd.nl <= 2048 && !spec->precision) {
-      const int reng = ea_rows ? E_STR16_EA : (w < pd.nl - 1 ? E_STRB16 : E_STR16);
+      const int reng = ea_rows ? E_STR16_EA : (w < std::max(pd.nl, pd.nc) - 1 ? E_STRB16 : E_STR16);
       pd.pad_ = ea_rows ? 1 : variant;
       rgroups[reng].push_back(pd);
       ridx[reng].push_back(p);
-      rlmax[reng] = std::max(rlmax[reng], pd.nl);
+      rlmax[reng] = std::max(rlmax[reng], std::max(pd.nl, pd.nc));
       continue;
+    }
+    if (keep) {  // beyond the replay engine: transpose (same cost for eapruned; ea's is not)
+      if (variant == 1)
+        return fail("ea on rows shorter than columns (%d x %d) exceeds the row-stripe engine", pd.nl, pd.nc);
+      std::swap(pd.xoff, pd.yoff);
+      std::swap(pd.nl, pd.nc);
+      if (w < pd.nl - pd.nc) continue;
     }
     const int eng = choose_engine(pd.nl, pd.nc, w, ea_rows);
     if (eng < 0) return fail("series of length %d x %d with window %d exceed this build's engines", pd.nl, pd.nc, w);
@@ -559,6 +582,27 @@ int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, con
   }
   CK(cudaStreamSynchronize(st));
   return 0;
+}
+
+extern "C" {
+
+int ek_distance_batch(const ek_spec* spec, int32_t variant, int64_t n_pairs, const double* series,
+                      int64_t series_len, const int64_t* s_off, const int64_t* s_len, const int64_t* t_off,
+                      const int64_t* t_len, const double* cutoffs, const int64_t* windows, double* out_cost,
+                      int64_t* out_cells) {
+  return distance_batch_impl(spec, variant, n_pairs, series, series_len, s_off, s_len, t_off, t_len, cutoffs,
+                             windows, out_cost, out_cells, false);
+}
+
+int ek_run_batch(const ek_spec* spec, int32_t engine, int64_t n_pairs, const double* series, int64_t series_len,
+                 const int64_t* l_off, const int64_t* l_len, const int64_t* c_off, const int64_t* c_len,
+                 const int64_t* windows, const double* cutoffs, double* out_cost, int64_t* out_cells) {
+  if (!windows && n_pairs > 0 && engine != 0) {
+    g_err = "ek_run_batch: ea / eapruned need a window per pair";
+    return -1;
+  }
+  return distance_batch_impl(spec, engine, n_pairs, series, series_len, l_off, l_len, c_off, c_len, cutoffs,
+                             windows, out_cost, out_cells, true);
 }
 
 // guarded engine for wide bands (EKB_GUARD=0/8/16 overrides, for tuning)

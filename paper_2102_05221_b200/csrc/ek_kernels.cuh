@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(128) k_pairs(const double* __restrict__ series
   NoLoader ld;
   for (int pid = blockIdx.x * (blockDim.x >> 5) + wib; pid < npairs; pid += nwarps) {
     const PairDesc pd = pairs[pid];
-    const Params pp = pair_params(prm, pd.nl);
+    const Params pp = pair_params(prm, max(pd.nl, pd.nc));
     __syncwarp();
     stage_series<KIND>(X, series + pd.xoff, pd.nl, PAD);
     stage_series<KIND>(Y, series + pd.yoff, pd.nc, PAD);

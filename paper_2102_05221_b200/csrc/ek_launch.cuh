@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(32) k_pairs_ref(const double* __restrict__ ser
   __shared__ double terms[32];
   for (int pid = blockIdx.x; pid < npairs; pid += gridDim.x) {
     const PairDesc pd = pairs[pid];
-    const Params pp = pair_params(prm, pd.nl);
+    const Params pp = pair_params(prm, max(pd.nl, pd.nc));
     const int nl = pd.nl, nc = pd.nc, w = pd.w;
     __syncwarp();
     stage_series<KIND>(X, series + pd.xoff, nl, PAD);

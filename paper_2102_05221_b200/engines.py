@@ -87,15 +87,27 @@ def _one(rec: Recurrence, variant: str, window, cutoff, backend) -> EngineResult
     return EngineResult(float(costs[0]), int(cells[0]))
 
 
+def _dispatch(rec: Recurrence, engine: str, window: int, cutoff: float, backend) -> EngineResult:
+    """engines._dispatch (engines.py:29-50) over the GPU seam: ``_speedups.run`` semantics
+    (speedups.py / ek_run_batch), the recurrence's orientation kept as built."""
+    from . import speedups
+
+    _backend.resolve(backend)
+    spec = rec.spec
+    h = _lib.SpecHandle(spec, longest_lengths=[max(rec.shape)])
+    costs, cells = speedups._run_raw(speedups._ENGINES[engine], [rec.lines], [rec.cols], h, [int(window)],
+                                     [float(cutoff)])
+    return EngineResult(float(costs[0]), int(cells[0]))
+
+
 def compute_base(rec: Recurrence, backend: str | None = None) -> EngineResult:
     """Exact cost over the full matrix; cells_computed is lines*cols (engines.py:60-62)."""
-    # the full matrix is the band of half-width len(lines) (every |i-j| < len(lines))
-    return _one(rec, "base", len(rec.lines), math.inf, backend)
+    return _dispatch(rec, "base", 0, math.inf, backend)
 
 
 def compute_ea(rec: Recurrence, window: int, cutoff: float = math.inf, backend: str | None = None) -> EngineResult:
     """Windowed cost, abandoning once a whole row exceeds ``cutoff`` (engines.py:65-69)."""
-    return _one(rec, "ea", window, cutoff, backend)
+    return _dispatch(rec, "ea", window, cutoff, backend)
 
 
 def compute_eapruned(rec: Recurrence, window: int, cutoff: float = math.inf, backend: str | None = None,
@@ -106,7 +118,7 @@ def compute_eapruned(rec: Recurrence, window: int, cutoff: float = math.inf, bac
     (the reference's stale-read checker for its pure-Python row engine) has no
     GPU counterpart; use compute-sanitizer on the library instead.
     """
-    return _one(rec, "eapruned", window, cutoff, backend)
+    return _dispatch(rec, "eapruned", window, cutoff, backend)
 
 
 def diagonal_upper_bound(rec: Recurrence, window: int) -> float:

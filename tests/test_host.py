@@ -128,3 +128,83 @@ def test_generator_is_seeded():
     b = datagen.warped_prototypes(5, 64, 2, 0.1, 3)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert np.allclose(a[0].mean(axis=1), 0, atol=1e-12)
+
+
+# ---- the Recurrence payload (kernels.py:128-154, 264-277): the reference's own kernel tests
+# (pkg/tests/test_kernels.py:119-162) restated, plus a check of every closure against the
+# live reference's where it is importable (this container)
+
+def test_erp_border_prefix():
+    rec = make_recurrence(DistanceSpec(kind="erp", window=2, erp_gap=0.0), [3.0, 1.0], [3.0, 1.0])
+    assert rec.init_v_border(1) == 9.0
+    assert rec.init_v_border(2) == 10.0
+    assert rec.init_corner == 0.0
+    assert rec.v_border_vals.tolist() == [0.0, 9.0, 10.0]
+
+
+def test_msm_canonical_is_absolute_regardless_of_mode():
+    for mode in ("squared", "absolute"):
+        rec = make_recurrence(DistanceSpec(kind="msm", msm_c=0.5, cost_mode=mode), [4.0, 0.0], [1.0, 0.0])
+        assert rec.canonical(1, 1) == 3.0
+
+
+def test_dtw_borders_are_infinite():
+    rec = make_recurrence(DistanceSpec(kind="dtw"), [1.0, 2.0], [3.0, 4.0])
+    for k in (1, 2):
+        assert math.isinf(rec.init_h_border(k))
+        assert math.isinf(rec.init_v_border(k))
+    assert rec.v_border_vals is None and rec.h_border_vals is None
+
+
+def _specs(rng, maxlen, mode="squared"):
+    return [DistanceSpec(kind="dtw", cost_mode=mode), DistanceSpec(kind="cdtw", window=3, cost_mode=mode),
+            DistanceSpec(kind="wdtw", wdtw_g=float(rng.uniform(0, 0.5)), cost_mode=mode),
+            DistanceSpec(kind="erp", window=int(rng.integers(0, maxlen)), erp_gap=float(rng.uniform(-1, 1)),
+                         cost_mode=mode),
+            DistanceSpec(kind="msm", msm_c=float(rng.uniform(0, 2)), cost_mode=mode),
+            DistanceSpec(kind="twe", twe_nu=float(rng.uniform(0, 1)), twe_lambda=float(rng.uniform(0, 2)),
+                         cost_mode=mode)]
+
+
+def test_border_monotonicity_and_nonnegative_moves(rng):
+    for mode in ("squared", "absolute"):
+        for spec in _specs(rng, 10, mode):
+            rec = make_recurrence(spec, rng.uniform(-9, 9, 10), rng.uniform(-9, 9, 8))
+            nl, nc = rec.shape
+            vb = [rec.init_v_border(i) for i in range(1, nl + 1)]
+            hb = [rec.init_h_border(j) for j in range(1, nc + 1)]
+            assert all(a <= b for a, b in zip(vb, vb[1:]))
+            assert all(a <= b for a, b in zip(hb, hb[1:]))
+            for i in range(1, nl + 1):
+                for j in range(1, nc + 1):
+                    assert rec.canonical(i, j) >= 0.0 and rec.alt_row(i, j) >= 0.0 and rec.alt_col(i, j) >= 0.0
+
+
+def test_recurrence_closures_equal_the_live_reference(rng):
+    """Every closure value and payload array bit-equal to the reference's make_recurrence."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    import refpkg
+
+    ek = refpkg.load()
+    if ek is None:
+        pytest.skip("reference package not present (GPU box)")
+    for mode in ("squared", "absolute"):
+        for spec in _specs(rng, 12, mode):
+            refspec = ek.DistanceSpec(**{k: getattr(spec, k) for k in ("kind", "window", "wdtw_g", "erp_gap", "msm_c",
+                                                                        "twe_nu", "twe_lambda", "cost_mode")})
+            for orient in ("auto", "st"):
+                a, b = rng.normal(0, 2, int(rng.integers(1, 12))), rng.normal(0, 2, int(rng.integers(1, 12)))
+                ours, ref = make_recurrence(spec, a, b, orient), ek.kernels.make_recurrence(refspec, a, b, orient)
+                assert ours.shape == ref.shape
+                nl, nc = ours.shape
+                for name in ("canonical", "alt_row", "alt_col"):
+                    f, g = getattr(ours, name), getattr(ref, name)
+                    assert [f(i, j) for i in range(1, nl + 1) for j in range(1, nc + 1)] == \
+                        [g(i, j) for i in range(1, nl + 1) for j in range(1, nc + 1)], (spec.kind, name)
+                assert [ours.init_v_border(i) for i in range(1, nl + 1)] == [ref.init_v_border(i) for i in range(1, nl + 1)]
+                assert [ours.init_h_border(j) for j in range(1, nc + 1)] == [ref.init_h_border(j) for j in range(1, nc + 1)]
+                for name in ("wdtw_weights", "v_border_vals", "h_border_vals"):
+                    x, y = getattr(ours, name), getattr(ref, name)
+                    assert (x is None) == (y is None) and (x is None or np.array_equal(x, y)), name

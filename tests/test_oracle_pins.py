@@ -122,3 +122,36 @@ def test_golden_subseq_fixtures():
         for chunk in (None, 97):
             off, d, _ = eko.subsequence(spec, "eapruned", g["q"], g["ref"], norm, chunk=chunk, threads=2)
             assert (off, d) == (g["off"][k], g["dist"][k])
+
+
+def test_refdrive_glue_matches_the_live_reference():
+    """The restated search loops around the reference's compiled kernel (oracle/refdrive.py,
+    the bench's CPU arm) give the live reference's answers, for every lb mode."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    import refpkg
+    from oracle import refdrive
+
+    ek = refpkg.load()
+    if ek is None or not refdrive.available():
+        pytest.skip("reference package / oracle/_ref not present (GPU box)")
+    rng = np.random.default_rng(31)
+    X = [np.cumsum(rng.normal(size=40)) for _ in range(25)] + [np.cumsum(rng.normal(size=33))]
+    Q = [np.cumsum(rng.normal(size=40)) for _ in range(3)]
+    for spec, refspec in ((DistanceSpec(kind="cdtw", window=4), ek.DistanceSpec(kind="cdtw", window=4)),
+                          (DistanceSpec(kind="dtw", cost_mode="absolute"),
+                           ek.DistanceSpec(kind="dtw", cost_mode="absolute"))):
+        for lb in ("none", "keogh", "keogh2"):
+            env = refdrive.candidate_envelopes(spec, X, lb)
+            for q in Q:
+                d, b, cells, comp, ab, skips = refdrive.nn_search(spec, "eapruned", q, X, lb, env)
+                rd, rb, st = ek.nn_search(q, X, ek.SearchConfig(spec=refspec, variant="eapruned", lb=lb))
+                assert (d, b, cells, comp, ab, skips) == (rd, rb, st.cells, st.computed, st.abandoned, st.lb_skips)
+        stream = np.cumsum(rng.normal(size=300))
+        for lb in ("none", "keogh2"):
+            off, d, cells = refdrive.subsequence_search(spec, "eapruned", Q[0][:30], stream, True, lb=lb)
+            ro, rd, st = ek.subsequence_search(Q[0][:30], stream, ek.SearchConfig(spec=refspec, variant="eapruned",
+                                                                                   normalize=True, lb=lb))
+            assert (off, d, cells) == (ro, rd, st.cells)
