@@ -106,6 +106,13 @@ int ek_nn_dev(const ek_spec* spec, int32_t variant, const double* d_queries, con
 int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int64_t total, const int64_t* off,
                 const int64_t* len, int64_t n, double* D, int64_t* cells);
 
+/* Pairs [pair_lo, pair_hi) of the upper triangle in row-major order (the order of
+ * numpy.triu_indices(n, 1)): out[p - pair_lo] = distance(spec, variant, X_i, X_j) for pair
+ * p = (i, j).  The unit of the multi-GPU all-pairs shard: a rank passes its
+ * contiguous pair range, the device maps indices to (i, j), no per-pair host arrays. */
+int ek_pairwise_range(const ek_spec* spec, int32_t variant, const double* series, int64_t total, const int64_t* off,
+                      const int64_t* len, int64_t n, int64_t pair_lo, int64_t pair_hi, double* out, int64_t* cells);
+
 int ek_pairwise_dev(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
                     const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells, void* stream);
 

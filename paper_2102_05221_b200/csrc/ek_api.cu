@@ -202,6 +202,12 @@ int inputs_finite(const double* a, long long na, const double* b, long long nb, 
   return bad ? fail("%s", kNonFinite) : 0;
 }
 
+// p[0..n) = v, p[n] = 0
+__global__ void k_fill_i32(int* p, long long n, int v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = i < n ? v : 0;
+}
+
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = v;
@@ -774,11 +780,19 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
                           (const int*)dord.as<int>(), 0, ka, ka, 1, 1, win, (int)max_len, ph.prm, (int)share,
                           dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 32,
-                          (const float*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count))
+                          (const float*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count, (int*)nullptr))
       return -1;
   }
   mark(st, "nn_phaseA");
   if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the LB keys and envelopes (side stream)
+  // LB path: per-query stop ranks (ncand = none yet) and the count of stopped queries
+  DBuf dqstop;
+  if (use_lb) {
+    if (dqstop.alloc(sizeof(int) * (size_t)(nq + 1), st)) return -1;
+    if (launch_plain(k_fill_i32, dim3((unsigned)std::min<long long>(64, (nq + 256) / 256)), dim3(256), 0, st,
+                     dqstop.as<int>(), (long long)nq, (int)ncand))
+      return -1;
+  }
   // phase B, one launch of two segments: the best ranks (where the survivors concentrate)
   // in small items for load balance, the rest in larger ones.  Without the LB path:
   // 4 + 64 ranks one pair per item, then items of 8 (measured best on C2 before the LB
@@ -808,7 +822,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                           dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 64 + 32 * sgi,
                           (const float*)(use_lb ? dskeys.as<float>() : nullptr),
                           (const float2*)denvq.as<float2>(), seg1_wide ? dovf2.as<int2>() : dovf.as<int2>(),
-                          seg1_wide ? ovf2_count : ovf_count))
+                          seg1_wide ? ovf2_count : ovf_count, (use_lb && ncand <= 16384) ? dqstop.as<int>() : (int*)nullptr))
       return -1;
   }
   mark(st, "nn_phaseB");
@@ -930,23 +944,25 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   return 0;
 }
 
+// d_D != null: the full matrix; else pairs [plo, phi) of the upper triangle into d_vec
 static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
                              const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells,
-                             cudaStream_t st) {
+                             cudaStream_t st, long long plo = 0, long long phi = -1, double* d_vec = nullptr) {
   if (check_spec(spec)) return -1;
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
+  if (cells) *cells = 0;
   if (n <= 0) return 0;
-  CK(cudaMemsetAsync(d_D, 0, sizeof(double) * (size_t)n * n, st));  // diagonal 0.0
-  if (n == 1) {
-    if (cells) *cells = 0;
-    return 0;
-  }
+  if (d_D) CK(cudaMemsetAsync(d_D, 0, sizeof(double) * (size_t)n * n, st));  // diagonal 0.0
+  const long long np_all = n * (n - 1) / 2;
+  if (phi < 0) phi = np_all;
+  if (plo < 0 || phi > np_all || plo > phi) return fail("pair range [%lld, %lld) outside [0, %lld)", plo, phi, np_all);
+  if (phi == plo) return 0;
   const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
   const int eng = choose_engine(max_len, max_len, win < 0 ? max_len : win, false, true);
   if (eng < 0) return fail("series length %d exceeds this build's engines", max_len);
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
-  const long long np = n * (n - 1) / 2;
+  const long long np = phi - plo;
   mark_reset();
   mark(st, "start");
   DBuf dcnt, dtot;
@@ -960,7 +976,7 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
   if (strip_scratch(tf, eng, 32 * wpb, tsmem, max_len, ph.prm, dstrip, st)) return -1;
   if (launch_persistent(tf, 32 * wpb, tsmem, st, np,
                         d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, ph.prm, d_D,
-                        dtot.as<unsigned long long>(), dcnt.as<int>()))
+                        plo, phi, d_vec, dtot.as<unsigned long long>(), dcnt.as<int>()))
     return -1;
   mark(st, "triangle");
   if (cells) {
@@ -1008,6 +1024,33 @@ int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int6
                         cells, st))
     return -1;
   CK(cudaMemcpyAsync(D, dD.p, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ek_pairwise_range(const ek_spec* spec, int32_t variant, const double* series, int64_t total, const int64_t* off,
+                      const int64_t* len, int64_t n, int64_t pair_lo, int64_t pair_hi, double* out, int64_t* cells) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  if (cells) *cells = 0;
+  if (n <= 1 || pair_hi <= pair_lo) return 0;
+  cudaStream_t st = g_ctx.stream;
+  std::vector<int32_t> l32(n);
+  int32_t mx = 0;
+  for (int64_t k = 0; k < n; ++k) mx = std::max(mx, l32[k] = (int32_t)len[k]);
+  const long long m = pair_hi - pair_lo;
+  DBuf ds, doff, dlen, dv;
+  if (ds.alloc(sizeof(double) * total, st) || doff.alloc(8 * n, st) || dlen.alloc(4 * n, st) ||
+      dv.alloc(sizeof(double) * (size_t)m, st))
+    return -1;
+  CK(cudaMemcpyAsync(ds.p, series, sizeof(double) * total, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(doff.p, off, 8 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dlen.p, l32.data(), 4 * n, cudaMemcpyHostToDevice, st));
+  if (inputs_finite(ds.as<double>(), total, nullptr, 0, st)) return -1;
+  if (pairwise_dev_impl(spec, variant, ds.as<double>(), doff.as<int64_t>(), dlen.as<int32_t>(), n, mx, nullptr, cells,
+                        st, pair_lo, pair_hi, dv.as<double>()))
+    return -1;
+  CK(cudaMemcpyAsync(out, dv.p, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return 0;
 }

@@ -20,6 +20,11 @@
 
 namespace ekb {
 
+#ifdef EKB_TRACE
+// per-warp timeline of the last k_nn launch (debug builds only): start, end, DP ns, items, DPs
+__device__ unsigned long long g_trace[8192 * 5];
+#endif
+
 // Engine codes: 0..2 diagonal P=4/8/16; 3..5 stripe S=4/8/16 (unbanded);
 // 6 stripe S=16 banded; 7 stripe S=16 banded with row abandoning ("ea");
 // 8..9 guarded diagonal P=8/16: a band narrower than the pair's own, valid as long as
@@ -309,8 +314,12 @@ __device__ __forceinline__ void tri_index(long long p, int n, int& i, int& j) {
 template <int KIND, int MODE, int ENG>
 __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ series, const long long* __restrict__ off,
                                                   const int* __restrict__ len, int n, int win, int lmax, Params prm,
-                                                  double* __restrict__ D, unsigned long long* __restrict__ cells_total,
+                                                  double* __restrict__ D, long long plo, long long phi,
+                                                  double* __restrict__ Dvec,
+                                                  unsigned long long* __restrict__ cells_total,
                                                   int* __restrict__ counter) {
+  // pairs [plo, phi) of the upper triangle (row-major, np.triu_indices order); Dvec != null
+  // writes cost p to Dvec[p - plo] (a rank's shard, ek_pairwise_range), else both cells of D
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
   const int wib = threadIdx.x >> 5;
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
   R* X = (R*)smem + wib * warp_stride(lmax, ENG) + PAD;
   R* Y = X + series_slot(lmax, PAD);
   R* tab = Y - PAD + series_slot(lmax, PAD);
-  const long long npairs = (long long)n * (n - 1) / 2;
+  const long long npairs = phi;
   NoLoader ld;
   unsigned long long my_cells = 0;
   if constexpr (engine_W(ENG) == 16) {
@@ -331,7 +340,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
     R* tabh = Yh - PAD + series_slot(lmax, PAD);
     for (;;) {
       long long p = 0;
-      if (lane == 0) p = (long long)atomicAdd((unsigned long long*)counter, 2ULL);
+      if (lane == 0) p = plo + (long long)atomicAdd((unsigned long long*)counter, 2ULL);
       p = __shfl_sync(FULL, p, 0);
       if (p >= npairs) break;
       int pa[2], pb[2], ps[2], pt[2];
@@ -369,8 +378,12 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
                       (same ? 2u : 1u);
         }
         if (hl == 0 && (same || half == 0)) {
-          D[(long long)pa[k] * n + pb[k]] = cost;
-          D[(long long)pb[k] * n + pa[k]] = cost;
+          if (Dvec) {
+            Dvec[p + k - plo] = cost;
+          } else {
+            D[(long long)pa[k] * n + pb[k]] = cost;
+            D[(long long)pb[k] * n + pa[k]] = cost;
+          }
         }
       }
     }
@@ -379,7 +392,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
   }
   for (;;) {
     long long p = 0;
-    if (lane == 0) p = (long long)atomicAdd((unsigned long long*)counter, 1ULL);
+    if (lane == 0) p = plo + (long long)atomicAdd((unsigned long long*)counter, 1ULL);
     p = __shfl_sync(FULL, p, 0);
     if (p >= npairs) break;
     int a, b;
@@ -404,8 +417,12 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
       my_cells += (unsigned long long)warp_cells<ENG>(nl, nc, w, tend, KIND == K_ERP ? 0 : 1);
     }
     if (lane == 0) {
-      D[(long long)a * n + b] = cost;
-      D[(long long)b * n + a] = cost;
+      if (Dvec) {
+        Dvec[p - plo] = cost;
+      } else {
+        D[(long long)a * n + b] = cost;
+        D[(long long)b * n + a] = cost;
+      }
     }
   }
   if (lane == 0 && cells_total) atomicAdd(cells_total, my_cells);
@@ -464,7 +481,8 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
                                             unsigned long long* cutbits, double* __restrict__ out,
                                             int* __restrict__ tend_out, int* __restrict__ counter,
                                             const float* __restrict__ skeys, const float2* __restrict__ envq,
-                                            int2* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+                                            int2* __restrict__ ovf_list, int* __restrict__ ovf_count,
+                                            int* __restrict__ qstop) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
   constexpr int PF = kChunk / 32;
@@ -493,9 +511,21 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
   // L2.  (Claiming one item ahead measured slower: a claimed item waits behind the
   // current one's DPs, which unbalances the tail.)
   int ck = (int)((blockIdx.x * (blockDim.x >> 5) + wib) % kNnCounters), ctr_left = kNnCounters;
+  // LB path: the ranks are sorted by the keys' top 16 bits (k_rank_radix; truncation rounds
+  // a positive float down), so once a rank's truncated key exceeds the threshold of the
+  // query's cutoff, every later rank fails its key test too: qstop[q] is the least such
+  // rank, items at or past it are skipped unread, and qstop[nq] counts the queries that
+  // have one -- when it reaches nq no item can hold a pair to visit and the warps leave
+  // without claiming the rest (the cutoff only decreases, so a stop stays valid).
+  const bool stops = use_lb && qstop != nullptr;
+#ifdef EKB_TRACE
+  unsigned long long tr_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_t0));
+  unsigned long long tr_dp = 0, tr_items = 0, tr_dps = 0;
+#endif
   for (;;) {
     long long it = -1;
-    if (lane == 0) {
+    if (lane == 0 && !(stops && *(volatile int*)(qstop + nq) >= nq)) {
       while (ctr_left > 0) {
         const long long cand = (long long)atomicAdd(ctr + ck, 1ULL) * kNnCounters + ck;
         if (cand < nitems) {
@@ -508,6 +538,9 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
     }
     it = __shfl_sync(FULL, it, 0);
     if (it < 0) break;
+#ifdef EKB_TRACE
+    ++tr_items;
+#endif
     const bool first_seg = !TWO_SEG || it < items1;
     const long long is = first_seg ? it : it - items1;
     const int q = (int)(is % nq);
@@ -523,9 +556,18 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
     float key = 0.f;
     double pf[PF];
     if (use_lb) {
+      if (stops && __shfl_sync(FULL, lane == 0 ? *(volatile int*)(qstop + q) : 0, 0) <= k_lo) continue;
       key = lane < cnt ? skeys[(long long)q * ncand + k_lo + lane] : 0.f;
       const double thr = lb_threshold<MODE>(cut, lq);
       todo = __ballot_sync(FULL, lane < cnt && (double)key <= thr);
+      if (stops) {
+        const float kt = __uint_as_float(__float_as_uint(key) & 0xffff0000u);  // the sort key, <= key
+        const unsigned past = __ballot_sync(FULL, lane < cnt && (double)kt > thr);
+        if (past && lane == 0) {
+          const int r0 = k_lo + __ffs(past) - 1;
+          if (atomicMin(qstop + q, r0) >= ncand) atomicAdd(qstop + nq, 1);
+        }
+      }
       if (!todo) continue;  // nothing to visit: the query is not even staged
     }
     // this item's candidates and their metadata, one per lane (K <= 32)
@@ -608,7 +650,16 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
         __syncwarp();
         const SmemSeriesT<R> X{q_rows ? QB : CB, nl};
         const SmemSeriesT<R> Y{q_rows ? CB : QB, nc};
+#ifdef EKB_TRACE
+        unsigned long long tr_a, tr_b;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_a));
+#endif
         run_engine<KIND, MODE, ENG, true>(X, nl, Y, nc, w, cut, cutbits + q, tabe, tablen, pp, ld, cost, tend);
+#ifdef EKB_TRACE
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_b));
+        tr_dp += tr_b - tr_a;
+        ++tr_dps;
+#endif
         if (share && lane == 0 && cost < EKB_INF) {
           // values are >= 0 (or +inf), so IEEE bits order as unsigned integers
           atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
@@ -626,6 +677,20 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
       }
     }
   }
+#ifdef EKB_TRACE
+  if (lane == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (gw < 8192) {
+      g_trace[gw * 5 + 0] = tr_t0;
+      g_trace[gw * 5 + 1] = t1;
+      g_trace[gw * 5 + 2] = tr_dp;
+      g_trace[gw * 5 + 3] = tr_items;
+      g_trace[gw * 5 + 4] = tr_dps;
+    }
+  }
+#endif
 }
 
 // Redo of the pairs a guarded band gave up on (`list`, *count of them) with a wider engine

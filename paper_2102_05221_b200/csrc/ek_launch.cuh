@@ -7,11 +7,11 @@
 namespace ekb {
 
 using PairsFn = void (*)(const double*, const PairDesc*, int, int, Params, double*, int*);
-using TriFn = void (*)(const double*, const long long*, const int*, int, int, int, Params, double*,
-                      unsigned long long*, int*);
+using TriFn = void (*)(const double*, const long long*, const int*, int, int, int, Params, double*, long long,
+                      long long, double*, unsigned long long*, int*);
 using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, int, int, int, int, int, int, Params, int, unsigned long long*,
-                      double*, int*, int*, const float*, const float2*, int2*, int*);
+                      double*, int*, int*, const float*, const float2*, int2*, int*, int*);
 using NNFixFn = void (*)(const double*, const long long*, const int*, const double*, const long long*, const int*,
                          int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*,
                          int2*, int*);

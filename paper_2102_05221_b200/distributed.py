@@ -8,8 +8,13 @@ Every unit of work is independent, so nothing on the data path is exchanged:
   reads its range plus the query length - 1 halo of the stream, and the ranks' best
   (distance, offset) records meet in one lexicographic minimum -- the same tie rule as
   on one GPU (lowest offset wins).
-* All-pairs: the upper-triangle pairs are dealt round-robin; the values are gathered
-  and mirrored.
+* All-pairs: the upper triangle (numpy.triu_indices order) is split into contiguous pair
+  ranges; each rank computes its range in one call (the device maps pair indices to
+  (i, j), search.pairwise_range), and the values are gathered and mirrored.
+
+Each process computes on its own GPU: ``bind_device()`` (called by every helper when it
+uses the library) selects ``LOCAL_RANK`` modulo the visible devices for torch and for the
+library (``ek_init``), as torchrun launches one process per GPU.
 
 The process group is torch.distributed's (NCCL between GPUs; gloo works for the
 host-side logic).  ``compute`` hooks let tests run the sharding with another
@@ -19,10 +24,11 @@ backend of the same signature (the CPU oracle under gloo).
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
-from . import engines, search
+from . import search
 from .kernels import DistanceSpec
 
 
@@ -31,6 +37,34 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     base, extra = divmod(n, world)
     lo = rank * base + min(rank, extra)
     return lo, lo + base + (1 if rank < extra else 0)
+
+
+_BOUND = None
+
+
+def bind_device(local_rank: int | None = None) -> int:
+    """Bind this process to GPU ``LOCAL_RANK % device_count`` (torch current device and the
+    library's context).  Returns the device index.  Idempotent."""
+    global _BOUND
+    from . import _lib
+
+    if local_rank is None:
+        local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n = _lib.lib().ek_device_count()
+    if n <= 0:
+        raise RuntimeError("no CUDA device for this rank (there is no CPU fallback)")
+    dev = local_rank % n
+    if _BOUND == dev:
+        return dev
+    try:
+        import torch
+
+        torch.cuda.set_device(dev)
+    except ImportError:  # pragma: no cover - torch is the plumbing, not required by the library
+        pass
+    _lib.check(_lib.lib().ek_init(dev))
+    _BOUND = dev
+    return dev
 
 
 def _group_info(group):
@@ -53,6 +87,8 @@ def nn_batch_sharded(spec: DistanceSpec, variant: str, queries, candidates, grou
     rank, world = _group_info(group)
     queries = list(queries) if not isinstance(queries, np.ndarray) else queries
     lo, hi = shard_range(len(queries), rank, world)
+    if compute is None:
+        bind_device()
     run = compute or search.nn_batch
     local = run(spec, variant, queries[lo:hi], candidates)
     parts = _all_gather(tuple(np.asarray(a) for a in local), group)
@@ -72,6 +108,8 @@ def subsequence_search_sharded(query, reference, cfg, group=None, compute=None):
     lo, hi = shard_range(max(nwin, 0), rank, world)
     best = (math.inf, -1, 0, 0, 0)
     if hi > lo:
+        if compute is None:
+            bind_device()
         run = compute or search.subsequence_search
         off, d, st = run(query, reference[lo:hi + lq - 1], cfg)
         best = (d, off + lo if off >= 0 else -1, st.computed, st.abandoned, st.cells)
@@ -86,21 +124,26 @@ def subsequence_search_sharded(query, reference, cfg, group=None, compute=None):
 
 
 def pairwise_sharded(spec: DistanceSpec, X, variant: str = "pruned_only", group=None, compute=None):
-    """The symmetric all-pairs matrix over all ranks (upper-triangle pairs dealt
-    round-robin, gathered, mirrored; diagonal 0.0) -> (D, cells) on every rank."""
+    """The symmetric all-pairs matrix over all ranks -> (D, cells) on every rank.
+
+    Rank r computes the contiguous pair range shard_range(n(n-1)/2, r, world) of the upper
+    triangle (numpy.triu_indices order) with one ``pairwise_range`` call; the ranges are
+    gathered and mirrored (diagonal 0.0).  ``compute(spec, variant, X, lo, hi) -> (costs,
+    cells)`` replaces the library (tests)."""
     rank, world = _group_info(group)
     X = [np.asarray(x, dtype=np.float64) for x in X]
     n = len(X)
+    lo, hi = shard_range(n * (n - 1) // 2, rank, world)
+    if compute is None:
+        bind_device()
+    run = compute or search.pairwise_range
+    costs, cells = run(spec, X, lo, hi, variant) if compute is None else run(spec, variant, X, lo, hi)
+    parts = _all_gather((lo, hi, np.asarray(costs), int(cells)), group)
     iu, ju = np.triu_indices(n, k=1)
-    mine = np.arange(rank, len(iu), world)
-    run = compute or engines.distance_batch
-    costs, cells = run(spec, variant, [(X[iu[k]], X[ju[k]]) for k in mine]) if len(mine) else (
-        np.zeros(0), np.zeros(0, dtype=np.int64))
-    parts = _all_gather((mine, np.asarray(costs), np.asarray(cells)), group)
     D = np.zeros((n, n), dtype=np.float64)
     total = 0
-    for idx, c, ce in parts:
-        D[iu[idx], ju[idx]] = c
-        D[ju[idx], iu[idx]] = c
-        total += int(np.sum(ce))
+    for plo, phi, c, ce in parts:
+        D[iu[plo:phi], ju[plo:phi]] = c
+        D[ju[plo:phi], iu[plo:phi]] = c
+        total += ce
     return D, total

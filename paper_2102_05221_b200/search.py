@@ -248,4 +248,30 @@ def pairwise(spec: DistanceSpec, X, variant: str = "pruned_only", backend=None, 
     return D, int(cells[0])
 
 
+def pairwise_range(spec: DistanceSpec, X, pair_lo: int, pair_hi: int, variant: str = "pruned_only", backend=None,
+                   precision: str = "float64"):
+    """Pairs [pair_lo, pair_hi) of the upper triangle, in ``numpy.triu_indices(n, 1)`` order,
+    in one GPU call -> (costs float64[pair_hi - pair_lo], cells).  The all-pairs shard of a
+    rank (distributed.pairwise_sharded); the device maps pair indices to (i, j)."""
+    if variant not in VARIANTS:
+        raise SpecError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    _backend.resolve(backend)
+    _lib.precision_code(precision)
+    flat, off, lens = _pack(X)
+    n = len(lens)
+    total = n * (n - 1) // 2
+    if not 0 <= pair_lo <= pair_hi <= total:
+        raise ValueError(f"pair range [{pair_lo}, {pair_hi}) outside [0, {total})")
+    out = np.empty(pair_hi - pair_lo, dtype=np.float64)
+    if pair_hi == pair_lo:
+        return out, 0
+    longest = np.unique(np.maximum.outer(np.unique(lens), np.unique(lens)))
+    h = _lib.SpecHandle(spec, longest_lengths=longest, precision=precision)
+    cells = np.zeros(1, dtype=np.int64)
+    _lib.check(_lib.lib().ek_pairwise_range(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(flat), len(flat),
+                                            _lib.iptr(off), _lib.iptr(lens), n, int(pair_lo), int(pair_hi),
+                                            _lib.dptr(out), _lib.iptr(cells)))
+    return out, int(cells[0])
+
+
 _ = math  # re-exported names only

@@ -54,7 +54,7 @@ def test_pairwise_exact_shape(gpu, name):
     X, _ = datagen.pairwise_workload()
     assert X.shape == (1024, 256)
     spec = b.spec_for(name)
-    D = gpu.pairwise(spec, X, variant="pruned_only")
+    D, _ = gpu.pairwise(spec, X, variant="pruned_only")
     Dw, _ = eko.pairwise(spec, X, threads=THREADS)
     assert np.array_equal(D.view(np.int64), Dw.view(np.int64)), int(np.sum(D != Dw))
     assert np.array_equal(D, D.T) and not np.diag(D).any()

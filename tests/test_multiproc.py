@@ -85,9 +85,10 @@ def _oracle_hooks():
         off, d, cells = eko.subsequence(cfg.spec, cfg.variant, q, ref, cfg.normalize, threads=1)
         return off, d, SearchStats(cells=cells)
 
-    def pairs(spec, variant, prs):
-        out = [eko.distance(spec, variant, a, b) for a, b in prs]
-        return np.array([o[0] for o in out]), np.array([o[1] for o in out], dtype=np.int64)
+    def pairs(spec, variant, X, lo, hi):  # pairs [lo, hi) in np.triu_indices order
+        iu, ju = np.triu_indices(len(X), k=1)
+        out = [eko.distance(spec, variant, X[iu[k]], X[ju[k]]) for k in range(lo, hi)]
+        return np.array([o[0] for o in out]), int(sum(o[1] for o in out))
 
     return nn, subseq, pairs
 
@@ -148,3 +149,63 @@ def test_two_rank_sharded_entry_points_match_single_process():
     D = eko.pairwise(DistanceSpec(kind="erp", window=5, erp_gap=0.0), X)[0]
     assert np.array_equal(res_pw[0], D)
     assert [distributed.shard_range(7, r, 3) for r in range(3)] == [(0, 3), (3, 5), (5, 7)]
+
+
+def _gpu_sharded_worker(rank, world, port, out):
+    """Both ranks call the REAL library (bind_device: LOCAL_RANK % device count -> both on
+    cuda:0 of a one-GPU box; their kernels never wait on each other)."""
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2102_05221_b200 import DistanceSpec, SearchConfig, datagen, distributed
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    C, _, protos = datagen.warped_prototypes(300, 128, 4, 0.1, 61)
+    Q, _, _ = datagen.warped_prototypes(21, 128, 4, 0.1, 62, protos=protos)
+    res_nn = distributed.nn_batch_sharded(DistanceSpec(kind="cdtw", window=12), "eapruned", Q, C)
+    rng = np.random.default_rng(7)
+    stream = np.cumsum(rng.normal(0, 1, 5000))
+    q = stream[2711:2811].copy()
+    cfg = SearchConfig(spec=DistanceSpec(kind="cdtw", window=5), variant="eapruned", normalize=True)
+    res_ss = distributed.subsequence_search_sharded(q, stream, cfg)
+    X = datagen.warped_prototypes(61, 96, 3, 0.1, 63)[0]
+    res_pw = {k: distributed.pairwise_sharded(spec, X)[0] for k, spec in
+              (("erp", DistanceSpec(kind="erp", window=9, erp_gap=0.0)), ("wdtw", DistanceSpec(kind="wdtw", wdtw_g=0.05)),
+               ("msm", DistanceSpec(kind="msm", msm_c=0.5)))}
+    if rank == 0:
+        out.put((res_nn[:2], res_ss[:2], res_pw, distributed._BOUND))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_two_rank_sharded_on_the_gpu_library_match_single_process(gpu):
+    """distributed.* over 2 gloo ranks on the real CUDA library equal one process's answers
+    (bit for bit), including the subsequence halo and the all-pairs pair ranges."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_sharded_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res_nn, res_ss, res_pw, bound = out.get(timeout=500)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert bound == 0
+    from paper_2102_05221_b200 import DistanceSpec, SearchConfig, datagen
+
+    C, _, protos = datagen.warped_prototypes(300, 128, 4, 0.1, 61)
+    Q, _, _ = datagen.warped_prototypes(21, 128, 4, 0.1, 62, protos=protos)
+    idx, dist_ = gpu.nn_batch(DistanceSpec(kind="cdtw", window=12), "eapruned", Q, C)[:2]
+    assert np.array_equal(res_nn[0], idx) and np.array_equal(res_nn[1], dist_)
+    rng = np.random.default_rng(7)
+    stream = np.cumsum(rng.normal(0, 1, 5000))
+    q = stream[2711:2811].copy()
+    cfg = SearchConfig(spec=DistanceSpec(kind="cdtw", window=5), variant="eapruned", normalize=True)
+    assert tuple(res_ss) == tuple(gpu.subsequence_search(q, stream, cfg)[:2]) and res_ss[0] == 2711
+    X = datagen.warped_prototypes(61, 96, 3, 0.1, 63)[0]
+    for k, spec in (("erp", DistanceSpec(kind="erp", window=9, erp_gap=0.0)), ("wdtw", DistanceSpec(kind="wdtw", wdtw_g=0.05)),
+                    ("msm", DistanceSpec(kind="msm", msm_c=0.5))):
+        assert np.array_equal(res_pw[k], gpu.pairwise(spec, X)[0]), k
