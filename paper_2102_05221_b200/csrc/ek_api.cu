@@ -202,6 +202,27 @@ int inputs_finite(const double* a, long long na, const double* b, long long nb, 
   return bad ? fail("%s", kNonFinite) : 0;
 }
 
+// cut[q] = the IEEE image of c0[q] (a distance: >= +0 or +inf), +0.0 for -0.0 / NaN never occurs
+__global__ void k_cut_from(unsigned long long* cut, const double* c0, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = c0[i];
+    if (v >= 0.0) atomicMin(cut + i, (unsigned long long)__double_as_longlong(v + 0.0));
+  }
+}
+
+// ek_nn's two candidate halves: r = [idx | dist | cells | computed | abandoned] x nq each;
+// the first half (lower indices) wins ties, as the serial scan's strict "<" does
+__global__ void k_nn_merge(long long nq, long long h, const long long* r1, const long long* r2, long long* out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
+    const long long i1 = r1[q], i2 = r2[q];
+    const double d1 = __longlong_as_double(r1[nq + q]), d2 = __longlong_as_double(r2[nq + q]);
+    const bool take2 = i2 >= 0 && (i1 < 0 || d2 < d1);
+    out[q] = take2 ? i2 + h : i1;
+    out[nq + q] = __double_as_longlong(take2 ? d2 : d1);
+    for (int k = 2; k < 5; ++k) out[k * nq + q] = r1[k * nq + q] + r2[k * nq + q];
+  }
+}
+
 // p[0..n) = v, p[n] = 0
 __global__ void k_fill_i32(int* p, long long n, int v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x)
@@ -631,9 +652,9 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
                        const int32_t* dqlen, int64_t nq, const double* dC, const int64_t* dcoff, const int32_t* dclen,
                        int64_t ncand, int32_t max_len, int32_t dense, int64_t* d_idx, double* d_dist,
                        int64_t* d_cells, int64_t* d_comp, int64_t* d_ab, cudaStream_t st, int nchunk = 0,
-                       int64_t chunk = 0) {
+                       int64_t chunk = 0, int ev0 = 0, const double* d_cut0 = nullptr) {
   // nchunk > 0: the candidates arrive in chunks of `chunk` series, chunk k once
-  // g_ctx.ev_chunk[k] has fired (ek_nn's overlapped upload); the LB keys of a chunk are
+  // g_ctx.ev_chunk[ev0 + k] has fired (ek_nn's overlapped upload); the LB keys of a chunk are
   // computed as soon as it is there, everything else waits for all of them
   if (check_spec(spec)) return -1;
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
@@ -643,7 +664,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   mark(st, "start");
   const bool lb_chunks = share_lb_path(spec, variant, dense, ncand);
   if (nchunk > 0 && !lb_chunks)
-    for (int k = 0; k < nchunk; ++k) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[k], 0));
+    for (int k = 0; k < nchunk; ++k) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[ev0 + k], 0));
   const int win = spec->window < 0 ? -1 : (int)std::min<long long>(spec->window, 1LL << 30);
   const int wmax = win < 0 ? max_len : win;
   const int eng = choose_engine(max_len, max_len, wmax, false);
@@ -708,7 +729,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     const int64_t csz = nchunk > 0 ? chunk : ncand;
     for (int k = 0; k < nch; ++k) {
       const int cb = (int)std::min<int64_t>(ncand, k * csz), ce = (int)std::min<int64_t>(ncand, (k + 1) * csz);
-      if (nchunk > 0) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[k], 0));
+      if (nchunk > 0) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[ev0 + k], 0));
       if (ce <= cb) continue;
       CK(envelope_pm(dC, (const long long*)dcoff + cb, L, ce - cb, win < 0 ? L : win, denv.as<float2>() + cb, scr, st,
                      (int)ncand));
@@ -754,6 +775,11 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   //    approximately; several on the LB ranking)
   if (launch_plain(k_fill_u64, dim3(64), dim3(256), 0, st, dcut.as<unsigned long long>(), (long long)nq,
                    0x7ff0000000000000ULL))
+    return -1;
+  // a caller's starting cutoffs (ek_nn's second candidate half: the first half's answers)
+  if (d_cut0 && share &&
+      launch_plain(k_cut_from, dim3((unsigned)((nq + 255) / 256)), dim3(256), 0, st, dcut.as<unsigned long long>(),
+                   d_cut0, (long long)nq))
     return -1;
   if (share) {
     // (the LB ranking's top candidates are not the Euclidean nearest: take the best of 16)
@@ -801,7 +827,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? env_int("EKB_NN_SEG1", 64) : ka + 64));
   const int K1_lb = env_int("EKB_NN_K1", 1), K2 = one_launch ? env_int("EKB_NN_K2", 4) : 8;
   const NNFn fnB = pick_nn(spec->kind, spec_mode(spec), engB);
-  const size_t smemB = pair_smem(max_len, engB, wpb, elem_size(spec));
+  const size_t smemB = pair_smem(max_len, engB, wpb, elem_size(spec)) + (size_t)env_int("EKB_NN_XSMEM", 0);
   // With the LB pre-test most pairs are cheap and the first segment's tail of long DPs
   // would idle the GPU, so both segments share one launch.  Without it (MSM, TWE, ...)
   // every pair runs the DP and the second segment waits for the first one's cutoffs.
@@ -927,10 +953,37 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
       CK(cudaEventRecord(g_ctx.ev_chunk[k], g_ctx.copy));
     }
   }
-  if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
-                  dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, dense, o, (double*)(o + n_queries), o + 2 * n_queries,
-                  o + 3 * n_queries, o + 4 * n_queries, st, nch, csz))
-    return -1;
+  // Two candidate halves when the LB path runs on a chunked upload: the first half's search
+  // runs while the second half is still in flight, and its answers seed the second half's
+  // cutoffs (a pair of the second half can only win with a cost below them; ties keep the
+  // first half's lower index), so the second search is mostly key tests.
+  const int halves = (nch >= 2 && share_lb_path(spec, variant, dense, n_cands) && n_cands >= 2048)
+                         ? std::max(1, std::min(2, env_int("EKB_NN_SPLIT", 1))) : 1;
+  if (halves == 1) {
+    if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
+                    dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, dense, o, (double*)(o + n_queries),
+                    o + 2 * n_queries, o + 3 * n_queries, o + 4 * n_queries, st, nch, csz))
+      return -1;
+  } else {
+    const int nc1 = nch / 2;                               // chunks of the first half
+    const int64_t h = std::min<int64_t>(n_cands, nc1 * csz);  // its candidates
+    DBuf dr;
+    if (dr.alloc(sizeof(int64_t) * 10 * (size_t)n_queries, st)) return -1;
+    int64_t* r1 = dr.as<int64_t>();
+    int64_t* r2 = r1 + 5 * n_queries;
+    if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
+                    dco.as<int64_t>(), dcl.as<int32_t>(), h, mx, dense, r1, (double*)(r1 + n_queries),
+                    r1 + 2 * n_queries, r1 + 3 * n_queries, r1 + 4 * n_queries, st, nc1, csz, 0, nullptr))
+      return -1;
+    if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
+                    dco.as<int64_t>() + h, dcl.as<int32_t>() + h, n_cands - h, mx, dense, r2, (double*)(r2 + n_queries),
+                    r2 + 2 * n_queries, r2 + 3 * n_queries, r2 + 4 * n_queries, st, nch - nc1, csz, nc1,
+                    (const double*)(r1 + n_queries)))
+      return -1;
+    if (launch_plain(k_nn_merge, dim3((unsigned)((n_queries + 255) / 256)), dim3(256), 0, st, (long long)n_queries,
+                     (long long)h, (const long long*)r1, (const long long*)r2, (long long*)o))
+      return -1;
+  }
   // one copy back: five result arrays and the validation flag
   std::vector<int64_t> h(5 * n_queries + 1);
   CK(cudaMemcpyAsync(h.data(), o, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, st));

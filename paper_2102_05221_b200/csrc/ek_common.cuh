@@ -164,7 +164,11 @@ EKB_DI R msm_alt(bool between, R c, R dother, R de) {
 // One cell.  D, T, L are the dependency values; the result is the reference's
 // value bit-for-bit whenever the dependencies are.  (For the DTW family the
 // band offset k.off is folded into the cost: cost + 0.0 == cost exactly.)
-template <int KIND, int MODE, bool OFF = true, class R = real_t<MODE>>
+// T_LAST: take the T operand last (the diagonal engine's shuffled operand, so its latency
+// overlaps the first minimum).  The minimum of the three is the same value either way: the
+// first operand D is never NaN for a cell inside the band, values are >= +0 or +inf, and
+// "if a < v" never selects a NaN second operand.
+template <int KIND, int MODE, bool OFF = true, bool T_LAST = false, class R = real_t<MODE>>
 EKB_DI R cell(R D, R T, R L, const RowD<KIND, R>& r, const ColD<KIND, R>& c, const DiagK<KIND, R>& k,
               SlotS<KIND, R>& st, const Params& p) {
   if constexpr (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW) {
@@ -172,8 +176,8 @@ EKB_DI R cell(R D, R T, R L, const RowD<KIND, R>& r, const ColD<KIND, R>& c, con
     R cost = pcost<MODE>(r.x, c.y);
     if constexpr (KIND == K_WDTW) cost = dmul(cost, k.w);
     if constexpr (OFF) cost = dadd(cost, k.off);  // +0.0 in band (exact), +inf outside
-    R m = dmin_ref(D, T);
-    m = dmin_ref(m, L);
+    R m = dmin_ref(D, T_LAST ? L : T);
+    m = dmin_ref(m, T_LAST ? T : L);
     return dadd(m, cost);
   } else if constexpr (KIND == K_ERP) {
     R v = dadd(D, pcost<MODE>(r.x, c.y));

@@ -237,12 +237,21 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   // (and the guard test: a path needs >= P/2 double steps to cross a P-diagonal guard
   // lane) runs half as often
   bool alive = false;
+  // One double step evaluates two whole consecutive anti-diagonals (even slots at t, odd
+  // slots at t+1: d = i - j has the parity of t = i + j), which every path crosses, so
+  // without guards the liveness of every second double step suffices: it is taken in the
+  // voting step only (abandoning moves by at most one double step).
+  auto live_step = [&](int S) { return GUARD || (ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1); };
+  // ROT: the block's series loads address one base per block with compile-time offsets
+  const R* xblk = X.p + I0;
+  const R* yblk = Y.p + J0;
   // CHK: test for the end of the matrix after the step (only the block that can reach it)
   auto dstep = [&](auto S_, auto CHK_) -> bool {
     constexpr int S = decltype(S_)::value;
     constexpr bool CHK = decltype(CHK_)::value;
     constexpr int rx = ROT ? S % (H + 1) : 0;
     constexpr int ry = ROT ? (H - S % H) % H : 0;
+    const bool lv = live_step(S);
     auto XW = [&](int k) -> RowD<KIND, R>& { return xw[(k + rx) % (H + 1)]; };
     auto YW = [&](int m) -> ColD<KIND, R>& { return yw[(m + ry) % H]; };
     // ---- half step A: time t, even slots; cell (I0+m, J0-m) ----
@@ -254,8 +263,9 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     for (int m = 0; m < H; ++m) {
       const int p = 2 * m;
       const R T = (m == 0) ? tin : val[p - 1];
+      // slot 0's T arrives by shuffle: it enters its cell's minimum last
       const R v = (VIRT0 && p != 0) ? cell<KIND, MODE, false>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm)
-                                    : cell<KIND, MODE>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm);
+                                    : cell<KIND, MODE, true, true>(val[p], T, val[p + 1], XW(m), YW(m), kk[p], st[p], prm);
       if constexpr (BORDERED) {
         val[p] = (upd[p] || tb[p] == t) ? v : INF;
       } else if constexpr (COST_MASK) {
@@ -263,7 +273,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       } else {
         val[p] = upd[p] ? v : INF;
       }
-      alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
+      if (lv) alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
     }
     // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
     R lin = __shfl_down_sync(FULL, val[0], 1, W);
@@ -283,7 +293,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       } else {
         val[p] = upd[p] ? v : INF;
       }
-      alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
+      if (lv) alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
     }
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
@@ -318,10 +328,15 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     }
     if constexpr (ROT) {
       // logical xw[H] of the next step is ring slot rx; logical yw[0] is ring slot (ry+H-1)%H
+      // (I0 / J0 are the block's base + S + 1 here)
       const R xprev = XW(H).x;
       const R yprev = YW(0).y;
-      xw[rx] = make_row<KIND, MODE>(X.at(I0 + H - 1), xprev, prm);
-      yw[(ry + H - 1) % H] = make_col<KIND, MODE>(Y.at(J0 - 1), yprev, prm);
+#ifdef EKB_BOUNDS
+      (void)X.at(I0 + H - 1);
+      (void)Y.at(J0 - 1);
+#endif
+      xw[rx] = make_row<KIND, MODE>(xblk[S + H], xprev, prm);
+      yw[(ry + H - 1) % H] = make_col<KIND, MODE>(yblk[S], yprev, prm);
     } else {
 #pragma unroll
       for (int k = 0; k < H; ++k) xw[k] = xw[k + 1];
@@ -345,6 +360,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
           t_load = ld.next_t(dlo, dhi, H);
         }
       }
+      xblk = X.p + I0;
+      yblk = Y.p + J0;
       // blocks that end before anti-diagonal Tf skip the per-step end test
       if (t + 2 * U + 1 < Tf) {
         auto fast = [&](auto S_) { return dstep(S_, std::false_type{}); };

@@ -539,3 +539,22 @@ def test_pairwise_half_warp_stripe(gpu, rng, kind):
     D, _ = gpu.pairwise(spec, Xr)
     Do, _ = eko.pairwise(spec, Xr, threads=8)
     assert np.array_equal(D, Do)
+
+
+@pytest.mark.parametrize("kind,window", [("cdtw", 5), ("dtw", None)])
+def test_nn_candidate_halves_ties_and_seeding(gpu, rng, kind, window, monkeypatch):
+    """ek_nn from host arrays splits a large LB-path search into two candidate halves (the
+    second seeded with the first's answers): an exact duplicate across the halves resolves
+    to the lower index, a neighbour only in the second half is found, and everything equals
+    the oracle's serial scan."""
+    L, n = 40, 4096
+    C = np.cumsum(rng.normal(size=(n, L)), axis=1)
+    C[3000] = C[100]  # duplicate across the halves: index 100 must win
+    Q = np.stack([C[100] + 1e-3, C[3500] + 1e-3, C[2047] + 2e-3, rng.normal(size=L).cumsum()])
+    spec = gpu.DistanceSpec(kind=kind, window=window)
+    monkeypatch.setenv("EKB_NN_SPLIT", "2")  # read per call by the library (default 1: measured slower on C2)
+    for variant in ("eapruned", "ea"):
+        idx, dist = gpu.nn_batch(spec, variant, Q, C)[:2]
+        r = eko.nn(spec, variant, Q, C, threads=16)
+        assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"]), (idx, r["nn_index"])
+        assert idx[0] == 100 and idx[1] == 3500
