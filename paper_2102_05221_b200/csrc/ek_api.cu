@@ -223,6 +223,19 @@ __global__ void k_nn_merge(long long nq, long long h, const long long* r1, const
   }
 }
 
+// offsets / lengths of dense contiguous batches (series k at k * len)
+__global__ void k_dense_layout(long long nq, long long nc, int len, long long* qo, int* ql, long long* co, int* cl) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nq + nc; i += (long long)gridDim.x * blockDim.x) {
+    if (i < nq) {
+      qo[i] = i * len;
+      ql[i] = len;
+    } else {
+      co[i - nq] = (i - nq) * len;
+      cl[i - nq] = len;
+    }
+  }
+}
+
 // p[0..n) = v, p[n] = 0
 __global__ void k_fill_i32(int* p, long long n, int v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x)
@@ -917,9 +930,6 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
       dc.alloc(sizeof(double) * c_total, st) || dco.alloc(8 * std::max<int64_t>(1, n_cands), st) ||
       dcl.alloc(4 * std::max<int64_t>(1, n_cands), st) || dout.alloc(8 * (5 * n_queries + 1), st))
     return -1;
-  CK(cudaMemcpyAsync(dq.p, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dqo.p, q_off, 8 * n_queries, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dql.p, ql.data(), 4 * n_queries, cudaMemcpyHostToDevice, st));
   // on every exit the copy stream is drained before the buffers above are released
   struct CopyDrain {
     ~CopyDrain() { cudaStreamSynchronize(g_ctx.copy); }
@@ -927,21 +937,24 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   int64_t* o = dout.as<int64_t>();
   int* bad = (int*)(o + 5 * n_queries);  // validation flag rides with the results
   CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  if (check_finite(dq.as<double>(), q_total, bad, st)) return -1;
-  // Candidates: offsets and lengths first, then the values in chunks on the copy stream,
+  CK(cudaEventRecord(g_ctx.ev_fork, st));  // dc / bad allocated and zeroed in stream order
+  // dense batches stored contiguously: offsets and lengths are generated on the device
+  bool qcontig = dense != 0, ccontig = dense != 0;
+  for (int64_t k = 0; k < n_queries && qcontig; ++k) qcontig = q_off[k] == k * (int64_t)mx;
+  for (int64_t k = 0; k < n_cands && ccontig; ++k) ccontig = c_off[k] == k * (int64_t)mx;
+  // Candidates first (the bulk of the bytes): the values in chunks on the copy stream,
   // each checked for finiteness there and announced by an event, so the LB keys of early
   // chunks are computed while later ones are still in flight (dense batches: chunk k is
   // series [k * csz, (k + 1) * csz), contiguous in the buffer).
   int nch = 0;
   int64_t csz = n_cands;
+  // the queries go first on the same copy stream (1/16 of C2's bytes): the LB keys of each
+  // candidate chunk need them
+  CK(cudaStreamWaitEvent(g_ctx.copy, g_ctx.ev_fork, 0));
+  CK(cudaMemcpyAsync(dq.p, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, g_ctx.copy));
+  CK(cudaEventRecord(g_ctx.ev_join, g_ctx.copy));
   if (n_cands > 0) {
-    CK(cudaMemcpyAsync(dco.p, c_off, 8 * n_cands, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dcl.p, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
-    CK(cudaEventRecord(g_ctx.ev_fork, st));  // dc / bad allocated and zeroed in stream order
-    CK(cudaStreamWaitEvent(g_ctx.copy, g_ctx.ev_fork, 0));
-    bool contiguous = dense != 0;
-    for (int64_t k = 0; k < n_cands && contiguous; ++k) contiguous = c_off[k] == k * (int64_t)mx;
-    nch = (contiguous && n_cands >= 2 * Ctx::kChunks) ? std::max(1, std::min(Ctx::kChunks, env_int("EKB_NN_CHUNKS", 4))) : 1;
+    nch = (ccontig && n_cands >= 2 * Ctx::kChunks) ? std::max(1, std::min(Ctx::kChunks, env_int("EKB_NN_CHUNKS", 4))) : 1;
     csz = (n_cands + nch - 1) / nch;
     for (int k = 0; k < nch; ++k) {
       const int64_t b = std::min<int64_t>(c_total, nch == 1 ? 0 : k * csz * mx);
@@ -953,6 +966,20 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
       CK(cudaEventRecord(g_ctx.ev_chunk[k], g_ctx.copy));
     }
   }
+  CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the queries have landed
+  if (qcontig && ccontig) {
+    if (launch_plain(k_dense_layout, dim3(16), dim3(256), 0, st, (long long)n_queries, (long long)n_cands, (int)mx,
+                     (long long*)dqo.p, (int*)dql.p, (long long*)dco.p, (int*)dcl.p))
+      return -1;
+  } else {
+    CK(cudaMemcpyAsync(dqo.p, q_off, 8 * n_queries, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dql.p, ql.data(), 4 * n_queries, cudaMemcpyHostToDevice, st));
+    if (n_cands > 0) {
+      CK(cudaMemcpyAsync(dco.p, c_off, 8 * n_cands, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(dcl.p, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
+    }
+  }
+  if (check_finite(dq.as<double>(), q_total, bad, st)) return -1;
   // Two candidate halves when the LB path runs on a chunked upload: the first half's search
   // runs while the second half is still in flight, and its answers seed the second half's
   // cutoffs (a pair of the second half can only win with a cost below them; ties keep the

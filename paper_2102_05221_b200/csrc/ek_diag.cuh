@@ -238,10 +238,13 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   // lane) runs half as often
   bool alive = false;
   // One double step evaluates two whole consecutive anti-diagonals (even slots at t, odd
-  // slots at t+1: d = i - j has the parity of t = i + j), which every path crosses, so
-  // without guards the liveness of every second double step suffices: it is taken in the
-  // voting step only (abandoning moves by at most one double step).
-  auto live_step = [&](int S) { return GUARD || (ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1); };
+  // slots at t+1: d = i - j has the parity of t = i + j), which every path crosses, so the
+  // liveness of every second double step suffices: it is taken in the voting step only
+  // (abandoning moves by at most one double step).  Guards: a path crossing a guard lane
+  // visits its P >= 4 diagonals at >= 4 distinct anti-diagonals, and consecutive cells of
+  // a path are at most 2 anti-diagonals apart, so it has a live cell in the lane in >= 2
+  // consecutive double steps, one of which votes.
+  auto live_step = [&](int S) { return ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1; };
   // ROT: the block's series loads address one base per block with compile-time offsets
   const R* xblk = X.p + I0;
   const R* yblk = Y.p + J0;

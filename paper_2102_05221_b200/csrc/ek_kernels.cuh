@@ -470,7 +470,13 @@ struct LazyCand {
 #define EKB_NN_DTW_MINB 5  // measured: 96 registers without spills, C2 phase B -1%
 #endif
 // min resident blocks for the dtw/cdtw diagonal 1-NN kernels (0: the compiler's choice)
-__host__ __device__ constexpr int nn_minb(int kind, int eng) { return (kind == K_DTW && eng == E_DIAG4) ? EKB_NN_DTW_MINB : 0; }
+#ifndef EKB_NN_GUARD_MINB
+#define EKB_NN_GUARD_MINB 0  // MSM / TWE guarded P=4 band (C4 phase B): 0 = the compiler's choice
+#endif
+__host__ __device__ constexpr int nn_minb(int kind, int eng) {
+  return (kind == K_DTW && eng == E_DIAG4) ? EKB_NN_DTW_MINB
+         : ((kind == K_MSM || kind == K_TWE) && eng == E_GDIAG4) ? EKB_NN_GUARD_MINB : 0;
+}
 
 template <int KIND, int MODE, int ENG>
 __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __restrict__ Q, const long long* __restrict__ qoff,

@@ -122,7 +122,10 @@ def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None
                                                                              for _ in range(3)]
     if nq == 0:
         return tuple(out)
-    longest = np.unique(np.maximum.outer(np.unique(ql), np.unique(cl)))
+    if spec.kind == "wdtw":
+        longest = np.unique(np.maximum.outer(np.unique(ql), np.unique(cl)))
+    else:
+        longest = ()  # only WDTW needs per-length tables
     h = _lib.SpecHandle(spec, longest_lengths=longest, precision=precision)
     L = _lib.lib()
     _lib.check(L.ek_nn(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(qf), len(qf), _lib.iptr(qo), _lib.iptr(ql), nq,
