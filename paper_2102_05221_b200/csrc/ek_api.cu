@@ -688,10 +688,23 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   ParamHolder ph;
   if (ph.init(spec, st)) return -1;
   const long long npairs = (long long)nq * ncand;
-  DBuf dord, dkeys, dskeys, dout, dtend, dcut, dcnt, denv, denvq, denvs;
-  if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dout.alloc(sizeof(double) * (size_t)npairs, st) ||
-      dtend.alloc(sizeof(int) * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
+  DBuf dord, dkeys, dskeys, dacc, dfin, dcut, dcnt, denv, denvq, denvs;
+  // result accumulators (NNAcc): best u64 / cells i64 / computed i32 / idx i32 per query,
+  // the finite-result list (q << 32 | c, cost) and its count
+  if (dord.alloc(sizeof(int) * (size_t)npairs, st) || dacc.alloc(24 * (size_t)nq + 16, st) ||
+      dfin.alloc(16 * (size_t)npairs, st) || dcut.alloc(sizeof(unsigned long long) * (size_t)nq, st) ||
       dcnt.alloc(sizeof(int) * 128, st))
+    return -1;
+  NNAcc acc;
+  acc.best = dacc.as<unsigned long long>();
+  acc.cells = (long long*)(acc.best + nq);
+  acc.computed = (int*)(acc.cells + nq);
+  acc.idx = acc.computed + nq;
+  acc.fin_count = acc.idx + nq;
+  acc.fin = dfin.as<long long>();
+  acc.fin_cost = (double*)(acc.fin + npairs);
+  if (launch_plain(k_nn_acc_init, dim3((unsigned)std::min<long long>(64, (nq + 255) / 256)), dim3(256), 0, st, acc,
+                   (int)nq))
     return -1;
   // ints 8, 9: guarded-band overflows and their redo counter; 32 / 64 / 96: the k_nn work
   // counters (kNnCounters x u64) of phase A and of phase B's launches
@@ -758,9 +771,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       if (launch_plain(k_identity_order, dim3(1024), dim3(256), 0, st, (int)nq, (int)ncand, dord.as<int>())) return -1;
       CK(cudaMemcpyAsync(dskeys.p, dkeys.p, sizeof(float) * (size_t)npairs, cudaMemcpyDeviceToDevice, st));
     }
-    if (launch_plain(k_fill_nn_out, dim3(592), dim3(256), 0, st, dout.as<double>(), dtend.as<int>(), npairs))
-      return -1;
-    g_launches += 4;
+    g_launches += 3;
   } else if (rank) {
     if (dkeys.alloc(sizeof(float) * (size_t)npairs, st)) return -1;
     // FP32 Euclidean distance between piecewise aggregates (segments of 4 points)
@@ -818,7 +829,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
                           (const int*)dord.as<int>(), 0, ka, ka, 1, 1, win, (int)max_len, ph.prm, (int)share,
-                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 32,
+                          dcut.as<unsigned long long>(), acc, dcnt.as<int>() + 32,
                           (const float*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count, (int*)nullptr))
       return -1;
   }
@@ -858,7 +869,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     if (launch_persistent(fseg, 32 * wpb, smseg, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
                           (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), lo, mid,
                           hi, K1, K2, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
-                          dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 64 + 32 * sgi,
+                          acc, dcnt.as<int>() + 64 + 32 * sgi,
                           (const float*)(use_lb ? dskeys.as<float>() : nullptr),
                           (const float2*)denvq.as<float2>(), seg1_wide ? dovf2.as<int2>() : dovf.as<int2>(),
                           seg1_wide ? ovf2_count : ovf_count, (use_lb && ncand <= 16384) ? dqstop.as<int>() : (int*)nullptr))
@@ -882,17 +893,16 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       int* cnt = from2 ? ovf2_count : ovf_count;
       if (launch_persistent(ff, 32 * fwpb, fsmem, st, npairs, dQ, (const long long*)dqoff, (const int*)dqlen, dC,
                             (const long long*)dcoff, (const int*)dclen, (int)ncand, lst, (const int*)cnt, win,
-                            (int)max_len, fprm, dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
+                            (int)max_len, fprm, dcut.as<unsigned long long>(), acc,
                             cnt + 1, dovf2.as<int2>(), ovf2_count))
         return -1;
     }
     mark(st, "nn_fix");
   }
   // 4. lexicographic (distance, index) minimum + accounting
-  if (launch_plain(k_nn_reduce, dim3((unsigned)nq), dim3(256), 0, st, (const double*)dout.as<double>(),
-                   (const int*)dtend.as<int>(), (const int*)dqlen, (int)nq, (const int*)dclen, (int)ncand, win,
-                   (int)engine_is_diag(eng), eng_S(eng), kind_tag(spec->kind) == K_ERP ? 0 : 1,
-                   (long long*)d_idx, d_dist, (long long*)d_cells, (long long*)d_comp, (long long*)d_ab))
+  if (launch_plain(k_nn_pick, dim3(148), dim3(256), 0, st, acc) ||
+      launch_plain(k_nn_final, dim3((unsigned)std::min<long long>(64, (nq + 255) / 256)), dim3(256), 0, st, acc, (int)nq,
+                   (int)ncand, (long long*)d_idx, d_dist, (long long*)d_cells, (long long*)d_comp, (long long*)d_ab))
     return -1;
   mark(st, "reduce");
   return 0;

@@ -4,7 +4,7 @@
 //                 _speedups.run / engines.distance (engines.py:121-147)
 //   k_triangle  : the all-pairs upper triangle, mirrored
 //   k_nn        : 1-NN search with a per-query shared cutoff (search.py:81-160)
-//   (k_subseq in ek_subseq.cuh, k_nn_reduce in ek_misc.cu)
+//   (k_subseq in ek_subseq.cuh, the 1-NN result pick k_nn_pick / k_nn_final in ek_misc.cu)
 //
 // All kernels are warp-per-pair and persistent (grid = SM count x resident
 // blocks, work claimed with an atomic counter).  Series are staged into padded
@@ -430,6 +430,32 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
 
 // ---- 1-NN with a shared per-query cutoff -----------------------------------------
 
+// 1-NN results, accumulated on the fly instead of a per-pair Q x C matrix: per query the
+// least finite cost (IEEE image: values are >= +0, so the bits order as integers), the
+// count of finite results and the evaluated cells; the finite results themselves go to an
+// append-only list, from which the lowest index among equal minima is picked after the
+// search (k_nn_pick / k_nn_final, ek_misc.cu).  Every result with cost <= the final cutoff
+// is exact, so that is nn_search's answer (strict "<", lowest index) whatever the schedule.
+struct NNAcc {
+  unsigned long long* best;  // [nq]
+  long long* cells;          // [nq]
+  int* computed;             // [nq]
+  int* idx;                  // [nq] lowest index of the least cost (k_nn_pick)
+  long long* fin;            // [cap] q << 32 | c of each finite result
+  double* fin_cost;          // [cap]
+  int* fin_count;
+};
+// lane 0: one pair's result
+__device__ __forceinline__ void nn_publish(const NNAcc& a, int q, int c, double cost) {
+  if (cost < EKB_INF) {
+    atomicMin(a.best + q, (unsigned long long)__double_as_longlong(cost));
+    const int k = atomicAdd(a.fin_count, 1);
+    a.fin[k] = ((long long)q << 32) | (unsigned)c;
+    a.fin_cost[k] = cost;
+    atomicAdd(a.computed + q, 1);
+  }
+}
+
 constexpr int kChunk = 128;  // candidate staging granule (4 doubles per lane)
 constexpr int kNnCounters = 8;  // k_nn work counters (64-bit each)
 
@@ -484,8 +510,7 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
                                             const long long* __restrict__ coff, const int* __restrict__ clen,
                                             int ncand, const int* __restrict__ order, int rank_lo, int rank_mid,
                                             int rank_hi, int K1, int K2, int win, int lmax, Params prm, int share,
-                                            unsigned long long* cutbits, double* __restrict__ out,
-                                            int* __restrict__ tend_out, int* __restrict__ counter,
+                                            unsigned long long* cutbits, NNAcc acc, int* __restrict__ counter,
                                             const float* __restrict__ skeys, const float2* __restrict__ envq,
                                             int2* __restrict__ ovf_list, int* __restrict__ ovf_count,
                                             int* __restrict__ qstop) {
@@ -604,6 +629,7 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
       for (int u = 0; u < PF; ++u) pf[u] = (u * 32 + lane < lc) ? __ldg(s + u * 32 + lane) : 0.0;
     }
     __syncwarp();
+    long long icells = 0;  // this item's evaluated cells (one atomic per item)
     while (todo) {
       const int i = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -678,10 +704,11 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
           ovf_list[atomicAdd(ovf_count, 1)] = make_int2(q, c);
           cost = EKB_INF;
         }
-        out[(long long)q * ncand + c] = cost;
-        tend_out[(long long)q * ncand + c] = cells;
+        nn_publish(acc, q, c, cost);
+        icells += cells;
       }
     }
+    if (lane == 0 && icells) atomicAdd((unsigned long long*)acc.cells + q, (unsigned long long)icells);
   }
 #ifdef EKB_TRACE
   if (lane == 0) {
@@ -708,8 +735,7 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
                                                 const long long* __restrict__ coff, const int* __restrict__ clen,
                                                 int ncand, const int2* __restrict__ list,
                                                 const int* __restrict__ count, int win, int lmax, Params prm,
-                                                unsigned long long* cutbits, double* __restrict__ out,
-                                                int* __restrict__ tend_out, int* __restrict__ counter,
+                                                unsigned long long* cutbits, NNAcc acc, int* __restrict__ counter,
                                                 int2* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   extern __shared__ double smem[];
   constexpr int PAD = engine_pad(ENG);
@@ -751,8 +777,8 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
         cost = EKB_INF;
       }
       if (cost < EKB_INF) atomicMin(cutbits + q, (unsigned long long)__double_as_longlong(cost));
-      out[(long long)q * ncand + c] = cost;
-      tend_out[(long long)q * ncand + c] = cells;
+      nn_publish(acc, q, c, cost);
+      if (cells) atomicAdd((unsigned long long*)acc.cells + q, (unsigned long long)cells);
     }
   }
 }

@@ -11,9 +11,9 @@ using TriFn = void (*)(const double*, const long long*, const int*, int, int, in
                       long long, double*, unsigned long long*, int*);
 using NNFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,
                       const int*, int, const int*, int, int, int, int, int, int, int, Params, int, unsigned long long*,
-                      double*, int*, int*, const float*, const float2*, int2*, int*, int*);
+                      NNAcc, int*, const float*, const float2*, int2*, int*, int*);
 using NNFixFn = void (*)(const double*, const long long*, const int*, const double*, const long long*, const int*,
-                         int, const int2*, const int*, int, int, Params, unsigned long long*, double*, int*, int*,
+                         int, const int2*, const int*, int, int, Params, unsigned long long*, NNAcc, int*,
                          int2*, int*);
 using RefFn = void (*)(const double*, const PairDesc*, int, int, Params, double*, long long*);
 using UBFn = void (*)(const double*, const long long*, const int*, int, const double*, const long long*,

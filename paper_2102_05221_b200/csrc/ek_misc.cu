@@ -242,13 +242,6 @@ cudaError_t lb_matrix(int mode, const float2* qt, int nq, const float2* envp, in
   return cudaGetLastError();
 }
 
-__global__ void k_fill_nn_out(double* __restrict__ out, int* __restrict__ tend, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    out[i] = __longlong_as_double(0x7ff0000000000000LL);
-    tend[i] = 0;
-  }
-}
-
 // Per query: stable block radix sort of (key, candidate) -> ranked candidate order
 // (ties keep index order).  THREADS x ITEMS >= ncand; padding sorts last.
 template <int THREADS, int ITEMS>
@@ -338,54 +331,36 @@ __global__ void k_identity_order(int nq, int ncand, int* __restrict__ order) {
     order[i] = (int)(i % ncand);
 }
 
-// nn_search's outcome per query (search.py:101-123): lowest index among the
-// minimal distances -- the serial scan's strict "<" keeps the first one.
-__global__ void __launch_bounds__(256) k_nn_reduce(const double* __restrict__ dist, const int* __restrict__ tend,
-                                                   const int* __restrict__ qlen, int nq, const int* __restrict__ clen,
-                                                   int ncand, int win, int eng_diag, int S, int r0,
-                                                   long long* __restrict__ nn_idx, double* __restrict__ nn_dist,
-                                                   long long* __restrict__ cells, long long* __restrict__ computed,
-                                                   long long* __restrict__ abandoned) {
-  const int q = blockIdx.x;
-  double bd = __longlong_as_double(0x7ff0000000000000LL);
-  int bi = 0x7fffffff;
-  long long nc_ = 0, ab = 0, cl = 0;
-  for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
-    const double d = dist[(long long)q * ncand + c];
-    cl += tend[(long long)q * ncand + c];  // per-pair evaluated cells (k_nn)
-    if (d < __longlong_as_double(0x7ff0000000000000LL)) {
-      ++nc_;
-      if (d < bd || (d == bd && c < bi)) { bd = d; bi = c; }
-    } else {
-      ++ab;
-    }
+// nn_search's outcome per query (search.py:101-123) from the accumulators of k_nn
+// (NNAcc): the lowest index among the finite results equal to the query's least cost --
+// the serial scan's strict "<" keeps the first one.
+__global__ void k_nn_pick(NNAcc a) {
+  const int n = *a.fin_count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const long long qc = a.fin[k];
+    const int q = (int)(qc >> 32), c = (int)(qc & 0xffffffffLL);
+    if ((unsigned long long)__double_as_longlong(a.fin_cost[k]) == a.best[q]) atomicMin(a.idx + q, c);
   }
-  __shared__ double sd[256];
-  __shared__ int si[256];
-  __shared__ long long s1[256], s2[256], s3[256];
-  sd[threadIdx.x] = bd; si[threadIdx.x] = bi;
-  s1[threadIdx.x] = nc_; s2[threadIdx.x] = ab; s3[threadIdx.x] = cl;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const double od = sd[threadIdx.x + s];
-      const int oi = si[threadIdx.x + s];
-      if (od < sd[threadIdx.x] || (od == sd[threadIdx.x] && oi < si[threadIdx.x])) {
-        sd[threadIdx.x] = od; si[threadIdx.x] = oi;
-      }
-      s1[threadIdx.x] += s1[threadIdx.x + s];
-      s2[threadIdx.x] += s2[threadIdx.x + s];
-      s3[threadIdx.x] += s3[threadIdx.x + s];
-    }
-    __syncthreads();
+}
+__global__ void k_nn_final(NNAcc a, int nq, int ncand, long long* __restrict__ nn_idx, double* __restrict__ nn_dist,
+                           long long* __restrict__ cells, long long* __restrict__ computed,
+                           long long* __restrict__ abandoned) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    const int i = a.idx[q];
+    nn_idx[q] = i == 0x7fffffff ? -1 : i;
+    nn_dist[q] = __longlong_as_double((long long)a.best[q]);
+    cells[q] = a.cells[q];
+    computed[q] = a.computed[q];
+    abandoned[q] = ncand - a.computed[q];
   }
-  if (threadIdx.x == 0) {
-    const bool found = si[0] != 0x7fffffff;
-    nn_idx[q] = found ? si[0] : -1;
-    nn_dist[q] = sd[0];
-    cells[q] = s3[0];
-    computed[q] = s1[0];
-    abandoned[q] = s2[0];
+}
+__global__ void k_nn_acc_init(NNAcc a, int nq) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    a.best[q] = 0x7ff0000000000000ULL;
+    a.cells[q] = 0;
+    a.computed[q] = 0;
+    a.idx[q] = 0x7fffffff;
+    if (q == 0) *a.fin_count = 0;
   }
 }
 

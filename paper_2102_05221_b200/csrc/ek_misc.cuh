@@ -33,12 +33,12 @@ cudaError_t lb_qprep(int mode, const double* Q, const long long* qoff, int nq, i
 cudaError_t lb_matrix(int mode, const float2* qt, int nq, const float2* envp, int ncand, int c_begin, int c_end, int L,
                       float* out, cudaStream_t st);
 // out[i] = +inf, tend[i] = 0 (pairs the LB path never visits)
-__global__ void k_fill_nn_out(double* out, int* tend, long long n);
 __global__ void k_paa(const double* src, const long long* off, const int* len, int n, int R, int D, float* dst);
 __global__ void k_rank_paa(const float* Qp, int nq, const float* Cp, int ncand, int D, float* out);
 __global__ void k_identity_order(int nq, int ncand, int* order);
-__global__ void k_nn_reduce(const double* dist, const int* tend, const int* qlen, int nq, const int* clen, int ncand,
-                            int win, int eng_diag, int S, int r0, long long* nn_idx, double* nn_dist,
-                            long long* cells, long long* computed, long long* abandoned);
+__global__ void k_nn_pick(NNAcc a);
+__global__ void k_nn_final(NNAcc a, int nq, int ncand, long long* nn_idx, double* nn_dist, long long* cells,
+                           long long* computed, long long* abandoned);
+__global__ void k_nn_acc_init(NNAcc a, int nq);
 
 }  // namespace ekb
