@@ -502,6 +502,25 @@ def parity_vs(ref, runner):
                                                                     np.float64(d).view(np.int64))}
 
 
+DOMINANT_KERNEL = {"c1": "k_nn", "c2": "k_nn", "c4m": "k_nn", "c4t": "k_nn", "c3w": "k_triangle",
+                   "c3e": "k_triangle", "c5": "k_subseq_lb"}
+
+
+def ncu_traffic(name):
+    """(dram bytes per launch, source) of the config's dominant kernel, newest profiles/ summary."""
+    import glob
+
+    if name.endswith("_fp32"):
+        return None
+    profs = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_ncu_{name}_{DOMINANT_KERNEL[name]}*.json")))
+    if not profs:
+        return None
+    try:
+        return json.load(open(profs[-1])).get("dram_bytes_per_launch"), os.path.relpath(profs[-1], REPO)
+    except (OSError, ValueError):
+        return None
+
+
 def run_ours(args):
     import torch
 
@@ -604,16 +623,11 @@ def run_ours(args):
     }
     if "e2e" in head:
         line["e2e"] = head["e2e"]
-    # dram bytes per launch of the dominant kernel from the committed `ncu --set full` summary
-    import glob
-
-    profs = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_ncu_{args.config}_*.json")))
-    if profs:
-        try:
-            line["roofline"]["traffic"] = json.load(open(profs[-1])).get("dram_bytes_per_launch")
-            line["roofline"]["traffic_source"] = os.path.relpath(profs[-1], REPO)
-        except (OSError, ValueError):
-            pass
+    # dram bytes per launch of the dominant kernel from the committed `ncu --set full` summaries
+    for name, res in results.items():
+        tr = ncu_traffic(name)
+        if tr:
+            res["roofline"]["traffic"], res["roofline"]["traffic_source"] = tr
     for key in ("cpu_baseline", "parity"):
         if key in head:
             line[key] = head[key]

@@ -1271,8 +1271,19 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   }
   mark(st, "envelope");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
-  const int wpb = 8;
-  const size_t smem = sizeof(double) * ((size_t)subseq_qslot((int)lq, eng) + wpb * (size_t)subseq_warp((int)lq, eng));
+  // warps per block: 8, fewer for long queries (the normalised query once per block, one
+  // staged window per warp); a query beyond one warp's shared memory is refused
+  int wpb = 8;
+  auto ss_smem = [&](int k) {
+    return sizeof(double) * ((size_t)subseq_qslot((int)lq, eng) + k * (size_t)subseq_warp((int)lq, eng));
+  };
+  while (wpb > 1 && ss_smem(wpb) > 220 * 1024) --wpb;
+  if (ss_smem(wpb) > 226 * 1024) return fail("query length %lld exceeds this build's subsequence engines", (long long)lq);
+  const size_t smem = ss_smem(wpb);
+  // long queries (strip engines): per-warp boundary columns in global scratch
+  Params sprm{};
+  DBuf dstrip;
+  if (strip_scratch(fn, eng, 32 * wpb, smem, (int)lq, sprm, dstrip, st)) return -1;
   const double* qn_ = dqn.as<double>();
   if (ns > 0) {
     DBuf dso, dst;
@@ -1280,7 +1291,8 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     if (launch_persistent(fn, 32 * wpb, smem, st, ns, qn_, (int)lq, dref, (int)normalize, wst,
                           (const long long*)dseed.as<long long>(), (const float*)nullptr, ns, (const int*)nullptr, 0,
                           win, (int)share,
-                          dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>()))
+                          dcut.as<unsigned long long>(), dso.as<double>(), dst.as<int>(), dcnt.as<int>(),
+                          sprm.strip_buf, sprm.strip_stride))
       return -1;
   }
   mark(st, "subseq_phaseA");
@@ -1310,13 +1322,14 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                           (const long long*)dsurv.as<long long>(), (const float*)dsurvlb.as<float>(), nwin,
                           (const int*)dns.as<int>(), 1, win,
                           (int)share, dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(),
-                          dcnt.as<int>() + 4))
+                          dcnt.as<int>() + 4, sprm.strip_buf, sprm.strip_stride))
       return -1;
   } else {
     if (launch_persistent(fn, 32 * wpb, smem, st, (nwin + 31) / 32, qn_, (int)lq, dref, (int)normalize, wst,
                           (const long long*)nullptr, (const float*)nullptr, nwin, (const int*)nullptr, 0, win,
                           (int)share,
-                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2))
+                          dcut.as<unsigned long long>(), dout.as<double>(), dtend.as<int>(), dcnt.as<int>() + 2,
+                          sprm.strip_buf, sprm.strip_stride))
       return -1;
   }
   mark(st, "subseq_phaseB");

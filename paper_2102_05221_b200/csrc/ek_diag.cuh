@@ -39,6 +39,12 @@ namespace ekb {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifdef EKB_LIVE
+// debug builds: in-matrix band cells the diagonal engine evaluated, and those of them that
+// were live (value <= the cutoff in force) -- the share EAPruned's column pruning would skip
+__device__ unsigned long long g_live[2];
+#endif
+
 #ifndef EKB_DBOUND
 #define EKB_DBOUND 1  // MSM / TWE diagonal-distance bound in the liveness test
 #endif
@@ -226,6 +232,9 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   set_thr(cut64);
   bool dead = false;
   bool ovf = false;
+#ifdef EKB_LIVE
+  unsigned long long lv_ev = 0, lv_n = 0;
+#endif
 
   // One double step.  With ROT the register windows are rings whose rotation
   // (rx for xw, ry for yw) is a compile-time function of the unrolled step S,
@@ -277,6 +286,12 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
         val[p] = upd[p] ? v : INF;
       }
       if (lv) alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
+#ifdef EKB_LIVE
+      if (upd[p] && I0 + m >= 1 && I0 + m <= nl && J0 - m >= 1 && J0 - m <= nc) {
+        ++lv_ev;
+        lv_n += val[p] <= cut;
+      }
+#endif
     }
     // ---- half step B: time t+1, odd slots; cell (I0+m+1, J0-m) ----
     R lin = __shfl_down_sync(FULL, val[0], 1, W);
@@ -297,6 +312,12 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
         val[p] = upd[p] ? v : INF;
       }
       if (lv) alive |= hi_word(val[p]) <= (DBOUND ? thr_hi[DBOUND ? p : 0] : cut_hi);
+#ifdef EKB_LIVE
+      if (upd[p] && I0 + m + 1 >= 1 && I0 + m + 1 <= nl && J0 - m >= 1 && J0 - m <= nc) {
+        ++lv_ev;
+        lv_n += val[p] <= cut;
+      }
+#endif
     }
     // the final cell (nl, nc) is on anti-diagonal Tf: if Tf == t it sits in an even
     // slot, which half step B (odd slots) leaves untouched
@@ -385,6 +406,16 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     }
   }
 
+#ifdef EKB_LIVE
+  for (int o = W / 2; o; o >>= 1) {
+    lv_ev += __shfl_xor_sync(FULL, lv_ev, o, W);
+    lv_n += __shfl_xor_sync(FULL, lv_n, o, W);
+  }
+  if (lane == 0) {
+    atomicAdd(&g_live[0], lv_ev);
+    atomicAdd(&g_live[1], lv_n);
+  }
+#endif
   DiagResult res;
   res.t_end = (dead || ovf) ? t + 1 : Tf;  // last anti-diagonal evaluated
   res.ovf = ovf;

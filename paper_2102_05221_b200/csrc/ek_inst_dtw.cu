@@ -11,3 +11,12 @@ extern "C" int ek_debug_trace(unsigned long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, ekb::g_trace, sizeof(unsigned long long) * n);
 }
 #endif
+
+#ifdef EKB_LIVE
+// debug builds: the evaluated / live cell counters of this unit's diagonal engines (reset on read)
+extern "C" int ek_debug_live_dtw(unsigned long long* out) {
+  int e = (int)cudaMemcpyFromSymbol(out, ekb::g_live, 2 * sizeof(unsigned long long));
+  const unsigned long long z[2] = {0, 0};
+  return e | (int)cudaMemcpyToSymbol(ekb::g_live, z, sizeof z);
+}
+#endif

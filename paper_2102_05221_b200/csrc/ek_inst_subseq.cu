@@ -10,7 +10,9 @@ namespace ekb {
   case (M)*16 + E_STR4: return k_subseq<M, E_STR4>;                       \
   case (M)*16 + E_STR8: return k_subseq<M, E_STR8>;                       \
   case (M)*16 + E_STR16: return k_subseq<M, E_STR16>;                     \
-  case (M)*16 + E_STRB16: return k_subseq<M, E_STRB16>;
+  case (M)*16 + E_STRB16: return k_subseq<M, E_STRB16>;                   \
+  case (M)*16 + E_STRIP16: return k_subseq<M, E_STRIP16>;                 \
+  case (M)*16 + E_STRIPB16: return k_subseq<M, E_STRIPB16>;
 
 SubseqFn get_subseq(int mode, int eng) {
   switch (mode * 16 + eng) {

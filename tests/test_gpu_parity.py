@@ -558,3 +558,27 @@ def test_nn_candidate_halves_ties_and_seeding(gpu, rng, kind, window, monkeypatc
         r = eko.nn(spec, variant, Q, C, threads=16)
         assert np.array_equal(idx, r["nn_index"]) and np.array_equal(dist, r["nn_distance"]), (idx, r["nn_index"])
         assert idx[0] == 100 and idx[1] == 3500
+
+
+@pytest.mark.parametrize("lq,window,norm", [(600, None, True), (1024, None, False), (700, 300, True),
+                                             (513, None, True)])
+def test_subseq_long_query_strip_engines(gpu, rng, lq, window, norm):
+    """Queries longer than one 512-column row stripe: unbanded DTW and wide-band CDTW run the
+    strip engines inside the subsequence kernel (search.py:163-215 takes any length).  The
+    best window equals the oracle's; a planted copy is found."""
+    stream = np.cumsum(rng.normal(size=lq + 1400))
+    q = stream[901:901 + lq] + rng.normal(0, 1e-3, size=lq)
+    spec = gpu.DistanceSpec(kind="cdtw" if window is not None else "dtw", window=window)
+    got = gpu.subsequence_search(q, stream, gpu.SearchConfig(spec=spec, variant="eapruned", normalize=norm))[:2]
+    want = eko.subsequence(spec, "eapruned", q, stream, norm, chunk=256, threads=16)[:2]
+    assert got == want and got[0] == 901, (got, want)
+
+
+def test_subseq_profile_long_query(gpu, rng):
+    """Every window's exact distance for a 600-point unbanded DTW query (strip engine)."""
+    stream = np.cumsum(rng.normal(size=760))
+    q = np.cumsum(rng.normal(size=600))
+    spec = gpu.DistanceSpec(kind="dtw")
+    prof = gpu.subsequence_profile(q, stream, spec, normalize=True)
+    want = eko.subsequence_profile(spec, q, stream, True, threads=16)
+    assert np.array_equal(np.asarray(prof), want)
