@@ -15,6 +15,7 @@
 #include "../../include/elastik_b200.h"
 #include "ek_launch.cuh"
 #include "ek_misc.cuh"
+#include "ek_nn2.cuh"
 #include "ek_subseq.cuh"
 
 namespace ekb {
@@ -731,6 +732,15 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   //      for the survivors' reverse bound on a side stream.  Otherwise an approximate
   //      Euclidean ranking.  The order is a schedule only: it never decides a result.
   const bool rank = share && ncand <= 16384 && ncand > 1;
+  // Two pairs per warp (k_nn2) when the band fits one half-warp's 16 x 8 slots: the series
+  // are read through L1 from padded copies made here (queries once, candidates per chunk)
+  const bool use_nn2 = use_lb && kind_tag(spec->kind) == K_DTW && ncand <= 16384 &&
+                       diag_slots_needed(max_len, max_len, wmax) <= 128 && env_int("EKB_NN2", 1) != 0;
+  const int pitch2 = max_len + 2 * kPadG;
+  DBuf dqp, dcp;
+  if (use_nn2 && (dqp.alloc(elem_size(spec) * (size_t)pitch2 * nq, st) ||
+                  dcp.alloc(elem_size(spec) * (size_t)pitch2 * ncand, st)))
+    return -1;
   if (use_lb) {
     const int L = max_len;
     if (denv.alloc(sizeof(float2) * (size_t)L * ncand, st) || denvq.alloc(sizeof(float2) * (size_t)L * nq, st) ||
@@ -751,6 +761,10 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     DBuf dqt;
     if (dkeys.alloc(sizeof(float) * (size_t)npairs, st) || dqt.alloc(sizeof(float2) * (size_t)nq * L, st)) return -1;
     CK(lb_qprep(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, L, dqt.as<float2>(), st));
+    if (use_nn2) {
+      CK(nn2_pad(spec->precision, dQ, (const long long*)dqoff, (int)nq, L, pitch2, dqp.p, st));
+      ++g_launches;
+    }
     const int nch = nchunk > 0 ? nchunk : 1;
     const int64_t csz = nchunk > 0 ? chunk : ncand;
     for (int k = 0; k < nch; ++k) {
@@ -762,6 +776,11 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       CK(lb_matrix(spec_mode(spec), (const float2*)dqt.as<float2>(), (int)nq, (const float2*)denv.as<float2>(),
                    (int)ncand, cb, ce, L, dkeys.as<float>(), st));
       g_launches += 2;
+      if (use_nn2) {
+        CK(nn2_pad(spec->precision, dC, (const long long*)dcoff + cb, ce - cb, L, pitch2,
+                   (char*)dcp.p + elem_size(spec) * (size_t)pitch2 * cb, st));
+        ++g_launches;
+      }
     }
     mark(st, "lb_keys");
     // dkeys: the keys per (query, candidate); dskeys: the same in rank order
@@ -849,7 +868,8 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // keys).  LB path: items whose pairs all fail their key cost a load and a ballot, so
   // the tail uses full-warp items of 32.
   const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? env_int("EKB_NN_SEG1", 64) : ka + 64));
-  const int K1_lb = env_int("EKB_NN_K1", 1), K2 = one_launch ? env_int("EKB_NN_K2", 4) : 8;
+  // (k_nn2 takes smaller tail items: its survivors are spread over more warps)
+  const int K1_lb = env_int("EKB_NN_K1", 1), K2 = one_launch ? env_int("EKB_NN_K2", use_nn2 ? 2 : 4) : 8;
   const NNFn fnB = pick_nn(spec->kind, spec_mode(spec), engB);
   const size_t smemB = pair_smem(max_len, engB, wpb, elem_size(spec)) + (size_t)env_int("EKB_NN_XSMEM", 0);
   // With the LB pre-test most pairs are cheap and the first segment's tail of long DPs
@@ -864,6 +884,23 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     if (lo >= hi) continue;
     const long long items = (long long)nq * ((mid - lo + K1 - 1) / K1 + (hi - mid + K2 - 1) / K2);
     const bool seg1_wide = g4 && !one_launch && sgi == 0 && env_int("EKB_SEG1_G8", 1);
+    if (use_nn2 && one_launch) {
+      // per-query item counters, then the done bitmask (k_nn2's work source)
+      const long long qn_words = (nq + 1) & ~1LL;  // ints of the counters, 8-byte aligned
+      DBuf dqn;
+      const size_t qn_bytes = 4 * (size_t)qn_words + 8 * (size_t)((nq + 63) / 64);
+      if (dqn.alloc(qn_bytes, st)) return -1;
+      CK(cudaMemsetAsync(dqn.p, 0, qn_bytes, st));
+      const int dlo2 = std::max(-wmax, 1 - (int)max_len), dhi2 = std::min(wmax, (int)max_len - 1);
+      const int dbase2 = (dlo2 - 1) & ~1;
+      const bool virt0 = dlo2 - 1 == dbase2 && (dhi2 + 1 - dbase2) % 8 == 0;
+      CK(nn2_launch(spec_mode(spec), virt0, g_ctx.nsm, items, st, dqp.p, dcp.p, pitch2, (int)max_len, (int)nq,
+                    (int)ncand, (const int*)dord.as<int>(), lo, mid, hi, K1, K2, wmax, dcut.as<unsigned long long>(),
+                    acc, dqn.as<int>(), (unsigned long long*)(dqn.as<int>() + qn_words), (const float*)dskeys.as<float>(),
+                    (const float2*)denvq.as<float2>(), (int)max_len, dqstop.as<int>()));
+      ++g_launches;
+      continue;
+    }
     const NNFn fseg = seg1_wide ? pick_nn(spec->kind, spec_mode(spec), E_GDIAG8) : fnB;
     const size_t smseg = seg1_wide ? pair_smem(max_len, E_GDIAG8, wpb, elem_size(spec)) : smemB;
     if (launch_persistent(fseg, 32 * wpb, smseg, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,

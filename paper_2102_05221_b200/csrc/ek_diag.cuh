@@ -43,6 +43,9 @@ constexpr unsigned FULL = 0xffffffffu;
 // debug builds: in-matrix band cells the diagonal engine evaluated, and those of them that
 // were live (value <= the cutoff in force) -- the share EAPruned's column pruning would skip
 __device__ unsigned long long g_live[2];
+// and the live corridor at each vote: the span of lanes holding a live cell (first..last),
+// histogrammed per 64 anti-diagonals of t (16 x 33 bins)
+__device__ unsigned long long g_corr[16 * 33];
 #endif
 
 #ifndef EKB_DBOUND
@@ -324,6 +327,15 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     if (CHK && t + 1 >= Tf) return true;
     const bool vote = W == 32 && (ROT ? (S & 1) == 1 : ((t >> 1) & 1) == 1);
     if (vote) {
+#ifdef EKB_LIVE
+      if constexpr (!GUARD && W == 32) {
+        const unsigned m = __ballot_sync(FULL, alive);
+        if (lane == 0) {
+          const int span = m ? (32 - __clz(m)) - (__ffs(m) - 1) : 0;
+          atomicAdd(&g_corr[min(t >> 6, 15) * 33 + span], 1ull);
+        }
+      }
+#endif
       if constexpr (GUARD) {
         const unsigned live = __ballot_sync(FULL, alive);
         if (!live) {

@@ -549,6 +549,11 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
   // have one -- when it reaches nq no item can hold a pair to visit and the warps leave
   // without claiming the rest (the cutoff only decreases, so a stop stays valid).
   const bool stops = use_lb && qstop != nullptr;
+  // Leaving once every query has a stop is sound only when all the items of a query come
+  // from one counter, claimed in increasing rank: item it is on counter it % kNnCounters, and
+  // it = (segment base) + r nq + q, so that needs nq % kNnCounters == 0.  Otherwise an item
+  // below a stop could still sit unclaimed on a lagging counter; the per-item test remains.
+  const bool stop_exit = stops && nq % kNnCounters == 0;
 #ifdef EKB_TRACE
   unsigned long long tr_t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_t0));
@@ -556,7 +561,7 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
 #endif
   for (;;) {
     long long it = -1;
-    if (lane == 0 && !(stops && *(volatile int*)(qstop + nq) >= nq)) {
+    if (lane == 0 && !(stop_exit && *(volatile int*)(qstop + nq) >= nq)) {
       while (ctr_left > 0) {
         const long long cand = (long long)atomicAdd(ctr + ck, 1ULL) * kNnCounters + ck;
         if (cand < nitems) {
