@@ -141,6 +141,36 @@ int ek_subseq_profile(const ek_spec* spec, const double* query, int64_t lq, cons
 int ek_envelopes(const double* series, int64_t total, const int64_t* off, int64_t n, int64_t L, int64_t window,
                  double* upper, double* lower);
 
+/* ---- Ingestion ----
+ * ek_parse_tsv <- series.load_tsv (pkg/src/elastik/series.py:61-86), native fast path.
+ * UCR text (one series per line, the numeric label first, truncated to int; fields split by
+ * `sep`; \n, \r\n or \r line ends; blank lines skipped) into the packed layout every entry
+ * point takes: values[offsets[s] .. + lengths[s]], labels[s].  Call with values == NULL to
+ * count (n_series, n_values), then again with buffers of those sizes.  Returns 0, or 1 when
+ * the fast path does not decide the file (any token outside the plain decimal grammar,
+ * non-finite or overflowing values, a line without a value, non-ASCII text, an empty
+ * dataset; *bad_line = its line): the caller then runs the reference's loader, which
+ * accepts or raises exactly as series.load_tsv does.  Host only (no device needed). */
+int ek_parse_tsv(const char* text, int64_t len, int32_t sep, int64_t* n_series, int64_t* n_values,
+                 int64_t* labels, int64_t* offsets, int64_t* lengths, double* values, int64_t* bad_line);
+/* Page-locked host buffers (cudaHostAlloc, portable) and device buffers; NULL on failure. */
+void* ek_host_alloc(int64_t bytes);
+int ek_host_free(void* p);
+void* ek_dev_alloc(int64_t bytes);
+int ek_dev_free(void* p);
+/* dir 0: host -> device, 1: device -> host, 2: device -> device.  stream NULL: the library's
+ * stream, synchronised before returning; else enqueued on `stream`. */
+int ek_memcpy(void* dst, const void* src, int64_t bytes, int32_t dir, void* stream);
+/* series.derivative (series.py:134-144) of n device series: d_out[d_out_off[s] + i] =
+ * ((x[i+1] - x[i]) + (x[i+2] - x[i]) / 2) / 2 for i < d_len[s] - 2 (lengths >= 3 are the
+ * caller's check, DegenerateInputError in the Python API). */
+int ek_derivative_dev(const double* d_in, const int64_t* d_off, const int32_t* d_len, int64_t n, double* d_out,
+                      const int64_t* d_out_off, void* stream);
+/* series.znormalize (series.py:118-131) of n device series with numpy's pairwise-sum mean
+ * and std (std < 1e-12 -> zeros); h_len: the lengths on the host (each >= 2). */
+int ek_znormalize_dev(const double* d_in, const int64_t* d_off, const int32_t* d_len, const int32_t* h_len,
+                      int64_t n, double* d_out, const int64_t* d_out_off, void* stream);
+
 /* Number of kernel launches the library issued since the last reset (bench accounting). */
 int64_t ek_launch_count(int32_t reset);
 

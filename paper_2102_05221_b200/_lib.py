@@ -77,6 +77,16 @@ EXPORTS = {
                        _i64p, _dp, _i64p, _i64p, _i64p, C.c_void_p], C.c_int),
     "ek_subseq_profile": ([C.POINTER(EkSpec), _dp, C.c_int64, _dp, C.c_int64, C.c_int32, _dp], C.c_int),
     "ek_envelopes": ([_dp, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int64, _dp, _dp], C.c_int),
+    "ek_parse_tsv": ([C.c_char_p, C.c_int64, C.c_int32, _i64p, _i64p, _i64p, _i64p, _i64p, _dp, _i64p], C.c_int),
+    "ek_host_alloc": ([C.c_int64], C.c_void_p),
+    "ek_host_free": ([C.c_void_p], C.c_int),
+    "ek_dev_alloc": ([C.c_int64], C.c_void_p),
+    "ek_dev_free": ([C.c_void_p], C.c_int),
+    "ek_memcpy": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p], C.c_int),
+    "ek_derivative_dev": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
+                          C.c_int),
+    "ek_znormalize_dev": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                           C.c_void_p], C.c_int),
 }
 
 _lock = threading.Lock()

@@ -26,7 +26,9 @@ import os
 import sys
 import time
 
-from . import _backend
+import numpy as np
+
+from . import _backend, ingest
 from ._lib import PRECISIONS
 from .engines import VARIANTS, distance_batch
 from .errors import ElastikError
@@ -81,10 +83,15 @@ def _threads(value):
     return int(env) if env else 1
 
 
-def _load(path, args, znorm=False) -> LabeledDataset:
-    ds = load_tsv(path, delimiter=args.delimiter)
+def _load(path, args, znorm=False):
+    """A dataset file into a page-locked packed batch (ingest.load_tsv_packed); --znorm runs
+    series.znormalize on the device (DeviceSeries.znormalize, bit-identical)."""
+    ds = ingest.load_tsv_packed(path, delimiter=args.delimiter)
     if znorm:
-        ds = LabeledDataset(name=ds.name, entries=tuple((lab, znormalize(v)) for lab, v in ds.entries))
+        if np.any(ds.lengths < 2):  # the reference's error, from its own check
+            znormalize(ds.series(int(np.argmin(ds.lengths))))
+        with ingest.DeviceSeries.upload(ds) as d, d.znormalize() as z:
+            ds = ingest.pack(z.to_host(), ds.labels, ds.name)
     return ds
 
 

@@ -446,20 +446,6 @@ int strip_scratch(Fn fn, int eng, int block, size_t smem, int lmax, Params& prm,
   return 0;
 }
 
-// numpy pairwise-sum plan (see ek_subseq.cuh)
-void np_plan_rec(int start, int n, std::vector<int2>& leaves, std::vector<int>& ops) {
-  if (n <= 128) {
-    ops.push_back((int)leaves.size());
-    leaves.push_back(make_int2(start, n));
-    return;
-  }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  np_plan_rec(start, n2, leaves, ops);
-  np_plan_rec(start + n2, n - n2, leaves, ops);
-  ops.push_back(-1);
-}
-
 }  // namespace
 
 extern "C" {
@@ -1198,7 +1184,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   // numpy pairwise-sum plan for length lq
   std::vector<int2> leaves;
   std::vector<int> ops;
-  np_plan_rec(0, (int)lq, leaves, ops);
+  np_plan_build(0, (int)lq, leaves, ops);
   DBuf dleaves, dops, dcut, dout, dtend, dcnt;
   if (dleaves.alloc(sizeof(int2) * leaves.size(), st) || dops.alloc(sizeof(int) * ops.size(), st) ||
       dcut.alloc(8, st) || dout.alloc(sizeof(double) * (size_t)nwin, st) || dtend.alloc(sizeof(int) * (size_t)nwin, st) ||
@@ -1568,5 +1554,86 @@ extern "C" {
 
 double ek_fp64_peak_ops(void) { return alu_peak_ops<double>(); }
 double ek_fp32_peak_ops(void) { return alu_peak_ops<float>(); }
+
+}  // extern "C"
+
+// ---- ingestion: page-locked host buffers, device buffers, transforms ----
+extern "C" {
+
+void* ek_host_alloc(int64_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx() || bytes < 0) return nullptr;
+  void* p = nullptr;
+  const cudaError_t e = cudaHostAlloc(&p, (size_t)std::max<int64_t>(bytes, 8), cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    fail("cudaHostAlloc(%lld) failed: %s", (long long)bytes, cudaGetErrorString(e));
+    return nullptr;
+  }
+  return p;
+}
+
+int ek_host_free(void* p) {
+  if (!p) return 0;
+  CK(cudaFreeHost(p));
+  return 0;
+}
+
+void* ek_dev_alloc(int64_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx() || bytes < 0) return nullptr;
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, (size_t)std::max<int64_t>(bytes, 8));
+  if (e != cudaSuccess) {
+    fail("cudaMalloc(%lld) failed: %s", (long long)bytes, cudaGetErrorString(e));
+    return nullptr;
+  }
+  return p;
+}
+
+int ek_dev_free(void* p) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!p) return 0;
+  CK(cudaFree(p));
+  return 0;
+}
+
+int ek_memcpy(void* dst, const void* src, int64_t bytes, int32_t dir, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  if (bytes < 0 || dir < 0 || dir > 2) return fail("ek_memcpy: bad arguments");
+  if (bytes == 0) return 0;
+  cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
+  const cudaMemcpyKind k = dir == 0 ? cudaMemcpyHostToDevice : dir == 1 ? cudaMemcpyDeviceToHost
+                                                                        : cudaMemcpyDeviceToDevice;
+  CK(cudaMemcpyAsync(dst, src, (size_t)bytes, k, st));
+  if (!stream) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ek_derivative_dev(const double* d_in, const int64_t* d_off, const int32_t* d_len, int64_t n, double* d_out,
+                      const int64_t* d_out_off, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
+  CK(derivative_dev(d_in, (const long long*)d_off, (const int*)d_len, n, d_out, (const long long*)d_out_off, st));
+  ++g_launches;
+  if (!stream) CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ek_znormalize_dev(const double* d_in, const int64_t* d_off, const int32_t* d_len, const int32_t* h_len,
+                      int64_t n, double* d_out, const int64_t* d_out_off, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  for (int64_t s = 0; s < n; ++s)
+    if (h_len[s] < 2) return fail("z-normalization needs at least 2 points");
+  cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
+  const cudaError_t e = znormalize_dev(d_in, (const long long*)d_off, (const int*)d_len, (const int*)h_len, n, d_out,
+                                       (const long long*)d_out_off, st);
+  if (e != cudaSuccess) return fail("ek_znormalize_dev: %s", cudaGetErrorString(e));
+  ++g_launches;
+  if (!stream) CK(cudaStreamSynchronize(st));
+  return 0;
+}
 
 }  // extern "C"

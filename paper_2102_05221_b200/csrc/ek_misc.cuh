@@ -1,5 +1,6 @@
 // ek_misc.cuh -- declarations of the kind-independent kernels (ek_misc.cu).
 #pragma once
+#include <vector>
 #include "ek_kernels.cuh"
 
 namespace ekb {
@@ -40,5 +41,12 @@ __global__ void k_nn_pick(NNAcc a);
 __global__ void k_nn_final(NNAcc a, int nq, int ncand, long long* nn_idx, double* nn_dist, long long* cells,
                            long long* computed, long long* abandoned);
 __global__ void k_nn_acc_init(NNAcc a, int nq);
+
+// ingestion (ek_ingest.cu): numpy pairwise-sum plans, and the series transforms on the device
+void np_plan_build(int start, int n, std::vector<int2>& leaves, std::vector<int>& ops);
+cudaError_t derivative_dev(const double* in, const long long* off, const int* len, long long n, double* out,
+                           const long long* ooff, cudaStream_t st);
+cudaError_t znormalize_dev(const double* in, const long long* off, const int* len, const int* hl, long long n,
+                           double* out, const long long* ooff, cudaStream_t st);
 
 }  // namespace ekb

@@ -148,20 +148,34 @@ def nn_search(query, candidates, cfg: SearchConfig, envelopes=None):
     return float(dist[0]), int(idx[0]), stats
 
 
+def _batch(ds):
+    """The series of a LabeledDataset, or of an ingest.PackedDataset: equal lengths as a 2-D
+    view of its (page-locked) buffer, which ek_nn uploads without a copy."""
+    from .ingest import PackedDataset
+
+    if isinstance(ds, PackedDataset):
+        n = len(ds)
+        if n and np.all(ds.lengths == ds.lengths[0]) and np.array_equal(ds.offsets, np.arange(n) * ds.lengths[0]):
+            return ds.values[:n * int(ds.lengths[0])].reshape(n, int(ds.lengths[0]))
+        return [ds.series(s) for s in range(n)]
+    return ds.series
+
+
 def classify_1nn(train: LabeledDataset, test: LabeledDataset, cfg: SearchConfig,
                  threads: int | None = None) -> list[SearchRecord]:
     """1-NN classification of every test series against the train set (search.py:128-160).
 
     All queries go to the GPU in one call; ``threads`` is accepted for
-    signature compatibility and has no effect.
+    signature compatibility and has no effect.  ``train`` / ``test`` may also be
+    ``ingest.PackedDataset`` batches (load_tsv_packed).
     """
-    labels = train.labels
+    labels = [int(x) for x in train.labels]
     start = time.perf_counter()
-    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, test.series, train.series, backend=cfg.backend,
+    idx, dist, cells, comp, ab = nn_batch(cfg.spec, cfg.variant, _batch(test), _batch(train), backend=cfg.backend,
                                           precision=cfg.precision)
     per_query = (time.perf_counter() - start) / max(1, len(test))
     records = []
-    for q, (actual, _) in enumerate(test.entries):
+    for q, actual in enumerate(int(x) for x in test.labels):
         best = int(idx[q])
         records.append(SearchRecord(
             query_index=q, actual=actual, predicted=labels[best] if best >= 0 else -1, nn_index=best,
