@@ -264,7 +264,7 @@ class Runner:
         elif self.base in ("c3w", "c3e"):
             cells = np.zeros(1, dtype=np.int64)
             lib.check(self.L.ek_pairwise_dev(self.h.ref, 3, self.dX.data_ptr(), self.doff.data_ptr(),
-                                             self.dlen.data_ptr(), self.n, self.Lq, self.dD.data_ptr(),
+                                             self.dlen.data_ptr(), self.n, self.Lq, 1, self.dD.data_ptr(),
                                              lib.iptr(cells), stream_handle))
             self.last["cells"] = int(cells[0])
         else:

@@ -113,8 +113,11 @@ int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int6
 int ek_pairwise_range(const ek_spec* spec, int32_t variant, const double* series, int64_t total, const int64_t* off,
                       const int64_t* len, int64_t n, int64_t pair_lo, int64_t pair_hi, double* out, int64_t* cells);
 
+/* ek_pairwise on device arrays; dense != 0 promises every length equals max_len (the
+ * |i-j| tables of WDTW / TWE are then shared per block). */
 int ek_pairwise_dev(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
-                    const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells, void* stream);
+                    const int32_t* d_len, int64_t n, int32_t max_len, int32_t dense, double* d_D, int64_t* cells,
+                    void* stream);
 
 /* Best window of `reference` against `query` (dtw/cdtw), every stride-1 offset,
  * z-normalising the query once and each window on the fly when normalize != 0.

@@ -70,7 +70,7 @@ EXPORTS = {
     "ek_pairwise_range": ([C.POINTER(EkSpec), C.c_int32, _dp, C.c_int64, _i64p, _i64p, C.c_int64, C.c_int64, C.c_int64,
                            _dp, _i64p], C.c_int),
     "ek_pairwise_dev": ([C.POINTER(EkSpec), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
-                         C.c_void_p, _i64p, C.c_void_p], C.c_int),
+                         C.c_int32, C.c_void_p, _i64p, C.c_void_p], C.c_int),
     "ek_subseq": ([C.POINTER(EkSpec), C.c_int32, _dp, C.c_int64, _dp, C.c_int64, C.c_int32, _i64p, _dp, _i64p,
                    _i64p, _i64p], C.c_int),
     "ek_subseq_dev": ([C.POINTER(EkSpec), C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,

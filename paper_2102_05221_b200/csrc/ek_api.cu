@@ -829,11 +829,36 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // On the LB path phase A joins phase B's single launch: the top ranks are its first
   // items, and their long DPs no longer leave the GPU idle at a launch boundary.
   const bool one_launch = use_lb && kind_tag(spec->kind) == K_DTW;
+  // Bulk asynchronous candidate staging (Params.bulk, ek_tma.cuh) for the launches that take
+  // it: the non-LB path with a diagonal engine on a dense, even-length float64 batch at a
+  // 16-byte aligned base (every copy's address and size are then multiples of 16 bytes);
+  // it needs one more series slot per warp.
+  // Taken only when the slot costs no resident blocks (C4: TWE keeps its 2 blocks per SM and
+  // takes it; MSM's 4 would drop to 3, measured 3% slower).
+  auto bulk_launch = [&](NNFn f, int e, size_t sm, Params& p) -> size_t {
+    p = ph.prm;
+    p.bulk = (!use_lb && dense && !spec->precision && max_len % 2 == 0 && engine_is_diag(e) &&
+              ((uintptr_t)dC & 15) == 0 && env_int("EKB_BULK", 1) != 0) ? 1 : 0;
+    if (!p.bulk) return sm;
+    const size_t sm2 = sm + sizeof(double) * (size_t)wpb * series_slot(max_len, engine_pad(e));
+    int b1 = 0, b2 = 0;
+    if (sm > 48 * 1024) cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (sm2 > 48 * 1024) cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, f, 32 * wpb, sm) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, f, 32 * wpb, sm2) != cudaSuccess || b2 < b1) {
+      cudaGetLastError();
+      p.bulk = 0;
+      return sm;
+    }
+    return sm2;
+  };
   const int ka = (share && !one_launch) ? (int)std::min<int64_t>(4, ncand) : 0;
   if (ka > 0) {
-    if (launch_persistent(fn, 32 * wpb, smem, st, (long long)nq * ka, dQ, (const long long*)dqoff,
+    Params pa;
+    const size_t sma = bulk_launch(fn, eng, smem, pa);
+    if (launch_persistent(fn, 32 * wpb, sma, st, (long long)nq * ka, dQ, (const long long*)dqoff,
                           (const int*)dqlen, (int)nq, dC, (const long long*)dcoff, (const int*)dclen, (int)ncand,
-                          (const int*)dord.as<int>(), 0, ka, ka, 1, 1, win, (int)max_len, ph.prm, (int)share,
+                          (const int*)dord.as<int>(), 0, ka, ka, 1, 1, win, (int)max_len, pa, (int)share,
                           dcut.as<unsigned long long>(), acc, dcnt.as<int>() + 32,
                           (const float*)nullptr, (const float2*)nullptr, dovf.as<int2>(), ovf_count, (int*)nullptr))
       return -1;
@@ -888,10 +913,12 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       continue;
     }
     const NNFn fseg = seg1_wide ? pick_nn(spec->kind, spec_mode(spec), E_GDIAG8) : fnB;
-    const size_t smseg = seg1_wide ? pair_smem(max_len, E_GDIAG8, wpb, elem_size(spec)) : smemB;
+    Params pb;
+    const size_t smseg = bulk_launch(fseg, seg1_wide ? E_GDIAG8 : engB,
+                                     seg1_wide ? pair_smem(max_len, E_GDIAG8, wpb, elem_size(spec)) : smemB, pb);
     if (launch_persistent(fseg, 32 * wpb, smseg, st, items, dQ, (const long long*)dqoff, (const int*)dqlen, (int)nq, dC,
                           (const long long*)dcoff, (const int*)dclen, (int)ncand, (const int*)dord.as<int>(), lo, mid,
-                          hi, K1, K2, win, (int)max_len, ph.prm, (int)share, dcut.as<unsigned long long>(),
+                          hi, K1, K2, win, (int)max_len, pb, (int)share, dcut.as<unsigned long long>(),
                           acc, dcnt.as<int>() + 64 + 32 * sgi,
                           (const float*)(use_lb ? dskeys.as<float>() : nullptr),
                           (const float2*)denvq.as<float2>(), seg1_wide ? dovf2.as<int2>() : dovf.as<int2>(),
@@ -1060,7 +1087,8 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
 // d_D != null: the full matrix; else pairs [plo, phi) of the upper triangle into d_vec
 static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
                              const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells,
-                             cudaStream_t st, long long plo = 0, long long phi = -1, double* d_vec = nullptr) {
+                             cudaStream_t st, long long plo = 0, long long phi = -1, double* d_vec = nullptr,
+                             bool equal_len = false) {
   if (check_spec(spec)) return -1;
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
   if (cells) *cells = 0;
@@ -1085,10 +1113,20 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
   const int wpb = pick_wpb(max_len, eng, 4, 0, elem_size(spec));
   const TriFn tf = pick_tri(spec->kind, spec_mode(spec), eng);
   DBuf dstrip;
-  const size_t tsmem = pair_smem(max_len, eng, wpb, elem_size(spec));
+  size_t tsmem = pair_smem(max_len, eng, wpb, elem_size(spec));
   if (strip_scratch(tf, eng, 32 * wpb, tsmem, max_len, ph.prm, dstrip, st)) return -1;
+  // equal lengths: one |i-j| table per block (k_triangle, Params.shared_tab); the warps keep
+  // only their series (C3 WDTW: 2 -> 3 resident blocks)
+  Params tp = ph.prm;
+  const int tk = kind_tag(spec->kind);
+  if (equal_len && (tk == K_WDTW || tk == K_TWE) && !engine_is_diag(eng) && !engine_is_strip(eng) &&
+      env_int("EKB_SHARED_TAB", 1) != 0) {
+    tp.shared_tab = 1;
+    const int slot = series_slot(max_len, engine_pad(eng));
+    tsmem = elem_size(spec) * ((size_t)wpb * (32 / engine_W(eng)) * 2 * slot + 2 * ((size_t)max_len + kTabPad) + 1);
+  }
   if (launch_persistent(tf, 32 * wpb, tsmem, st, np,
-                        d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, ph.prm, d_D,
+                        d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, tp, d_D,
                         plo, phi, d_vec, dtot.as<unsigned long long>(), dcnt.as<int>()))
     return -1;
   mark(st, "triangle");
@@ -1102,11 +1140,13 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
 }
 
 int ek_pairwise_dev(const ek_spec* spec, int32_t variant, const double* d_series, const int64_t* d_off,
-                    const int32_t* d_len, int64_t n, int32_t max_len, double* d_D, int64_t* cells, void* stream) {
+                    const int32_t* d_len, int64_t n, int32_t max_len, int32_t dense, double* d_D, int64_t* cells,
+                    void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (ensure_ctx()) return -1;
   cudaStream_t st = stream ? (cudaStream_t)stream : g_ctx.stream;
-  return pairwise_dev_impl(spec, variant, d_series, d_off, d_len, n, max_len, d_D, cells, st);
+  return pairwise_dev_impl(spec, variant, d_series, d_off, d_len, n, max_len, d_D, cells, st, 0, -1, nullptr,
+                           dense != 0);
 }
 
 int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int64_t total, const int64_t* off,
@@ -1133,8 +1173,9 @@ int ek_pairwise(const ek_spec* spec, int32_t variant, const double* series, int6
   CK(cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (bad) return fail("%s", kNonFinite);
+  const bool eq = std::all_of(l32.begin(), l32.end(), [&](int32_t v) { return v == mx; });
   if (pairwise_dev_impl(spec, variant, ds.as<double>(), doff.as<int64_t>(), dlen.as<int32_t>(), n, mx, dD.as<double>(),
-                        cells, st))
+                        cells, st, 0, -1, nullptr, eq))
     return -1;
   CK(cudaMemcpyAsync(D, dD.p, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1160,8 +1201,9 @@ int ek_pairwise_range(const ek_spec* spec, int32_t variant, const double* series
   CK(cudaMemcpyAsync(doff.p, off, 8 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dlen.p, l32.data(), 4 * n, cudaMemcpyHostToDevice, st));
   if (inputs_finite(ds.as<double>(), total, nullptr, 0, st)) return -1;
+  const bool eq = std::all_of(l32.begin(), l32.end(), [&](int32_t v) { return v == mx; });
   if (pairwise_dev_impl(spec, variant, ds.as<double>(), doff.as<int64_t>(), dlen.as<int32_t>(), n, mx, nullptr, cells,
-                        st, pair_lo, pair_hi, dv.as<double>()))
+                        st, pair_lo, pair_hi, dv.as<double>(), eq))
     return -1;
   CK(cudaMemcpyAsync(out, dv.p, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

@@ -44,6 +44,13 @@ struct Params {
   // warp, indexed by the global warp id)
   double* strip_buf;
   int strip_stride;
+  // k_nn, non-LB path on dense even-length float64 batches with a diagonal engine: stage
+  // each candidate with one bulk asynchronous copy (TMA), one pair ahead, into a second
+  // per-warp candidate slot (see ek_tma.cuh); 0 = synchronous staging
+  int bulk;
+  // k_triangle on equal lengths with a row-stripe engine that reads an |i-j| table (WDTW,
+  // TWE): one table per block instead of one per pair slot (every pair has the same one)
+  int shared_tab;
 };
 
 // Params for one pair whose longest series has length m.

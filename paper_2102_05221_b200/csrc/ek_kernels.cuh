@@ -17,6 +17,7 @@
 #include "ek_diag.cuh"
 #include "ek_stripe.cuh"
 #include "ek_lb.cuh"
+#include "ek_tma.cuh"
 
 namespace ekb {
 
@@ -325,9 +326,30 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   using R = real_t<MODE>;
-  R* X = (R*)smem + wib * warp_stride(lmax, ENG) + PAD;
+  // prm.shared_tab (all series of length lmax): the warps' slots hold only the series, and
+  // one two-sided |i-j| table after them serves the whole block
+  constexpr bool TABLED = (KIND == K_WDTW || KIND == K_TWE) && !engine_is_diag(ENG) && !engine_is_strip(ENG);
+  const bool shtab = TABLED && prm.shared_tab != 0;
+  const int wst = shtab ? (32 / engine_W(ENG)) * 2 * series_slot(lmax, PAD) : warp_stride(lmax, ENG);
+  R* X = (R*)smem + wib * wst + PAD;
   R* Y = X + series_slot(lmax, PAD);
   R* tab = Y - PAD + series_slot(lmax, PAD);
+  const R* btab = (R*)smem + (blockDim.x >> 5) * wst + lmax + kTabPad;  // its d = 0 entry
+  if (shtab) {
+    R* bt = (R*)smem + (blockDim.x >> 5) * wst;
+    const Params pp = pair_params(prm, lmax);
+    const int half = lmax + kTabPad;
+    for (int k = threadIdx.x; k <= 2 * half; k += blockDim.x) {
+      const int d = min(abs(k - half), lmax);
+      if constexpr (KIND == K_WDTW) {
+        bt[k] = (d < pp.wt_len) ? (R)pp.wt[d] : (R)0.0;
+      } else {
+        const R dij = (R)d;
+        bt[k] = dmul((R)pp.nu, dadd(dij, dij));
+      }
+    }
+    __syncthreads();
+  }
   const long long npairs = phi;
   NoLoader ld;
   unsigned long long my_cells = 0;
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
     // two pairs per claim, one per half-warp, in lockstep when their shapes match; a pair
     // of different shapes runs in two passes with both halves on the same pair
     const int half = (threadIdx.x >> 4) & 1, hl = threadIdx.x & 15;
-    R* Xh = X + half * (warp_stride(lmax, ENG) / 2);  // each half: [X][Y][|i-j| table]
+    R* Xh = X + half * (wst / 2);  // each half: [X][Y][|i-j| table (unless shared)]
     R* Yh = Xh + series_slot(lmax, PAD);
     R* tabh = Yh - PAD + series_slot(lmax, PAD);
     for (;;) {
@@ -368,7 +390,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
           stage_series<KIND, R, 16>(Xh, series + off[s], nl, PAD);
           stage_series<KIND, R, 16>(Yh, series + off[t], nc, PAD);
           const int tablen = max(nl, nc) + 1;
-          const R* tabe = engine_table<KIND, ENG>(tabh, tablen, lmax, pp);
+          const R* tabe = shtab ? btab : engine_table<KIND, ENG>(tabh, tablen, lmax, pp);
           __syncwarp();
           run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{Xh, nl}, nl, SmemSeriesT<R>{Yh, nc}, nc, w, EKB_INF,
                                              nullptr, tabe, tablen, pp, ld, cost, tend);
@@ -410,7 +432,7 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
       stage_series<KIND>(X, series + off[s], nl, PAD);
       stage_series<KIND>(Y, series + off[t], nc, PAD);
       const int tablen = max(nl, nc) + 1;
-      const R* tabe = engine_table<KIND, ENG>(tab, tablen, lmax, pp);
+      const R* tabe = shtab ? btab : engine_table<KIND, ENG>(tab, tablen, lmax, pp);
       __syncwarp();
       run_engine<KIND, MODE, ENG, false>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, EKB_INF, nullptr, tabe,
                                          tablen, pp, ld, cost, tend);
@@ -520,9 +542,25 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   using R = real_t<MODE>;
-  R* QB = (R*)smem + wib * warp_stride(lmax, ENG) + PAD;
+  // prm.bulk: a second candidate slot after the warp's usual layout (diagonal engines have
+  // no table, so both slots stay 16-byte aligned), filled by bulk copies one pair ahead
+  const bool bulk = (MODE & M_F32) == 0 && engine_is_diag(ENG) && skeys == nullptr && prm.bulk != 0;
+  const int wstride = warp_stride(lmax, ENG) + (prm.bulk ? series_slot(lmax, PAD) : 0);
+  R* QB = (R*)smem + wib * wstride + PAD;
   R* CB = QB + series_slot(lmax, PAD);
   R* tab = CB - PAD + series_slot(lmax, PAD);
+  R* const CB2 = (R*)smem + wib * wstride + warp_stride(lmax, ENG) + PAD;
+  __shared__ unsigned long long nn_bar[4][2];  // per warp (blockDim <= 128): one mbarrier per slot
+  unsigned bphase = 0;                          // bit b: parity of slot b's next completion
+  int bcur = 0;                                 // slot of the pair about to run
+  if (bulk) {
+    if (lane == 0) {
+      mbar_init(&nn_bar[wib][0], 1);
+      mbar_init(&nn_bar[wib][1], 1);
+      mbar_init_fence();
+    }
+    __syncwarp();
+  }
   // two segments in one launch: ranks [rank_lo, rank_mid) in items of K1, then
   // [rank_mid, rank_hi) in items of K2, each round-major over the queries, so warps
   // that finish the first segment's tail start on the second at once.  Only the
@@ -627,7 +665,15 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
       stage_series<KIND>(QB, Q + qoff[q], lq, PAD);
       staged_q = q;
     }
-    if (!use_lb) {  // the first pair's first data chunk
+    if (bulk) {  // the first pair's candidate, whole, into the current slot
+      const double* s = C + __shfl_sync(FULL, ooff, 0);
+      const int lc = __shfl_sync(FULL, olen, 0);
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async();
+        bulk_g2s(bcur ? CB2 : CB, s, 8u * (unsigned)lc, &nn_bar[wib][bcur]);
+      }
+    } else if (!use_lb) {  // the first pair's first data chunk
       const double* s = C + __shfl_sync(FULL, ooff, 0);
       const int lc = __shfl_sync(FULL, olen, 0);
 #pragma unroll
@@ -647,7 +693,26 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
       const int w = win < 0 ? nl : win;
       bool evaluate = w >= nl - nc;
       int staged = min(kChunk, lc);  // candidate elements already in CB
-      if (use_lb) {
+      R* CBc = CB;                    // the slot holding this pair's candidate
+      if (bulk) {
+        // this pair's copy has landed: request the next pair's into the other slot (its last
+        // readers finished with the previous pair: __syncwarp, then the proxy fence), and
+        // write the pads around this one
+        mbar_wait(&nn_bar[wib][bcur], (bphase >> bcur) & 1u);
+        bphase ^= 1u << bcur;
+        CBc = bcur ? CB2 : CB;
+        const double* ns = C + __shfl_sync(FULL, ooff, min(i + 1, 31));
+        const int nl2 = __shfl_sync(FULL, olen, min(i + 1, 31));
+        __syncwarp();
+        if (i + 1 < cnt && lane == 0) {
+          fence_proxy_async();
+          bulk_g2s(bcur ? CB : CB2, ns, 8u * (unsigned)nl2, &nn_bar[wib][bcur ^ 1]);
+        }
+        stage_pads<KIND>(CBc, lc, PAD, (double)CBc[0]);
+        staged = lc;
+        bcur ^= 1;
+        __syncwarp();
+      } else if (use_lb) {
         // the key against the current (tighter) cutoff, then the reverse bound
         const double thr = lb_threshold<MODE>(cut, nl);
         evaluate = evaluate && (double)__shfl_sync(FULL, key, i) <= thr;
@@ -680,13 +745,13 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
       int tend = 0;
       if (evaluate) {
         const Params pp = pair_params(prm, nl);
-        LazyCand<R> ld{CB, csrc, lc, staged, !q_rows};
+        LazyCand<R> ld{CBc, csrc, lc, staged, !q_rows};
         const int tablen = max(nl, nc) + 1;
         if constexpr (!engine_is_diag(ENG)) ld.load_to(lc);  // the stripe engine reads all columns up front
         const R* tabe = engine_table<KIND, ENG>(tab, tablen, lmax, pp);
         __syncwarp();
-        const SmemSeriesT<R> X{q_rows ? QB : CB, nl};
-        const SmemSeriesT<R> Y{q_rows ? CB : QB, nc};
+        const SmemSeriesT<R> X{q_rows ? QB : CBc, nl};
+        const SmemSeriesT<R> Y{q_rows ? CBc : QB, nc};
 #ifdef EKB_TRACE
         unsigned long long tr_a, tr_b;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_a));
