@@ -167,6 +167,22 @@ EKB_DI R msm_alt(bool between, R c, R dother, R de) {
   R m = (dother < de) ? dother : de;  // "d1 if d1 < d2 else d2" (value-identical)
   return between ? c : dadd(c, m);
 }
+// The same value with the choice folded into one fused multiply-add: fma(m, f, c) with
+// f = 0.0 (between) or 1.0 is RN(c + m * f) = c or RN(c + m), since m * f is exact (m is a
+// finite difference).  A one-word select builds f, and the FMA replaces the add and the
+// 64-bit select (two ALU selects) -- the MSM cell is ALU-pipe bound.
+EKB_DI double msm_alt_fma(bool between, double c, double dother, double de) {
+  const double m = (dother < de) ? dother : de;
+  const double f = __hiloint2double(between ? 0 : 0x3ff00000, 0);
+  return __fma_rn(m, f, c);
+}
+EKB_DI float msm_alt_fma(bool between, float c, float dother, float de) {
+  const float m = (dother < de) ? dother : de;
+  return __fmaf_rn(m, between ? 0.f : 1.f, c);
+}
+#ifndef EKB_MSM_FMA
+#define EKB_MSM_FMA 1
+#endif
 
 // One cell.  D, T, L are the dependency values; the result is the reference's
 // value bit-for-bit whenever the dependencies are.  (For the DTW family the
@@ -203,8 +219,8 @@ EKB_DI R cell(R D, R T, R L, const RowD<KIND, R>& r, const ColD<KIND, R>& c, con
     const int se = sign_bit(e);
     bool brow = se != r.s;  // l_{i-1}<=l_i<=c_j or l_{i-1}>=l_i>=c_j (see msm_alt)
     bool bcol = se == c.s;  // l_i<=c_j<=c_{j-1} or l_i>=c_j>=c_{j-1}
-    R ar = msm_alt(brow, (R)p.msm_c, r.dr, de);
-    R ac = msm_alt(bcol, (R)p.msm_c, c.dc, de);
+    R ar = EKB_MSM_FMA ? msm_alt_fma(brow, (R)p.msm_c, r.dr, de) : msm_alt(brow, (R)p.msm_c, r.dr, de);
+    R ac = EKB_MSM_FMA ? msm_alt_fma(bcol, (R)p.msm_c, c.dc, de) : msm_alt(bcol, (R)p.msm_c, c.dc, de);
     R v = dadd(D, de);
     v = dmin_ref(v, dadd(T, ar));
     return dmin_ref(v, dadd(L, ac));

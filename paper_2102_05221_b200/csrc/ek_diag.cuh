@@ -46,6 +46,10 @@ __device__ unsigned long long g_live[2];
 // and the live corridor at each vote: the span of lanes holding a live cell (first..last),
 // histogrammed per 64 anti-diagonals of t (16 x 33 bins)
 __device__ unsigned long long g_corr[16 * 33];
+// narrow-window simulation (a 16-lane = 64-diagonal window, 2-lane guards, re-centred when a
+// guard lane is live and the corridor fits 12 lanes, else overflow): pairs, narrowed pairs,
+// overflowed pairs, votes, narrow votes, narrow votes of overflowed pairs, re-centrings
+__device__ unsigned long long g_sn[8];
 #endif
 
 #ifndef EKB_DBOUND
@@ -237,6 +241,10 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   bool ovf = false;
 #ifdef EKB_LIVE
   unsigned long long lv_ev = 0, lv_n = 0;
+  bool sn_narrow = false, sn_ovf = false, sn_ever = false;
+  int sn_wlo = 0;
+  unsigned long long sn_votes = 0, sn_nvotes = 0, sn_shifts = 0;
+  const int sn_lanes = (dhi + 2 - dbase + P - 1) / P;  // lanes holding the band
 #endif
 
   // One double step.  With ROT the register windows are rings whose rotation
@@ -333,6 +341,30 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
         if (lane == 0) {
           const int span = m ? (32 - __clz(m)) - (__ffs(m) - 1) : 0;
           atomicAdd(&g_corr[min(t >> 6, 15) * 33 + span], 1ull);
+          if (m && sn_lanes > 16) {
+            const int lo = __ffs(m) - 1, hi = 31 - __clz(m);
+            ++sn_votes;
+            if (!sn_narrow) {
+              if (hi - lo + 1 <= 12) {
+                sn_narrow = sn_ever = true;
+                sn_wlo = max(0, min(lo - 2, sn_lanes - 16));
+              }
+            } else if (sn_narrow) {
+              ++sn_nvotes;
+              const bool blo = lo < sn_wlo + 2 && sn_wlo > 0;
+              const bool bhi = hi > sn_wlo + 13 && sn_wlo + 16 < sn_lanes;
+              if (blo || bhi) {
+                if (hi - lo + 1 <= 12) {
+                  sn_wlo = max(0, min(lo - 2, sn_lanes - 16));
+                  ++sn_shifts;
+                } else {  // expand in place (counted per expansion)
+                  sn_ovf = true;
+                  sn_narrow = false;
+                  atomicAdd(&g_sn[7], 1ull);
+                }
+              }
+            }
+          }
         }
       }
 #endif
@@ -426,6 +458,15 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   if (lane == 0) {
     atomicAdd(&g_live[0], lv_ev);
     atomicAdd(&g_live[1], lv_n);
+    if (sn_votes) {
+      atomicAdd(&g_sn[0], 1ull);
+      atomicAdd(&g_sn[1], sn_ever ? 1ull : 0ull);
+      atomicAdd(&g_sn[2], sn_ovf ? 1ull : 0ull);
+      atomicAdd(&g_sn[3], sn_votes);
+      atomicAdd(&g_sn[4], sn_nvotes);
+      atomicAdd(&g_sn[5], sn_ovf ? sn_nvotes : 0ull);
+      atomicAdd(&g_sn[6], sn_shifts);
+    }
   }
 #endif
   DiagResult res;

@@ -58,7 +58,7 @@ cudaError_t nn2_launch(int mode, bool virt0, int nsm, long long warp_units, cuda
 #ifdef EKB_TRACE
 // debug builds: the per-warp timeline of the last dtw k_nn launch (ekb::g_trace of this unit)
 extern "C" int ek_debug_trace(unsigned long long* out, int n) {
-  if (n > 8192 * 5) n = 8192 * 5;
+  if (n > 8192 * 8) n = 8192 * 8;
   return (int)cudaMemcpyFromSymbol(out, ekb::g_trace, sizeof(unsigned long long) * n);
 }
 #endif
@@ -69,6 +69,11 @@ extern "C" int ek_debug_live_dtw(unsigned long long* out) {
   int e = (int)cudaMemcpyFromSymbol(out, ekb::g_live, 2 * sizeof(unsigned long long));
   const unsigned long long z[2] = {0, 0};
   return e | (int)cudaMemcpyToSymbol(ekb::g_live, z, sizeof z);
+}
+extern "C" int ek_debug_sn_dtw(unsigned long long* out) {
+  int e = (int)cudaMemcpyFromSymbol(out, ekb::g_sn, 8 * sizeof(unsigned long long));
+  static const unsigned long long z[8] = {};
+  return e | (int)cudaMemcpyToSymbol(ekb::g_sn, z, sizeof z);
 }
 extern "C" int ek_debug_corr_dtw(unsigned long long* out) {
   int e = (int)cudaMemcpyFromSymbol(out, ekb::g_corr, 16 * 33 * sizeof(unsigned long long));

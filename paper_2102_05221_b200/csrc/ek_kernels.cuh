@@ -23,7 +23,7 @@ namespace ekb {
 
 #ifdef EKB_TRACE
 // per-warp timeline of the last k_nn launch (debug builds only): start, end, DP ns, items, DPs
-__device__ unsigned long long g_trace[8192 * 5];
+__device__ unsigned long long g_trace[8192 * 8];
 #endif
 
 // Engine codes: 0..2 diagonal P=4/8/16; 3..5 stripe S=4/8/16 (unbanded);
@@ -519,7 +519,7 @@ struct LazyCand {
 #endif
 // min resident blocks for the dtw/cdtw diagonal 1-NN kernels (0: the compiler's choice)
 #ifndef EKB_NN_GUARD_MINB
-#define EKB_NN_GUARD_MINB 0  // MSM / TWE guarded P=4 band (C4 phase B): 0 = the compiler's choice
+#define EKB_NN_GUARD_MINB 3  // MSM / TWE guarded P=4 band (C4 phase B): 3 blocks (TWE -3%, MSM without spills)
 #endif
 __host__ __device__ constexpr int nn_minb(int kind, int eng) {
   return (kind == K_DTW && eng == E_DIAG4) ? EKB_NN_DTW_MINB
@@ -786,11 +786,11 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
     if (gw < 8192) {
-      g_trace[gw * 5 + 0] = tr_t0;
-      g_trace[gw * 5 + 1] = t1;
-      g_trace[gw * 5 + 2] = tr_dp;
-      g_trace[gw * 5 + 3] = tr_items;
-      g_trace[gw * 5 + 4] = tr_dps;
+      g_trace[gw * 8 + 0] = tr_t0;
+      g_trace[gw * 8 + 1] = t1;
+      g_trace[gw * 8 + 2] = tr_dp;
+      g_trace[gw * 8 + 3] = tr_items;
+      g_trace[gw * 8 + 4] = tr_dps;
     }
   }
 #endif

@@ -288,6 +288,10 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
     yw[(RY - (S + 1) % RY) % RY] = yblk[S];
   };
 
+#ifdef EKB_TRACE
+  unsigned long long tr_t0, tr_blocks = 0, tr_busy = 0, tr_pairs = 0, tr_exh = 0, tr_last_pair = 0, tr_maxblk = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_t0));
+#endif
   for (;;) {
     // ---- publish and refill the idle halves (warp-uniform) ----
     const unsigned idle = __ballot_sync(FULL, !run);
@@ -299,7 +303,16 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
         if (half == h) st = 0;
       }
       int q = 0, c = 0;
-      if (!next_pair(q, c)) continue;
+      if (!next_pair(q, c)) {
+#ifdef EKB_TRACE
+        if (!tr_exh) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_exh));
+#endif
+        continue;
+      }
+#ifdef EKB_TRACE
+      ++tr_pairs;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_last_pair));
+#endif
       const double cq = ld_cut(cutbits + q);
       if (half == h) {
         pq = q;
@@ -322,6 +335,13 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
       }
     }
     if (!__any_sync(FULL, run)) break;
+#ifdef EKB_TRACE
+    {
+      const unsigned rb = __ballot_sync(FULL, run);
+      ++tr_blocks;
+      tr_busy += ((rb & 1u) ? 1 : 0) + ((rb >> 16) & 1u ? 1 : 0);
+    }
+#endif
     // ---- one block of U double steps for both halves ----
     // every lane loads its half's cutoff (pq is always a valid query): no merge of a
     // conditional load, so nothing waits for it before the block's end
@@ -330,16 +350,24 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
     const bool chk = __any_sync(FULL, run && t + 2 * U + 1 >= Tf);
     const R* xblk = xp + I0;
     const R* yblk = yp + J0;
+    // After step RX - 1 the rings are back at phase 0: a half that stopped at the block's
+    // first votes is refilled there (half a block sooner) when there is work left.  (Votes
+    // are self-contained cut tests of their own double step, so their spacing may change.)
+    auto brk = [&](auto S_) -> bool {
+      constexpr int S = decltype(S_)::value;
+      if constexpr (S == RX - 1) return !exhausted && __ballot_sync(FULL, !run) != 0u;
+      return false;
+    };
     if (!chk) {
       auto fast = [&](auto S_) {
         dstep(S_, std::false_type{}, xblk, yblk);
-        return false;
+        return brk(S_);
       };
       unrolled_steps<0, U>(fast);
     } else {
       auto last = [&](auto S_) {
         dstep(S_, std::true_type{}, xblk, yblk);
-        return false;
+        return brk(S_);
       };
       unrolled_steps<0, U>(last);
     }
@@ -349,6 +377,22 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
       cut_hi = hi_word(cut);
     }
   }
+#ifdef EKB_TRACE
+  if (lane == 0) {  // per warp: start, end, busy half-blocks, blocks, pairs (tools/trace_nn.py)
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gw < 8192) {
+      g_trace[gw * 8 + 0] = tr_t0;
+      g_trace[gw * 8 + 1] = t1;
+      g_trace[gw * 8 + 2] = tr_busy;
+      g_trace[gw * 8 + 3] = tr_blocks;
+      g_trace[gw * 8 + 4] = tr_pairs;
+      g_trace[gw * 8 + 5] = tr_exh;
+      g_trace[gw * 8 + 6] = tr_last_pair;
+    }
+  }
+#endif
 }
 
 }  // namespace ekb

@@ -36,3 +36,17 @@ cum = 0
 for k in range(33):
     cum += tot[k]
     print(f"span<={k:2d} lanes: {cum / n:.3f}")
+
+# narrow-window simulation of the same step (EKB_NN2=0 runs the one-pair engine that carries it)
+if hasattr(r.L, "ek_debug_sn_dtw"):
+    sn = r.L.ek_debug_sn_dtw
+    sn.argtypes = [C.POINTER(C.c_ulonglong)]
+    b8 = (C.c_ulonglong * 8)()
+    sn(b8)
+    r.step(s.cuda_stream)
+    torch.cuda.synchronize()
+    sn(b8)
+    names = ["pairs", "narrowed", "overflowed", "votes", "narrow_votes", "narrow_votes_overflowed", "recentrings", "expansions"]
+    d = {n: int(b8[k]) for k, n in enumerate(names)}
+    d["narrow_share"] = d["narrow_votes"] / max(1, d["votes"])
+    print(json.dumps({"narrow_sim": d}))

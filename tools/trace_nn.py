@@ -26,9 +26,9 @@ for _ in range(3):
 torch.cuda.synchronize()
 L = r.L
 L.ek_debug_trace.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-buf = (C.c_ulonglong * (8192 * 5))()
-L.ek_debug_trace(buf, 8192 * 5)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 5).astype(np.float64)
+buf = (C.c_ulonglong * (8192 * 8))()
+L.ek_debug_trace(buf, 8192 * 8)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 8).astype(np.float64)
 a = a[a[:, 1] > 0]
 t0 = a[:, 0].min()
 st, en, dp, it, nd = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, a[:, 2] / 1e3, a[:, 3], a[:, 4]
