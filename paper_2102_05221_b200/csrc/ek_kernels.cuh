@@ -521,13 +521,15 @@ struct LazyCand {
 #ifndef EKB_NN_GUARD_MINB
 #define EKB_NN_GUARD_MINB 3  // MSM / TWE guarded P=4 band (C4 phase B): 3 blocks (TWE -3%, MSM without spills)
 #endif
-__host__ __device__ constexpr int nn_minb(int kind, int eng) {
+// (the FP32 kernels keep the compiler's choice: forcing 3 blocks there let them grow past
+// 4 blocks' worth of registers, C4 FP32 TWE 23.8 -> 27.0 ms)
+__host__ __device__ constexpr int nn_minb(int kind, int eng, int mode) {
   return (kind == K_DTW && eng == E_DIAG4) ? EKB_NN_DTW_MINB
-         : ((kind == K_MSM || kind == K_TWE) && eng == E_GDIAG4) ? EKB_NN_GUARD_MINB : 0;
+         : ((kind == K_MSM || kind == K_TWE) && eng == E_GDIAG4 && (mode & M_F32) == 0) ? EKB_NN_GUARD_MINB : 0;
 }
 
 template <int KIND, int MODE, int ENG>
-__global__ void __launch_bounds__(128, nn_minb(KIND, ENG)) k_nn(const double* __restrict__ Q, const long long* __restrict__ qoff,
+__global__ void __launch_bounds__(128, nn_minb(KIND, ENG, MODE)) k_nn(const double* __restrict__ Q, const long long* __restrict__ qoff,
                                             const int* __restrict__ qlen, int nq, const double* __restrict__ C,
                                             const long long* __restrict__ coff, const int* __restrict__ clen,
                                             int ncand, const int* __restrict__ order, int rank_lo, int rank_mid,
