@@ -757,12 +757,15 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       const int cb = (int)std::min<int64_t>(ncand, k * csz), ce = (int)std::min<int64_t>(ncand, (k + 1) * csz);
       if (nchunk > 0) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[ev0 + k], 0));
       if (ce <= cb) continue;
+      // k_nn2's padded candidate copies come out of the same pass when the fused kernel serves L
+      const bool fuse_pad = use_nn2 && env_pm8_smem(L) <= 200 * 1024;
       CK(envelope_pm(dC, (const long long*)dcoff + cb, L, ce - cb, win < 0 ? L : win, denv.as<float2>() + cb, scr, st,
-                     (int)ncand));
+                     (int)ncand, fuse_pad ? (char*)dcp.p + elem_size(spec) * (size_t)pitch2 * cb : nullptr,
+                     spec->precision, pitch2, kPadG));
       CK(lb_matrix(spec_mode(spec), (const float2*)dqt.as<float2>(), (int)nq, (const float2*)denv.as<float2>(),
                    (int)ncand, cb, ce, L, dkeys.as<float>(), st));
       g_launches += 2;
-      if (use_nn2) {
+      if (use_nn2 && !fuse_pad) {
         CK(nn2_pad(spec->precision, dC, (const long long*)dcoff + cb, ce - cb, L, pitch2,
                    (char*)dcp.p + elem_size(spec) * (size_t)pitch2 * cb, st));
         ++g_launches;

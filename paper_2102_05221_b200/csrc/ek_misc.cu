@@ -492,8 +492,111 @@ cudaError_t envelope(const double* C, const long long* coff, int L, int nser, in
                      cudaStream_t st) {
   return envelope_launch<kEnvPlain>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st);
 }
+// Point-major candidate envelopes for the LB keys, warp per series, eight series per block:
+// each warp builds its series' sparse table in its own shared-memory rows (the same levels
+// and clipped windows as k_envelope, so the same floats), and the block writes its eight
+// series' envelopes transposed, eight consecutive candidates per point (k_envelope's
+// block-per-series writes land one 8-byte value per 32-byte sector).  With `padded`, the
+// warp also writes the padded copy k_nn2 reads (kPadG_ elements of 0.0 before the series, of
+// +inf after it; float in the FP32 mode): one pass over the candidates instead of two.
+constexpr int kEnvPmSeries = 8;
+template <class R>
+__global__ void __launch_bounds__(256) k_envelope_pm8(const double* __restrict__ C, const long long* __restrict__ coff,
+                                                       int L, int nser, int w, float2* __restrict__ env, int stride,
+                                                       R* __restrict__ padded, int pitch, int padg) {
+  extern __shared__ __align__(16) unsigned char envpm_sm[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* const tile = reinterpret_cast<float2*>(envpm_sm);          // [L][8]
+  float* const hi = reinterpret_cast<float*>(tile + (size_t)L * kEnvPmSeries) + (size_t)wib * 4 * L;
+  float* const lo = hi + L;
+  float* const hi2 = hi + 2 * L;
+  float* const lo2 = hi + 3 * L;
+  const int W = min(w, L - 1);
+  const int pmin = 31 - __clz(min(W + 1, L)), pmax = 31 - __clz(min(2 * W + 1, L));
+  const int c0 = blockIdx.x * kEnvPmSeries;
+  const int c = c0 + wib;
+  if (c < nser) {
+    const double* src = C + coff[c];
+    R* pc = padded ? padded + (long long)c * pitch : nullptr;
+    for (int k = lane; k < L; k += 32) {
+      const double x = src[k];
+      hi[k] = __double2float_ru(x);
+      lo[k] = __double2float_rd(x);
+      if (pc) pc[padg + k] = (R)x;
+    }
+    if (pc) {
+      for (int k = lane; k < padg; k += 32) {
+        pc[k] = (R)0.0;
+        pc[padg + L + k] = rinf<R>();
+      }
+    }
+    __syncwarp();
+    for (int p = 1; p <= pmax; ++p) {
+      const int sh = 1 << (p - 1), n = L - (1 << p) + 1;
+      const bool inplace = p <= pmin;
+      float* const dh = inplace ? hi : hi2;
+      float* const dl = inplace ? lo : lo2;
+      for (int base = 0; base < n; base += 128) {  // four values per lane read before any write
+        float vh[4], vl[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int k = base + r * 32 + lane;
+          if (k < n) {
+            vh[r] = tmax(hi[k], hi[k + sh]);
+            vl[r] = tmin(lo[k], lo[k + sh]);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int k = base + r * 32 + lane;
+          if (k < n) {
+            dh[k] = vh[r];
+            dl[k] = vl[r];
+          }
+        }
+        __syncwarp();
+      }
+    }
+    for (int k = lane; k < L; k += 32) {
+      const int a = max(k - W, 0), b = min(k + W, L - 1);
+      const int p = 31 - __clz(b - a + 1);
+      const float* th = p == pmin ? hi : hi2;
+      const float* tl = p == pmin ? lo : lo2;
+      const int b2 = b - (1 << p) + 1;
+      tile[k * kEnvPmSeries + wib] = make_float2(-tmax(th[a], th[b2]), tmin(tl[a], tl[b2]));
+    }
+  }
+  __syncthreads();
+  const int ns = min(kEnvPmSeries, nser - c0);
+  for (int i = threadIdx.x; i < L * kEnvPmSeries; i += blockDim.x) {
+    const int k = i / kEnvPmSeries, sidx = i % kEnvPmSeries;
+    if (sidx < ns) env[(long long)k * stride + c0 + sidx] = tile[i];
+  }
+}
+
+size_t env_pm8_smem(int L) { return (size_t)L * kEnvPmSeries * (sizeof(float2) + 4 * sizeof(float)); }
+
 cudaError_t envelope_pm(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
-                        cudaStream_t st, int stride) {
+                        cudaStream_t st, int stride, void* padded, int padded_f32, int pitch, int padg) {
+  const size_t sm = env_pm8_smem(L);
+  if (nser > 0 && L > 0 && sm <= 200 * 1024) {
+    const unsigned grid = (unsigned)((nser + kEnvPmSeries - 1) / kEnvPmSeries);
+    cudaError_t e;
+    if (padded_f32) {
+      if (sm > 48 * 1024 && (e = cudaFuncSetAttribute((const void*)k_envelope_pm8<float>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+        return e;
+      k_envelope_pm8<float><<<grid, 256, sm, st>>>(C, coff, L, nser, w, env, stride, (float*)padded, pitch, padg);
+    } else {
+      if (sm > 48 * 1024 && (e = cudaFuncSetAttribute((const void*)k_envelope_pm8<double>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+        return e;
+      k_envelope_pm8<double><<<grid, 256, sm, st>>>(C, coff, L, nser, w, env, stride, (double*)padded, pitch, padg);
+    }
+    return cudaGetLastError();
+  }
+  if (padded) return cudaErrorInvalidValue;  // (long series: the caller pads separately)
   return envelope_launch<kEnvPointMajor>(C, coff, L, nser, w, env, nullptr, nullptr, scratch, st, stride);
 }
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,

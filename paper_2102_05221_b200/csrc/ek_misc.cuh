@@ -19,8 +19,12 @@ cudaError_t envelope(const double* C, const long long* coff, int L, int nser, in
                      cudaStream_t st);
 // point-major float2 (-upper, lower) at env[k * nser + c]: the layout k_lb_matrix reads
 // (stride: the row stride of env, >= nser; a chunk of candidates passes env + its first index)
+// padded != null (k_nn2's padded copies, float when padded_f32): written in the same pass;
+// env_pm8_smem(L) > 200 KB (very long series) takes the block-per-series kernel, without padding
 cudaError_t envelope_pm(const double* C, const long long* coff, int L, int nser, int w, float2* env, void* scratch,
-                        cudaStream_t st, int stride);
+                        cudaStream_t st, int stride, void* padded = nullptr, int padded_f32 = 0, int pitch = 0,
+                        int padg = 0);
+size_t env_pm8_smem(int L);
 cudaError_t envelope_exact(const double* C, const long long* coff, int L, int nser, int w, double* up, double* dn,
                            void* scratch, cudaStream_t st);
 
