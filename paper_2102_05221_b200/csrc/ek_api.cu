@@ -4,6 +4,7 @@
 // weight tables (libm exp, kernels.py:80-92) arrive precomputed from the caller.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -979,6 +980,13 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   std::lock_guard<std::mutex> lk(g_mu);
   if (ensure_ctx()) return -1;
   if (n_queries <= 0) return 0;
+  static const bool htime = env_int("EKB_HOST_TIMING", 0) != 0;
+  const auto ht0 = std::chrono::steady_clock::now();
+  auto hlap = [&](const char* what) {
+    if (htime)
+      fprintf(stderr, "ek_nn host %s %.1f us\n", what,
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ht0).count());
+  };
   cudaStream_t st = g_ctx.stream;
   std::vector<int32_t> ql(n_queries), cl(n_cands);
   int32_t mx = 0;
@@ -1014,6 +1022,7 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   // the queries go first on the same copy stream (1/16 of C2's bytes): the LB keys of each
   // candidate chunk need them
   CK(cudaStreamWaitEvent(g_ctx.copy, g_ctx.ev_fork, 0));
+  hlap("first copy enqueued at");
   CK(cudaMemcpyAsync(dq.p, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, g_ctx.copy));
   CK(cudaEventRecord(g_ctx.ev_join, g_ctx.copy));
   if (n_cands > 0) {
@@ -1075,9 +1084,11 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
       return -1;
   }
   // one copy back: five result arrays and the validation flag
+  hlap("all work enqueued at");
   std::vector<int64_t> h(5 * n_queries + 1);
   CK(cudaMemcpyAsync(h.data(), o, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  hlap("results on the host at");
   if (*(const int*)(h.data() + 5 * n_queries)) return fail("%s", kNonFinite);
   std::memcpy(nn_idx, h.data(), 8 * n_queries);
   std::memcpy(nn_dist, h.data() + n_queries, 8 * n_queries);
