@@ -348,6 +348,10 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
     unsigned long long nextcut;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(nextcut) : "l"(cutbits + pq));
     const bool chk = __any_sync(FULL, run && t + 2 * U + 1 >= Tf);
+    if (!run) {  // an idle half's indices would keep advancing past its last series' pads
+      I0 = 0;
+      J0 = 0;
+    }
     const R* xblk = xp + I0;
     const R* yblk = yp + J0;
     // After step RX - 1 the rings are back at phase 0: a half that stopped at the block's
