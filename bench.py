@@ -314,6 +314,20 @@ class Runner:
         ekb.subsequence_search(q, stream, SearchConfig(spec=self.spec, variant="eapruned", normalize=True))
         return q.nbytes + stream.nbytes, 40
 
+    def e2e_pipelined(self, k):
+        """k steps through the public streaming API (NNPipeline, two deep): every step uploads
+        its queries and candidates from pinned host memory and reads its results back, and
+        step i+1's upload overlaps step i's search.  Returns the wall time of the k steps."""
+        import paper_2102_05221_b200 as ekb
+
+        if self.pinned is None:
+            self.pinned = tuple(pinned_copy(a) for a in self.host)
+        Q, C = self.pinned
+        t0 = time.perf_counter()
+        for _ in ekb.nn_batch_stream(self.spec, "eapruned", ((Q, C) for _ in range(k)), precision=self.precision):
+            pass
+        return time.perf_counter() - t0
+
 
 def phase_times(L):
     import ctypes as C
@@ -582,6 +596,18 @@ def run_ours(args):
                     t_e2e.append(time.perf_counter() - t0)
             res["e2e"] = {"value": r.units / float(np.mean(t_e2e)), "unit": r.unit, "h2d_bytes_per_step": int(hb),
                           "d2h_bytes_per_step": int(db), "path": "public Python API (pinned numpy in, numpy out)"}
+            if r.base in NN_NAMES:
+                # the same calls pipelined two deep (NNPipeline): one call's upload overlaps the
+                # previous call's search; the synchronous per-call number stays as e2e_sync
+                k = max(2, min(steps, 10))
+                r.e2e_pipelined(2)  # slots allocated, untimed
+                dt = float(np.mean([r.e2e_pipelined(k) for _ in range(2)]))
+                res["e2e_sync"] = dict(res["e2e"])
+                res["e2e"] = {"value": k * r.units / dt, "unit": r.unit, "h2d_bytes_per_step": int(hb),
+                              "d2h_bytes_per_step": int(db), "steps": k,
+                              "path": "public Python API, streaming (search.NNPipeline: ek_nn_submit / ek_nn_collect, "
+                                      "two batches in flight; pinned numpy in, numpy out, every step's inputs uploaded "
+                                      "and its results read back inside the timed region)"}
         if r.base in NN_NAMES:
             idx = r.out[: r.nq].cpu().numpy().copy()
             if not fp32:
@@ -623,6 +649,8 @@ def run_ours(args):
     }
     if "e2e" in head:
         line["e2e"] = head["e2e"]
+    if "e2e_sync" in head:
+        line["e2e_sync"] = head["e2e_sync"]
     # dram bytes per launch of the dominant kernel from the committed `ncu --set full` summaries
     for name, res in results.items():
         tr = ncu_traffic(name)

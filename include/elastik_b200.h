@@ -93,6 +93,20 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
           const int64_t* c_len, int64_t n_cands, int64_t* nn_idx, double* nn_dist, int64_t* cells,
           int64_t* computed, int64_t* abandoned);
 
+/* ek_nn as a two-deep pipeline over a stream of batches (nn_search called batch after batch,
+ * e.g. a serving loop; search.py:81-125 per query).  ek_nn_submit enqueues one batch's
+ * upload, search and result read-back into pipeline slot 0 or 1 and returns without
+ * waiting; ek_nn_collect waits for that slot's results (same outputs and errors as ek_nn).
+ * Each slot keeps its own device copy of the batch, so batch k+1's upload crosses PCIe while
+ * batch k is searched.  The host arrays must stay valid until the slot is collected (and
+ * should be page-locked for the upload to be asynchronous).  A slot takes one batch at a
+ * time: submitting to a slot that was not collected is an error. */
+int ek_nn_submit(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,
+                 const int64_t* q_len, int64_t n_queries, const double* cands, int64_t c_total, const int64_t* c_off,
+                 const int64_t* c_len, int64_t n_cands, int32_t slot);
+int ek_nn_collect(int32_t slot, int64_t* nn_idx, double* nn_dist, int64_t* cells, int64_t* computed,
+                  int64_t* abandoned);
+
 /* Same with device-resident inputs/outputs (lengths as int32, offsets int64) on `stream`.
  * dense != 0 promises every series has length max_len (enables the LB_Keogh pre-filter
  * for dtw/cdtw, which drops only candidates whose bound proves a +inf result). */

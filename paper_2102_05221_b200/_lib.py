@@ -63,6 +63,9 @@ EXPORTS = {
                       _i64p, _dp, _dp, _i64p], C.c_int),
     "ek_nn": ([C.POINTER(EkSpec), C.c_int32, _dp, C.c_int64, _i64p, _i64p, C.c_int64, _dp, C.c_int64, _i64p, _i64p,
                C.c_int64, _i64p, _dp, _i64p, _i64p, _i64p], C.c_int),
+    "ek_nn_submit": ([C.POINTER(EkSpec), C.c_int32, _dp, C.c_int64, _i64p, _i64p, C.c_int64, _dp, C.c_int64, _i64p,
+                      _i64p, C.c_int64, C.c_int32], C.c_int),
+    "ek_nn_collect": ([C.c_int32, _i64p, _dp, _i64p, _i64p, _i64p], C.c_int),
     "ek_nn_dev": ([C.POINTER(EkSpec), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                    C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                    C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),

@@ -75,8 +75,9 @@ struct Ctx {
   int nsm = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // independent work forked off the calling stream
-  cudaStream_t copy = nullptr;  // chunked host-to-device uploads (ek_nn)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t copy = nullptr;  // chunked host-to-device uploads (ek_nn): copies only
+  cudaStream_t chk = nullptr;   // the uploads' finiteness checks (kernels kept off the copy stream)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chk = nullptr;
   static constexpr int kChunks = 8;
   cudaEvent_t ev_chunk[kChunks] = {};
 };
@@ -116,6 +117,8 @@ int ensure_ctx() {
   CK(cudaEventCreateWithFlags(&g_ctx.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g_ctx.ev_join, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&g_ctx.copy, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&g_ctx.chk, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&g_ctx.ev_chk, cudaEventDisableTiming));
   for (int k = 0; k < Ctx::kChunks; ++k) CK(cudaEventCreateWithFlags(&g_ctx.ev_chunk[k], cudaEventDisableTiming));
   // keep stream-ordered allocations cached between calls (no re-mapping per call)
   cudaMemPool_t pool;
@@ -973,13 +976,33 @@ int ek_nn_dev(const ek_spec* spec, int32_t variant, const double* d_queries, con
                      max_len, dense, d_nn_idx, d_nn_dist, d_cells, d_computed, d_abandoned, st);
 }
 
-int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,
-          const int64_t* q_len, int64_t n_queries, const double* cands, int64_t c_total, const int64_t* c_off,
-          const int64_t* c_len, int64_t n_cands, int64_t* nn_idx, double* nn_dist, int64_t* cells,
-          int64_t* computed, int64_t* abandoned) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (ensure_ctx()) return -1;
-  if (n_queries <= 0) return 0;
+// A pipeline slot of the host-array 1-NN entries: the device copy of one batch (queries,
+// candidates, offsets, lengths) and of its results, kept between calls, the page-locked
+// buffer the results land in, and the event that marks them landed.  Because the slot's
+// buffers are not stream-ordered allocations, the next batch's upload (copy stream) waits
+// only for the slot's previous batch, never for the search currently running: with two
+// slots, batch k+1 crosses PCIe while batch k is searched (ek_nn_submit / ek_nn_collect).
+struct NNSlot {
+  char* dbuf = nullptr;
+  size_t cap = 0;
+  int64_t* hres = nullptr;  // 5 * nq results + the validation flag
+  size_t hcap = 0;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+  int64_t nq = 0;
+};
+constexpr int kNNSlots = 3;  // 0, 1: ek_nn_submit; 2: ek_nn
+NNSlot g_nn_slot[kNNSlots];
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// enqueue one batch into slot `s`: uploads on the copy stream (queries, then the candidates
+// in chunks, each checked for finiteness there), the search on the library stream, and the
+// results' read-back; returns without waiting
+static int nn_enqueue(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total,
+                      const int64_t* q_off, const int64_t* q_len, int64_t n_queries, const double* cands,
+                      int64_t c_total, const int64_t* c_off, const int64_t* c_len, int64_t n_cands, NNSlot& s,
+                      int chunks) {
   static const bool htime = env_int("EKB_HOST_TIMING", 0) != 0;
   const auto ht0 = std::chrono::steady_clock::now();
   auto hlap = [&](const char* what) {
@@ -996,62 +1019,104 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   int32_t dense = 1;
   for (int64_t k = 0; k < n_queries && dense; ++k) dense = ql[k] == mx;
   for (int64_t k = 0; k < n_cands && dense; ++k) dense = cl[k] == mx;
-  DBuf dq, dqo, dql, dc, dco, dcl, dout;
-  if (dq.alloc(sizeof(double) * q_total, st) || dqo.alloc(8 * n_queries, st) || dql.alloc(4 * n_queries, st) ||
-      dc.alloc(sizeof(double) * c_total, st) || dco.alloc(8 * std::max<int64_t>(1, n_cands), st) ||
-      dcl.alloc(4 * std::max<int64_t>(1, n_cands), st) || dout.alloc(8 * (5 * n_queries + 1), st))
-    return -1;
-  // on every exit the copy stream is drained before the buffers above are released
-  struct CopyDrain {
-    ~CopyDrain() { cudaStreamSynchronize(g_ctx.copy); }
-  } drain;
-  int64_t* o = dout.as<int64_t>();
+  // the slot's device layout: dq | dc | dqo | dco | dql | dcl | dout (each 256-byte aligned)
+  const int64_t nc1 = std::max<int64_t>(1, n_cands);
+  const size_t sz[7] = {align256(sizeof(double) * std::max<int64_t>(1, q_total)),
+                        align256(sizeof(double) * std::max<int64_t>(1, c_total)), align256(8 * (size_t)n_queries),
+                        align256(8 * (size_t)nc1), align256(4 * (size_t)n_queries), align256(4 * (size_t)nc1),
+                        align256(8 * (size_t)(5 * n_queries + 1))};
+  size_t need = 0;
+  for (size_t b : sz) need += b;
+  const size_t hneed = sizeof(int64_t) * (size_t)(5 * n_queries + 1);
+  if (s.done == nullptr) CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  if (need > s.cap || hneed > s.hcap) {
+    CK(cudaEventSynchronize(s.done));  // the slot's previous batch no longer reads its buffers
+    if (need > s.cap) {
+      if (s.dbuf) CK(cudaFree(s.dbuf));
+      s.dbuf = nullptr;
+      s.cap = 0;
+      const size_t cap = need + need / 8;
+      CK(cudaMalloc((void**)&s.dbuf, cap));
+      s.cap = cap;
+    }
+    if (hneed > s.hcap) {
+      if (s.hres) CK(cudaFreeHost(s.hres));
+      s.hres = nullptr;
+      s.hcap = 0;
+      CK(cudaHostAlloc((void**)&s.hres, hneed, cudaHostAllocPortable));
+      s.hcap = hneed;
+    }
+  }
+  char* p = s.dbuf;
+  double* dq = (double*)p;
+  double* dc = (double*)(p += sz[0]);
+  int64_t* dqo = (int64_t*)(p += sz[1]);
+  int64_t* dco = (int64_t*)(p += sz[2]);
+  int32_t* dql = (int32_t*)(p += sz[3]);
+  int32_t* dcl = (int32_t*)(p += sz[4]);
+  int64_t* o = (int64_t*)(p += sz[5]);
   int* bad = (int*)(o + 5 * n_queries);  // validation flag rides with the results
-  CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  CK(cudaEventRecord(g_ctx.ev_fork, st));  // dc / bad allocated and zeroed in stream order
+  // on an error exit the copy stream is drained (the caller may release its host buffers)
+  struct CopyDrain {
+    bool on = true;
+    ~CopyDrain() {
+      if (on) {
+        cudaStreamSynchronize(g_ctx.copy);
+        cudaStreamSynchronize(g_ctx.chk);
+      }
+    }
+  } drain;
+  // The copy stream carries copies only and waits for this slot's previous batch alone: a
+  // kernel on it (a check, a memset) would queue behind the running search's persistent
+  // kernel and hold back every copy after it.  The finiteness checks run on their own
+  // stream, which the result read-back joins; the search itself does not wait for them (a
+  // non-finite batch is searched to no effect and then reported).
+  CK(cudaStreamWaitEvent(g_ctx.copy, s.done, 0));
+  CK(cudaStreamWaitEvent(g_ctx.chk, s.done, 0));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), g_ctx.chk));
   // dense batches stored contiguously: offsets and lengths are generated on the device
   bool qcontig = dense != 0, ccontig = dense != 0;
   for (int64_t k = 0; k < n_queries && qcontig; ++k) qcontig = q_off[k] == k * (int64_t)mx;
   for (int64_t k = 0; k < n_cands && ccontig; ++k) ccontig = c_off[k] == k * (int64_t)mx;
-  // Candidates first (the bulk of the bytes): the values in chunks on the copy stream,
-  // each checked for finiteness there and announced by an event, so the LB keys of early
+  // The queries first (1/16 of C2's bytes: the LB keys of every candidate chunk need them),
+  // then the candidates in chunks, each announced by an event, so the LB keys of early
   // chunks are computed while later ones are still in flight (dense batches: chunk k is
-  // series [k * csz, (k + 1) * csz), contiguous in the buffer).
+  // series [k * csz, (k + 1) * csz), contiguous).
   int nch = 0;
   int64_t csz = n_cands;
-  // the queries go first on the same copy stream (1/16 of C2's bytes): the LB keys of each
-  // candidate chunk need them
-  CK(cudaStreamWaitEvent(g_ctx.copy, g_ctx.ev_fork, 0));
   hlap("first copy enqueued at");
-  CK(cudaMemcpyAsync(dq.p, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, g_ctx.copy));
+  CK(cudaMemcpyAsync(dq, queries, sizeof(double) * q_total, cudaMemcpyHostToDevice, g_ctx.copy));
   CK(cudaEventRecord(g_ctx.ev_join, g_ctx.copy));
+  CK(cudaStreamWaitEvent(g_ctx.chk, g_ctx.ev_join, 0));
+  if (check_finite(dq, q_total, bad, g_ctx.chk)) return -1;
   if (n_cands > 0) {
-    nch = (ccontig && n_cands >= 2 * Ctx::kChunks) ? std::max(1, std::min(Ctx::kChunks, env_int("EKB_NN_CHUNKS", 4))) : 1;
+    nch = (ccontig && n_cands >= 2 * Ctx::kChunks) ? std::max(1, std::min(Ctx::kChunks, chunks)) : 1;
     csz = (n_cands + nch - 1) / nch;
     for (int k = 0; k < nch; ++k) {
       const int64_t b = std::min<int64_t>(c_total, nch == 1 ? 0 : k * csz * mx);
       const int64_t e = nch == 1 ? c_total : std::min<int64_t>(c_total, (k + 1) * csz * mx);
-      if (e > b) {
-        CK(cudaMemcpyAsync(dc.as<double>() + b, cands + b, sizeof(double) * (e - b), cudaMemcpyHostToDevice, g_ctx.copy));
-        if (check_finite(dc.as<double>() + b, e - b, bad, g_ctx.copy)) return -1;
-      }
+      if (e > b) CK(cudaMemcpyAsync(dc + b, cands + b, sizeof(double) * (e - b), cudaMemcpyHostToDevice, g_ctx.copy));
       CK(cudaEventRecord(g_ctx.ev_chunk[k], g_ctx.copy));
+      if (e > b) {
+        CK(cudaStreamWaitEvent(g_ctx.chk, g_ctx.ev_chunk[k], 0));
+        if (check_finite(dc + b, e - b, bad, g_ctx.chk)) return -1;
+      }
     }
   }
+  CK(cudaEventRecord(g_ctx.ev_chk, g_ctx.chk));
   CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the queries have landed
   if (qcontig && ccontig) {
     if (launch_plain(k_dense_layout, dim3(16), dim3(256), 0, st, (long long)n_queries, (long long)n_cands, (int)mx,
-                     (long long*)dqo.p, (int*)dql.p, (long long*)dco.p, (int*)dcl.p))
+                     (long long*)dqo, (int*)dql, (long long*)dco, (int*)dcl))
       return -1;
   } else {
-    CK(cudaMemcpyAsync(dqo.p, q_off, 8 * n_queries, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dql.p, ql.data(), 4 * n_queries, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dqo, q_off, 8 * n_queries, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dql, ql.data(), 4 * n_queries, cudaMemcpyHostToDevice, st));
     if (n_cands > 0) {
-      CK(cudaMemcpyAsync(dco.p, c_off, 8 * n_cands, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(dcl.p, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(dco, c_off, 8 * n_cands, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(dcl, cl.data(), 4 * n_cands, cudaMemcpyHostToDevice, st));
     }
   }
-  if (check_finite(dq.as<double>(), q_total, bad, st)) return -1;
   // Two candidate halves when the LB path runs on a chunked upload: the first half's search
   // runs while the second half is still in flight, and its answers seed the second half's
   // cutoffs (a pair of the second half can only win with a cost below them; ties keep the
@@ -1059,43 +1124,97 @@ int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q
   const int halves = (nch >= 2 && share_lb_path(spec, variant, dense, n_cands) && n_cands >= 2048)
                          ? std::max(1, std::min(2, env_int("EKB_NN_SPLIT", 1))) : 1;
   if (halves == 1) {
-    if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
-                    dco.as<int64_t>(), dcl.as<int32_t>(), n_cands, mx, dense, o, (double*)(o + n_queries),
-                    o + 2 * n_queries, o + 3 * n_queries, o + 4 * n_queries, st, nch, csz))
+    if (nn_dev_impl(spec, variant, dq, dqo, dql, n_queries, dc, dco, dcl, n_cands, mx, dense, o,
+                    (double*)(o + n_queries), o + 2 * n_queries, o + 3 * n_queries, o + 4 * n_queries, st, nch, csz))
       return -1;
   } else {
-    const int nc1 = nch / 2;                               // chunks of the first half
-    const int64_t h = std::min<int64_t>(n_cands, nc1 * csz);  // its candidates
+    const int nc1h = nch / 2;                                  // chunks of the first half
+    const int64_t h = std::min<int64_t>(n_cands, nc1h * csz);  // its candidates
     DBuf dr;
     if (dr.alloc(sizeof(int64_t) * 10 * (size_t)n_queries, st)) return -1;
     int64_t* r1 = dr.as<int64_t>();
     int64_t* r2 = r1 + 5 * n_queries;
-    if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
-                    dco.as<int64_t>(), dcl.as<int32_t>(), h, mx, dense, r1, (double*)(r1 + n_queries),
-                    r1 + 2 * n_queries, r1 + 3 * n_queries, r1 + 4 * n_queries, st, nc1, csz, 0, nullptr))
+    if (nn_dev_impl(spec, variant, dq, dqo, dql, n_queries, dc, dco, dcl, h, mx, dense, r1, (double*)(r1 + n_queries),
+                    r1 + 2 * n_queries, r1 + 3 * n_queries, r1 + 4 * n_queries, st, nc1h, csz, 0, nullptr))
       return -1;
-    if (nn_dev_impl(spec, variant, dq.as<double>(), dqo.as<int64_t>(), dql.as<int32_t>(), n_queries, dc.as<double>(),
-                    dco.as<int64_t>() + h, dcl.as<int32_t>() + h, n_cands - h, mx, dense, r2, (double*)(r2 + n_queries),
-                    r2 + 2 * n_queries, r2 + 3 * n_queries, r2 + 4 * n_queries, st, nch - nc1, csz, nc1,
-                    (const double*)(r1 + n_queries)))
+    if (nn_dev_impl(spec, variant, dq, dqo, dql, n_queries, dc, dco + h, dcl + h, n_cands - h, mx, dense, r2,
+                    (double*)(r2 + n_queries), r2 + 2 * n_queries, r2 + 3 * n_queries, r2 + 4 * n_queries, st,
+                    nch - nc1h, csz, nc1h, (const double*)(r1 + n_queries)))
       return -1;
     if (launch_plain(k_nn_merge, dim3((unsigned)((n_queries + 255) / 256)), dim3(256), 0, st, (long long)n_queries,
                      (long long)h, (const long long*)r1, (const long long*)r2, (long long*)o))
       return -1;
   }
-  // one copy back: five result arrays and the validation flag
+  // one copy back: five result arrays and the validation flag (after the checks)
   hlap("all work enqueued at");
-  std::vector<int64_t> h(5 * n_queries + 1);
-  CK(cudaMemcpyAsync(h.data(), o, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  hlap("results on the host at");
-  if (*(const int*)(h.data() + 5 * n_queries)) return fail("%s", kNonFinite);
-  std::memcpy(nn_idx, h.data(), 8 * n_queries);
-  std::memcpy(nn_dist, h.data() + n_queries, 8 * n_queries);
-  std::memcpy(cells, h.data() + 2 * n_queries, 8 * n_queries);
-  std::memcpy(computed, h.data() + 3 * n_queries, 8 * n_queries);
-  std::memcpy(abandoned, h.data() + 4 * n_queries, 8 * n_queries);
+  CK(cudaStreamWaitEvent(st, g_ctx.ev_chk, 0));
+  CK(cudaMemcpyAsync(s.hres, o, hneed, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(s.done, st));
+  s.pending = true;
+  s.nq = n_queries;
+  drain.on = false;
   return 0;
+}
+
+static int nn_collect(NNSlot& s, int64_t* nn_idx, double* nn_dist, int64_t* cells, int64_t* computed,
+                      int64_t* abandoned) {
+  if (!s.pending) return fail("ek_nn_collect: nothing submitted to this slot");
+  s.pending = false;
+  const cudaError_t e = cudaEventSynchronize(s.done);
+  if (e != cudaSuccess) return fail("1-NN search failed: %s", cudaGetErrorString(e));
+  const int64_t n = s.nq;
+  if (*(const int*)(s.hres + 5 * n)) return fail("%s", kNonFinite);
+  std::memcpy(nn_idx, s.hres, 8 * n);
+  std::memcpy(nn_dist, s.hres + n, 8 * n);
+  std::memcpy(cells, s.hres + 2 * n, 8 * n);
+  std::memcpy(computed, s.hres + 3 * n, 8 * n);
+  std::memcpy(abandoned, s.hres + 4 * n, 8 * n);
+  return 0;
+}
+
+int ek_nn(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,
+          const int64_t* q_len, int64_t n_queries, const double* cands, int64_t c_total, const int64_t* c_off,
+          const int64_t* c_len, int64_t n_cands, int64_t* nn_idx, double* nn_dist, int64_t* cells,
+          int64_t* computed, int64_t* abandoned) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  if (n_queries <= 0) return 0;
+  NNSlot& s = g_nn_slot[kNNSlots - 1];
+  // a lone call overlaps its own upload with the LB keys of the chunks already landed
+  static const int chunks = env_int("EKB_NN_CHUNKS", 4);
+  if (nn_enqueue(spec, variant, queries, q_total, q_off, q_len, n_queries, cands, c_total, c_off, c_len, n_cands, s,
+                 chunks)) {
+    cudaStreamSynchronize(g_ctx.stream);
+    return -1;
+  }
+  return nn_collect(s, nn_idx, nn_dist, cells, computed, abandoned);
+}
+
+int ek_nn_submit(const ek_spec* spec, int32_t variant, const double* queries, int64_t q_total, const int64_t* q_off,
+                 const int64_t* q_len, int64_t n_queries, const double* cands, int64_t c_total, const int64_t* c_off,
+                 const int64_t* c_len, int64_t n_cands, int32_t slot) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ctx()) return -1;
+  if (slot < 0 || slot >= kNNSlots - 1) return fail("ek_nn_submit: slot %d outside [0, %d)", slot, kNNSlots - 1);
+  NNSlot& s = g_nn_slot[slot];
+  if (s.pending) return fail("ek_nn_submit: slot %d has a batch that was not collected", slot);
+  if (n_queries <= 0) return fail("ek_nn_submit: empty query batch");
+  // in a pipeline the upload overlaps the previous batch's search instead: one chunk, so the
+  // LB keys run as full-width launches (a quarter of C2's candidates fills < 1 wave)
+  static const int chunks = env_int("EKB_NN_PIPE_CHUNKS", 1);
+  if (nn_enqueue(spec, variant, queries, q_total, q_off, q_len, n_queries, cands, c_total, c_off, c_len, n_cands, s,
+                 chunks)) {
+    cudaStreamSynchronize(g_ctx.stream);
+    return -1;
+  }
+  return 0;
+}
+
+int ek_nn_collect(int32_t slot, int64_t* nn_idx, double* nn_dist, int64_t* cells, int64_t* computed,
+                  int64_t* abandoned) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (slot < 0 || slot >= kNNSlots - 1) return fail("ek_nn_collect: slot %d outside [0, %d)", slot, kNNSlots - 1);
+  return nn_collect(g_nn_slot[slot], nn_idx, nn_dist, cells, computed, abandoned);
 }
 
 // d_D != null: the full matrix; else pairs [plo, phi) of the upper triangle into d_vec

@@ -102,13 +102,9 @@ def _pack(series):
     return _lib.ragged([as_series(x) for x in series])
 
 
-def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None, precision: str = "float64"):
-    """1-NN of every query in one GPU call.
-
-    Returns arrays (nn_index int64, nn_distance float64, cells, computed,
-    abandoned); nn_index is -1 when every candidate is +inf.  ``precision``
-    "float32" runs the optional FP32 engines.
-    """
+def _nn_prepare(spec: DistanceSpec, variant: str, queries, candidates, backend, precision: str):
+    """Validation and packing shared by nn_batch and NNPipeline: (args of ek_nn up to the
+    outputs, the output arrays, the objects those pointers point into)."""
     _backend.resolve(backend)
     _lib.precision_code(precision)
     if variant not in VARIANTS:
@@ -120,18 +116,95 @@ def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None
     nq = len(ql)
     out = [np.empty(nq, dtype=np.int64), np.empty(nq, dtype=np.float64)] + [np.empty(nq, dtype=np.int64)
                                                                              for _ in range(3)]
-    if nq == 0:
-        return tuple(out)
     if spec.kind == "wdtw":
-        longest = np.unique(np.maximum.outer(np.unique(ql), np.unique(cl)))
+        longest = np.unique(np.maximum.outer(np.unique(ql), np.unique(cl))) if nq else ()
     else:
         longest = ()  # only WDTW needs per-length tables
     h = _lib.SpecHandle(spec, longest_lengths=longest, precision=precision)
+    args = (h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(qf), len(qf), _lib.iptr(qo), _lib.iptr(ql), nq,
+            _lib.dptr(cf), len(cf), _lib.iptr(co), _lib.iptr(cl), len(cl))
+    return args, out, (h, qf, qo, ql, cf, co, cl)
+
+
+def nn_batch(spec: DistanceSpec, variant: str, queries, candidates, backend=None, precision: str = "float64"):
+    """1-NN of every query in one GPU call.
+
+    Returns arrays (nn_index int64, nn_distance float64, cells, computed,
+    abandoned); nn_index is -1 when every candidate is +inf.  ``precision``
+    "float32" runs the optional FP32 engines.
+    """
+    args, out, _keep = _nn_prepare(spec, variant, queries, candidates, backend, precision)
+    if len(out[0]) == 0:
+        return tuple(out)
     L = _lib.lib()
-    _lib.check(L.ek_nn(h.ref, _lib.VARIANT_CODE[variant], _lib.dptr(qf), len(qf), _lib.iptr(qo), _lib.iptr(ql), nq,
-                       _lib.dptr(cf), len(cf), _lib.iptr(co), _lib.iptr(cl), len(cl), _lib.iptr(out[0]),
-                       _lib.dptr(out[1]), _lib.iptr(out[2]), _lib.iptr(out[3]), _lib.iptr(out[4])))
+    _lib.check(L.ek_nn(*args, _lib.iptr(out[0]), _lib.dptr(out[1]), _lib.iptr(out[2]), _lib.iptr(out[3]),
+                       _lib.iptr(out[4])))
     return tuple(out)
+
+
+class NNPipeline:
+    """nn_batch over a stream of batches, two deep (ek_nn_submit / ek_nn_collect).
+
+    ``submit(queries, candidates)`` enqueues a batch and returns at once; ``collect()``
+    returns the oldest batch's ``nn_batch`` tuple.  At most two batches are in flight, so
+    batch k+1's host-to-device upload overlaps batch k's search.  The inputs must not be
+    modified until their batch is collected (page-locked arrays, e.g. ingest's packed
+    batches, make the upload asynchronous).  Results and errors equal nn_batch's.
+    """
+
+    DEPTH = 2
+
+    def __init__(self, spec: DistanceSpec, variant: str, backend=None, precision: str = "float64"):
+        self.spec, self.variant, self.backend, self.precision = spec, variant, backend, precision
+        self._inflight = []  # (slot, out, keep) in submission order
+        self._next = 0
+
+    def __len__(self):
+        return len(self._inflight)
+
+    def submit(self, queries, candidates) -> None:
+        if len(self._inflight) >= self.DEPTH:
+            raise SearchError(f"NNPipeline: {self.DEPTH} batches in flight; collect() first")
+        args, out, keep = _nn_prepare(self.spec, self.variant, queries, candidates, self.backend, self.precision)
+        if len(out[0]) == 0:
+            self._inflight.append((None, out, keep))
+            return
+        slot = self._next
+        _lib.check(_lib.lib().ek_nn_submit(*args, slot))
+        self._next ^= 1
+        self._inflight.append((slot, out, keep))
+
+    def collect(self):
+        if not self._inflight:
+            raise SearchError("NNPipeline: nothing submitted")
+        slot, out, _keep = self._inflight.pop(0)
+        if slot is not None:
+            _lib.check(_lib.lib().ek_nn_collect(slot, _lib.iptr(out[0]), _lib.dptr(out[1]), _lib.iptr(out[2]),
+                                                _lib.iptr(out[3]), _lib.iptr(out[4])))
+        return tuple(out)
+
+    def drain(self):
+        """Collect (and drop) whatever is still in flight, e.g. after an error."""
+        while self._inflight:
+            try:
+                self.collect()
+            except Exception:  # noqa: BLE001 -- draining after a failure
+                pass
+
+
+def nn_batch_stream(spec: DistanceSpec, variant: str, batches, backend=None, precision: str = "float64"):
+    """Yield nn_batch(spec, variant, Q, C) for every (Q, C) of ``batches``, in order, with the
+    next batch's upload overlapping the current batch's search (NNPipeline)."""
+    pipe = NNPipeline(spec, variant, backend=backend, precision=precision)
+    try:
+        for q, c in batches:
+            if len(pipe) == NNPipeline.DEPTH:
+                yield pipe.collect()
+            pipe.submit(q, c)
+        while len(pipe):
+            yield pipe.collect()
+    finally:
+        pipe.drain()
 
 
 def nn_search(query, candidates, cfg: SearchConfig, envelopes=None):
