@@ -988,6 +988,7 @@ struct NNSlot {
   int64_t* hres = nullptr;  // 5 * nq results + the validation flag
   size_t hcap = 0;
   cudaEvent_t done = nullptr;
+  cudaStream_t st = nullptr;  // the slot's search stream (null: the library stream)
   bool pending = false;
   int64_t nq = 0;
 };
@@ -1010,7 +1011,7 @@ static int nn_enqueue(const ek_spec* spec, int32_t variant, const double* querie
       fprintf(stderr, "ek_nn host %s %.1f us\n", what,
               std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ht0).count());
   };
-  cudaStream_t st = g_ctx.stream;
+  cudaStream_t st = s.st ? s.st : g_ctx.stream;
   std::vector<int32_t> ql(n_queries), cl(n_cands);
   int32_t mx = 0;
   for (int64_t k = 0; k < n_queries; ++k) mx = std::max(mx, ql[k] = (int32_t)q_len[k]);
@@ -1198,13 +1199,18 @@ int ek_nn_submit(const ek_spec* spec, int32_t variant, const double* queries, in
   if (slot < 0 || slot >= kNNSlots - 1) return fail("ek_nn_submit: slot %d outside [0, %d)", slot, kNNSlots - 1);
   NNSlot& s = g_nn_slot[slot];
   if (s.pending) return fail("ek_nn_submit: slot %d has a batch that was not collected", slot);
+  // Each pipeline slot searches on its own stream: batch k+1's LB keys and the first blocks
+  // of its phase B take the SMs that batch k's phase B releases in its tail (the last long
+  // DPs), instead of waiting for its last block.  EKB_NN_PIPE_STREAMS=0: the library stream.
+  static const bool own = env_int("EKB_NN_PIPE_STREAMS", 1) != 0;
+  if (own && !s.st) CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
   if (n_queries <= 0) return fail("ek_nn_submit: empty query batch");
   // in a pipeline the upload overlaps the previous batch's search instead: one chunk, so the
   // LB keys run as full-width launches (a quarter of C2's candidates fills < 1 wave)
   static const int chunks = env_int("EKB_NN_PIPE_CHUNKS", 1);
   if (nn_enqueue(spec, variant, queries, q_total, q_off, q_len, n_queries, cands, c_total, c_off, c_len, n_cands, s,
                  chunks)) {
-    cudaStreamSynchronize(g_ctx.stream);
+    cudaStreamSynchronize(s.st ? s.st : g_ctx.stream);
     return -1;
   }
   return 0;
