@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <map>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -129,16 +130,73 @@ int ensure_ctx() {
   return 0;
 }
 
-// RAII stream-ordered device allocation
+// Per-stream workspace of the multi-phase entries (nn_dev_impl): one cached stream-ordered
+// allocation per launching stream, handed out by bumping a pointer, instead of a dozen
+// cudaMallocAsync / cudaFreeAsync pairs per call (each a driver call on the launch path:
+// they delayed C2's first long kernel by ~30 us per step).  Reuse across calls is ordered
+// by the stream itself; work a call forks to other streams is joined back before it ends.
+// A call that outgrows the workspace falls back to cudaMallocAsync for the excess, and the
+// next call on that stream starts with a workspace of the size it needed.
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, off = 0, want = 0;
+};
+std::map<cudaStream_t, Arena> g_arenas;
+Arena* g_arena_cur = nullptr;
+constexpr size_t kArenaAlign = 512;
+
+struct ArenaScope {
+  Arena* prev;
+  bool on = false;
+  ArenaScope(cudaStream_t st, bool enable) : prev(g_arena_cur) {
+    if (!enable || g_arena_cur) return;  // (a nested scope keeps allocating after the outer one's buffers)
+    if (g_arenas.size() > 16 && !g_arenas.count(st)) {  // streams come and go: drop idle workspaces
+      cudaDeviceSynchronize();
+      for (auto& kv : g_arenas)
+        if (kv.second.base) cudaFree(kv.second.base);
+      g_arenas.clear();
+    }
+    Arena& a = g_arenas[st];
+    if (a.want > a.cap) {
+      const size_t cap = a.want + a.want / 8;
+      // plain cudaMalloc / cudaFree: both synchronise the device, so no stream still uses the old block
+      if (a.base) cudaFree(a.base);
+      a.base = nullptr;
+      a.cap = 0;
+      if (cudaMalloc((void**)&a.base, cap) == cudaSuccess) a.cap = cap;
+      else cudaGetLastError();
+    }
+    a.off = 0;
+    a.want = 0;
+    g_arena_cur = &a;
+    on = true;
+  }
+  ~ArenaScope() {
+    if (on) g_arena_cur = prev;
+  }
+};
+
+// RAII device allocation: from the active workspace, else stream-ordered
 struct DBuf {
   void* p = nullptr;
   cudaStream_t s = nullptr;
+  bool pooled = false;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
-  ~DBuf() { if (p) cudaFreeAsync(p, s); }
+  ~DBuf() { if (p && !pooled) cudaFreeAsync(p, s); }
   int alloc(size_t bytes, cudaStream_t st) {
     s = st;
     if (bytes == 0) bytes = 8;
+    if (Arena* a = g_arena_cur) {
+      const size_t b = (bytes + kArenaAlign - 1) & ~(kArenaAlign - 1);
+      a->want += b;
+      if (a->off + b <= a->cap) {
+        p = a->base + a->off;
+        a->off += b;
+        pooled = true;
+        return 0;
+      }
+    }
     cudaError_t e = cudaMallocAsync(&p, bytes, st);
     if (e != cudaSuccess) return fail("cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
     return 0;
@@ -664,6 +722,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   if (variant < 0 || variant > 3) return fail("unknown variant code %d", variant);
   if (nq <= 0) return 0;
   if (ncand <= 0) return fail("candidate set is empty");
+  ArenaScope ws(st, env_int("EKB_WORKSPACE", 1) != 0);  // every DBuf below comes out of the stream's workspace
   mark_reset();
   mark(st, "start");
   const bool lb_chunks = share_lb_path(spec, variant, dense, ncand);
@@ -694,12 +753,30 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   acc.fin_count = acc.idx + nq;
   acc.fin = dfin.as<long long>();
   acc.fin_cost = (double*)(acc.fin + npairs);
-  if (launch_plain(k_nn_acc_init, dim3((unsigned)std::min<long long>(64, (nq + 255) / 256)), dim3(256), 0, st, acc,
-                   (int)nq))
-    return -1;
-  // ints 8, 9: guarded-band overflows and their redo counter; 32 / 64 / 96: the k_nn work
-  // counters (kNnCounters x u64) of phase A and of phase B's launches
-  CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 128, st));
+  // The small initialisations (result accumulators, work counters, cutoffs, stop ranks): on
+  // the LB path they run on the side stream next to the envelope / key kernels and are
+  // joined before the seed; otherwise on the launching stream.
+  // ints 8, 9 of dcnt: guarded-band overflows and their redo counter; 32 / 64 / 96: the k_nn
+  // work counters (kNnCounters x u64) of phase A and of phase B's launches
+  DBuf dqstop;
+  auto small_inits = [&](cudaStream_t s2) -> int {
+    if (launch_plain(k_nn_acc_init, dim3((unsigned)std::min<long long>(64, (nq + 255) / 256)), dim3(256), 0, s2, acc,
+                     (int)nq))
+      return -1;
+    CK(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * 128, s2));
+    if (launch_plain(k_fill_u64, dim3(64), dim3(256), 0, s2, dcut.as<unsigned long long>(), (long long)nq,
+                     0x7ff0000000000000ULL))
+      return -1;
+    // LB path: per-query stop ranks (ncand = none yet)
+    if (lb_chunks) {
+      if (dqstop.alloc(sizeof(int) * (size_t)(nq + 1), st)) return -1;
+      if (launch_plain(k_fill_i32, dim3((unsigned)std::min<long long>(64, (nq + 256) / 256)), dim3(256), 0, s2,
+                       dqstop.as<int>(), (long long)nq, (int)ncand))
+        return -1;
+    }
+    return 0;
+  };
+  if (!lb_chunks && small_inits(st)) return -1;
   int* const ovf_count = dcnt.as<int>() + 8;  // guarded-band overflows (phase B) and their redo counter
   // phase B engine: with a cutoff, wide bands run as a guarded P=8 band (EAPruned's pruned
   // columns skipped wholesale; overflows are redone by k_nn_fix).  ERP keeps its window
@@ -744,35 +821,48 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       scr = denvs.p;
       scr2 = denvs2.p;
     }
-    CK(cudaEventRecord(g_ctx.ev_fork, st));
-    CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_fork, 0));
-    CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr2, g_ctx.side));
-    CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
     DBuf dqt;
     if (dkeys.alloc(sizeof(float) * (size_t)npairs, st) || dqt.alloc(sizeof(float2) * (size_t)nq * L, st)) return -1;
-    CK(lb_qprep(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, L, dqt.as<float2>(), st));
-    if (use_nn2) {
-      CK(nn2_pad(spec->precision, dQ, (const long long*)dqoff, (int)nq, L, pitch2, dqp.p, st));
-      ++g_launches;
-    }
+    // the queries' side of the keys (prepared points, padded copies) and, on the side
+    // stream, their envelopes for the reverse bound and the small initialisations
+    CK(cudaEventRecord(g_ctx.ev_fork, st));  // the inputs are ordered on st
+    auto query_prep = [&]() -> int {
+      CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_fork, 0));
+      CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr2, g_ctx.side));
+      if (small_inits(g_ctx.side)) return -1;
+      CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
+      CK(lb_qprep(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, L, dqt.as<float2>(), st));
+      if (use_nn2) {
+        CK(nn2_pad(spec->precision, dQ, (const long long*)dqoff, (int)nq, L, pitch2, dqp.p, st));
+        ++g_launches;
+      }
+      return 0;
+    };
+    // A chunked upload delivers the queries first; resident inputs start with the first long
+    // kernel (the candidates' envelopes) so the host gets ahead of the device at once.
+    if (nchunk > 0 && query_prep()) return -1;
     const int nch = nchunk > 0 ? nchunk : 1;
     const int64_t csz = nchunk > 0 ? chunk : ncand;
     for (int k = 0; k < nch; ++k) {
       const int cb = (int)std::min<int64_t>(ncand, k * csz), ce = (int)std::min<int64_t>(ncand, (k + 1) * csz);
       if (nchunk > 0) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[ev0 + k], 0));
-      if (ce <= cb) continue;
-      // k_nn2's padded candidate copies come out of the same pass when the fused kernel serves L
-      const bool fuse_pad = use_nn2 && env_pm8_smem(L) <= 200 * 1024;
-      CK(envelope_pm(dC, (const long long*)dcoff + cb, L, ce - cb, win < 0 ? L : win, denv.as<float2>() + cb, scr, st,
-                     (int)ncand, fuse_pad ? (char*)dcp.p + elem_size(spec) * (size_t)pitch2 * cb : nullptr,
-                     spec->precision, pitch2, kPadG));
-      CK(lb_matrix(spec_mode(spec), (const float2*)dqt.as<float2>(), (int)nq, (const float2*)denv.as<float2>(),
-                   (int)ncand, cb, ce, L, dkeys.as<float>(), st));
-      g_launches += 2;
-      if (use_nn2 && !fuse_pad) {
-        CK(nn2_pad(spec->precision, dC, (const long long*)dcoff + cb, ce - cb, L, pitch2,
-                   (char*)dcp.p + elem_size(spec) * (size_t)pitch2 * cb, st));
-        ++g_launches;
+      if (ce > cb) {
+        // k_nn2's padded candidate copies come out of the same pass when the fused kernel serves L
+        const bool fuse_pad = use_nn2 && env_pm8_smem(L) <= 200 * 1024;
+        CK(envelope_pm(dC, (const long long*)dcoff + cb, L, ce - cb, win < 0 ? L : win, denv.as<float2>() + cb, scr, st,
+                       (int)ncand, fuse_pad ? (char*)dcp.p + elem_size(spec) * (size_t)pitch2 * cb : nullptr,
+                       spec->precision, pitch2, kPadG));
+        if (nchunk == 0 && k == 0 && query_prep()) return -1;
+        CK(lb_matrix(spec_mode(spec), (const float2*)dqt.as<float2>(), (int)nq, (const float2*)denv.as<float2>(),
+                     (int)ncand, cb, ce, L, dkeys.as<float>(), st));
+        g_launches += 2;
+        if (use_nn2 && !fuse_pad) {
+          CK(nn2_pad(spec->precision, dC, (const long long*)dcoff + cb, ce - cb, L, pitch2,
+                     (char*)dcp.p + elem_size(spec) * (size_t)pitch2 * cb, st));
+          ++g_launches;
+        }
+      } else if (nchunk == 0 && k == 0 && query_prep()) {
+        return -1;
       }
     }
     mark(st, "lb_keys");
@@ -809,9 +899,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // 2. cutoff seed: the least exact diagonal upper bound over each query's top-ranked
   //    candidates (one on the Euclidean ranking, whose top candidate minimises that bound
   //    approximately; several on the LB ranking)
-  if (launch_plain(k_fill_u64, dim3(64), dim3(256), 0, st, dcut.as<unsigned long long>(), (long long)nq,
-                   0x7ff0000000000000ULL))
-    return -1;
+  if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the side stream: query envelopes, initialisations
   // a caller's starting cutoffs (ek_nn's second candidate half: the first half's answers)
   if (d_cut0 && share &&
       launch_plain(k_cut_from, dim3((unsigned)((nq + 255) / 256)), dim3(256), 0, st, dcut.as<unsigned long long>(),
@@ -871,15 +959,6 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       return -1;
   }
   mark(st, "nn_phaseA");
-  if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the LB keys and envelopes (side stream)
-  // LB path: per-query stop ranks (ncand = none yet) and the count of stopped queries
-  DBuf dqstop;
-  if (use_lb) {
-    if (dqstop.alloc(sizeof(int) * (size_t)(nq + 1), st)) return -1;
-    if (launch_plain(k_fill_i32, dim3((unsigned)std::min<long long>(64, (nq + 256) / 256)), dim3(256), 0, st,
-                     dqstop.as<int>(), (long long)nq, (int)ncand))
-      return -1;
-  }
   // phase B, one launch of two segments: the best ranks (where the survivors concentrate)
   // in small items for load balance, the rest in larger ones.  Without the LB path:
   // 4 + 64 ranks one pair per item, then items of 8 (measured best on C2 before the LB
