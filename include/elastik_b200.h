@@ -192,7 +192,9 @@ int ek_znormalize_dev(const double* d_in, const int64_t* d_off, const int32_t* d
 int64_t ek_launch_count(int32_t reset);
 
 /* Measurement helpers (bench.py): record CUDA events between the phases of the
- * next ek_nn / ek_pairwise / ek_subseq call (host or _dev); read back per-phase device times. */
+ * next ek_nn / ek_pairwise / ek_subseq call (host or _dev); read back per-phase device times.
+ * on = 1: every phase; on = 2: only the marks that bracket the DP kernels of a 1-NN call
+ * (fewer events inside a timed step); 0: none. */
 void ek_set_profiling(int32_t on);
 int32_t ek_phase_times(double* ms, const char** names, int32_t max);
 

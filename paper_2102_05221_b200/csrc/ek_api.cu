@@ -78,7 +78,7 @@ struct Ctx {
   cudaStream_t side = nullptr;  // independent work forked off the calling stream
   cudaStream_t copy = nullptr;  // chunked host-to-device uploads (ek_nn): copies only
   cudaStream_t chk = nullptr;   // the uploads' finiteness checks (kernels kept off the copy stream)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chk = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chk = nullptr, ev_q = nullptr;
   static constexpr int kChunks = 8;
   cudaEvent_t ev_chunk[kChunks] = {};
 };
@@ -86,7 +86,7 @@ Ctx g_ctx;
 std::mutex g_mu;
 
 // optional phase timing (bench.py): events recorded on the launching stream
-bool g_prof = false;
+int g_prof = 0;  // 1: every phase mark; 2: only the marks that bracket the DP kernels
 constexpr int kMaxMarks = 16;
 cudaEvent_t g_ev[kMaxMarks];
 const char* g_evname[kMaxMarks];
@@ -94,8 +94,8 @@ int g_nev = 0;
 bool g_ev_init = false;
 
 void mark_reset() { g_nev = 0; }
-void mark(cudaStream_t st, const char* name) {
-  if (!g_prof || g_nev >= kMaxMarks) return;
+void mark(cudaStream_t st, const char* name, bool dp = true) {
+  if (!g_prof || (g_prof == 2 && !dp) || g_nev >= kMaxMarks) return;
   if (!g_ev_init) {
     for (int k = 0; k < kMaxMarks; ++k) cudaEventCreate(&g_ev[k]);
     g_ev_init = true;
@@ -117,6 +117,7 @@ int ensure_ctx() {
   CK(cudaStreamCreateWithFlags(&g_ctx.side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&g_ctx.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g_ctx.ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&g_ctx.ev_q, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&g_ctx.copy, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&g_ctx.chk, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&g_ctx.ev_chk, cudaEventDisableTiming));
@@ -724,7 +725,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   if (ncand <= 0) return fail("candidate set is empty");
   ArenaScope ws(st, env_int("EKB_WORKSPACE", 1) != 0);  // every DBuf below comes out of the stream's workspace
   mark_reset();
-  mark(st, "start");
+  mark(st, "start", false);
   const bool lb_chunks = share_lb_path(spec, variant, dense, ncand);
   if (nchunk > 0 && !lb_chunks)
     for (int k = 0; k < nchunk; ++k) CK(cudaStreamWaitEvent(st, g_ctx.ev_chunk[ev0 + k], 0));
@@ -826,15 +827,27 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
     // the queries' side of the keys (prepared points, padded copies) and, on the side
     // stream, their envelopes for the reverse bound and the small initialisations
     CK(cudaEventRecord(g_ctx.ev_fork, st));  // the inputs are ordered on st
+    // (resident inputs: the prepared points and padded copies run on the side stream too,
+    // next to the candidates' envelopes, and the key matrix waits for them)
     auto query_prep = [&]() -> int {
+      cudaStream_t qs = nchunk > 0 ? st : g_ctx.side;
       CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_fork, 0));
-      CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr2, g_ctx.side));
-      if (small_inits(g_ctx.side)) return -1;
-      CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
-      CK(lb_qprep(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, L, dqt.as<float2>(), st));
+      if (qs == st) {
+        CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr2, g_ctx.side));
+        if (small_inits(g_ctx.side)) return -1;
+        CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
+      }
+      CK(lb_qprep(spec_mode(spec), dQ, (const long long*)dqoff, (int)nq, L, dqt.as<float2>(), qs));
       if (use_nn2) {
-        CK(nn2_pad(spec->precision, dQ, (const long long*)dqoff, (int)nq, L, pitch2, dqp.p, st));
+        CK(nn2_pad(spec->precision, dQ, (const long long*)dqoff, (int)nq, L, pitch2, dqp.p, qs));
         ++g_launches;
+      }
+      if (qs != st) {
+        CK(cudaEventRecord(g_ctx.ev_q, g_ctx.side));
+        CK(cudaStreamWaitEvent(st, g_ctx.ev_q, 0));
+        CK(envelope(dQ, (const long long*)dqoff, L, (int)nq, win < 0 ? L : win, denvq.as<float2>(), scr2, g_ctx.side));
+        if (small_inits(g_ctx.side)) return -1;
+        CK(cudaEventRecord(g_ctx.ev_join, g_ctx.side));
       }
       return 0;
     };
@@ -865,7 +878,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
         return -1;
       }
     }
-    mark(st, "lb_keys");
+    mark(st, "lb_keys", false);
     // dkeys: the keys per (query, candidate); dskeys: the same in rank order
     if (ncand <= 16384) {
       CK(rank_radix((const float*)dkeys.as<float>(), (int)nq, (int)ncand, dord.as<int>(), st, dskeys.as<float>()));
@@ -895,7 +908,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   } else {
     if (launch_plain(k_identity_order, dim3(1024), dim3(256), 0, st, (int)nq, (int)ncand, dord.as<int>())) return -1;
   }
-  mark(st, "rank");
+  mark(st, "rank", false);
   // 2. cutoff seed: the least exact diagonal upper bound over each query's top-ranked
   //    candidates (one on the Euclidean ranking, whose top candidate minimises that bound
   //    approximately; several on the LB ranking)
@@ -1040,7 +1053,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
       launch_plain(k_nn_final, dim3((unsigned)std::min<long long>(64, (nq + 255) / 256)), dim3(256), 0, st, acc, (int)nq,
                    (int)ncand, (long long*)d_idx, d_dist, (long long*)d_cells, (long long*)d_comp, (long long*)d_ab))
     return -1;
-  mark(st, "reduce");
+  mark(st, "reduce", false);
   return 0;
 }
 
@@ -1735,7 +1748,7 @@ extern "C" {
 
 void ek_set_profiling(int32_t on) {
   std::lock_guard<std::mutex> lk(g_mu);
-  g_prof = on != 0;
+  g_prof = on;
 }
 
 // Device time (ms) between consecutive phase marks of the last profiled call;
