@@ -1454,6 +1454,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   const int eng = choose_engine((int)lq, (int)lq, win < 0 ? (int)lq : win, false);
   if (eng < 0) return fail("query length %lld exceeds this build's engines", (long long)lq);
   const bool share = !profile && (variant == 1 || variant == 2);
+  ArenaScope ws(st, env_int("EKB_WORKSPACE", 1) != 0);
   // numpy pairwise-sum plan for length lq
   std::vector<int2> leaves;
   std::vector<int> ops;
@@ -1634,22 +1635,27 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   }
   // reduce
   const int nb = (int)std::min<long long>(1024, (nwin + 255) / 256);
-  DBuf pd, pi, pc, pa, pcl;
-  if (pd.alloc(8 * nb, st) || pi.alloc(8 * nb, st) || pc.alloc(8 * nb, st) || pa.alloc(8 * nb, st) || pcl.alloc(8 * nb, st))
-    return -1;
+  // five partial arrays of nb entries in one buffer: one copy back
+  DBuf pred;
+  if (pred.alloc(5 * 8 * (size_t)nb, st)) return -1;
+  double* const pd = pred.as<double>();
+  long long* const pi = (long long*)(pd + nb);
+  long long* const pc = pi + nb;
+  long long* const pa = pc + nb;
+  long long* const pcl = pa + nb;
   const int wv = win < 0 ? (int)lq : win;
   if (launch_plain(k_red1_partial, dim3(nb), dim3(256), 0, st, (const double*)dout.as<double>(),
-                   (const int*)dtend.as<int>(), nwin, (int)lq, wv, (int)engine_is_diag(eng), eng_S(eng),
-                   pd.as<double>(), pi.as<long long>(), pc.as<long long>(), pa.as<long long>(), pcl.as<long long>()))
+                   (const int*)dtend.as<int>(), nwin, (int)lq, wv, (int)engine_is_diag(eng), eng_S(eng), pd, pi, pc, pa,
+                   pcl))
     return -1;
-  std::vector<double> hd(nb);
-  std::vector<long long> hi(nb), hc(nb), ha(nb), hcl(nb);
-  CK(cudaMemcpyAsync(hd.data(), pd.p, 8 * nb, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hi.data(), pi.p, 8 * nb, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hc.data(), pc.p, 8 * nb, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(ha.data(), pa.p, 8 * nb, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hcl.data(), pcl.p, 8 * nb, cudaMemcpyDeviceToHost, st));
+  std::vector<long long> hall(5 * (size_t)nb);
+  CK(cudaMemcpyAsync(hall.data(), pred.p, 5 * 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  const double* const hd = reinterpret_cast<const double*>(hall.data());
+  const long long* const hi = hall.data() + nb;
+  const long long* const hc = hi + nb;
+  const long long* const ha = hc + nb;
+  const long long* const hcl = ha + nb;
   double bd = INFINITY;
   long long bo = -1, tc = 0, ta = 0, tcl = 0;
   for (int b = 0; b < nb; ++b) {
