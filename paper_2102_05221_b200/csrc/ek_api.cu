@@ -267,9 +267,9 @@ int inputs_finite(const double* a, long long na, const double* b, long long nb, 
 }
 
 // cut[q] = the IEEE image of c0[q] (a distance: >= +0 or +inf), +0.0 for -0.0 / NaN never occurs
-__global__ void k_cut_from(unsigned long long* cut, const double* c0, long long n) {
+__global__ void k_cut_from(unsigned long long* cut, const double* c0, long long n, double scale = 1.0) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const double v = c0[i];
+    const double v = c0[i] * scale;
     if (v >= 0.0) atomicMin(cut + i, (unsigned long long)__double_as_longlong(v + 0.0));
   }
 }
@@ -914,9 +914,16 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   //    approximately; several on the LB ranking)
   if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the side stream: query envelopes, initialisations
   // a caller's starting cutoffs (ek_nn's second candidate half: the first half's answers)
+#ifdef EKB_TRACE
+  // experiment: start from (a multiple of) the previous call's answers left in d_dist
+  const double dbg_scale = env_int("EKB_DEBUG_CUT0", 0) / 100.0;
+  if (dbg_scale > 0 && !d_cut0) d_cut0 = d_dist;
+#else
+  const double dbg_scale = 0;
+#endif
   if (d_cut0 && share &&
       launch_plain(k_cut_from, dim3((unsigned)((nq + 255) / 256)), dim3(256), 0, st, dcut.as<unsigned long long>(),
-                   d_cut0, (long long)nq))
+                   d_cut0, (long long)nq, dbg_scale > 0 ? dbg_scale : 1.0))
     return -1;
   if (share) {
     // (the LB ranking's top candidates are not the Euclidean nearest: take the best of 16)
@@ -977,7 +984,7 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // 4 + 64 ranks one pair per item, then items of 8 (measured best on C2 before the LB
   // keys).  LB path: items whose pairs all fail their key cost a load and a ballot, so
   // the tail uses full-warp items of 32.
-  const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? env_int("EKB_NN_SEG1", 64) : ka + 64));
+  const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? env_int("EKB_NN_SEG1", 64) : ka + env_int("EKB_NN_SEG1R", 64)));
   // (k_nn2 takes smaller tail items: its survivors are spread over more warps)
   const int K1_lb = env_int("EKB_NN_K1", 1), K2 = one_launch ? env_int("EKB_NN_K2", use_nn2 ? 2 : 4) : 8;
   const NNFn fnB = pick_nn(spec->kind, spec_mode(spec), engB);
@@ -1047,6 +1054,13 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
         return -1;
     }
     mark(st, "nn_fix");
+    if (env_int("EKB_DEBUG_OVF", 0)) {  // overflow counts of the guarded bands (synchronises)
+      int h[4] = {0, 0, 0, 0};
+      cudaMemcpyAsync(h, dcnt.as<int>() + 8, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "guarded-band overflows: first level %d (redone %d), second level %d (redone %d)\n", h[0], h[1],
+              h[2], h[3]);
+    }
   }
   // 4. lexicographic (distance, index) minimum + accounting
   if (launch_plain(k_nn_pick, dim3(148), dim3(256), 0, st, acc) ||

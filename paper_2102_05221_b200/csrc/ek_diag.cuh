@@ -171,6 +171,14 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
   constexpr bool BORDERED = (KIND == K_ERP);
   // the DTW family masks out-of-band diagonals through their cost (+inf offset)
   constexpr bool COST_MASK = (KIND == K_DTW || KIND == K_CDTW || KIND == K_WDTW);
+  // MSM / TWE with VIRT0 (the guarded bands: both virtual diagonals in slot 0 of their lanes):
+  // only slot 0 is masked, through its result: v + 0.0 == v exactly inside the band (v >= +0,
+  // +inf or NaN), v + inf == +inf on a virtual diagonal (or NaN where v is: beyond the
+  // matrix, never selected by an in-band cell).  Every other out-of-band slot lies beyond a
+  // virtual diagonal, starts at +inf and only sees +inf / NaN inputs (as for the DTW family
+  // above).  One FP64 add per lane and double step replaces the two selects per cell of
+  // "upd ? v : INF": these cells are bound by the select (ALU) pipe.
+  constexpr bool RES_MASK = (KIND == K_MSM || KIND == K_TWE) && VIRT0;
   const int lane = threadIdx.x & (W - 1);
   const int dlo = max(-w, 1 - nc), dhi = min(w, nl - 1);
   const int dbase = (dlo - 1) & ~1;  // floor to even, includes the lower virtual diagonal
@@ -205,6 +213,7 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
     }
   }
 
+  const R off0 = upd[0] ? (R)0.0 : INF;  // RES_MASK: slot 0's mask
   int t = 2;
   int I0 = (t + d0) >> 1, J0 = (t - d0) >> 1;
   RowD<KIND, R> xw[H + 1];
@@ -293,6 +302,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
         val[p] = (upd[p] || tb[p] == t) ? v : INF;
       } else if constexpr (COST_MASK) {
         val[p] = v;
+      } else if constexpr (RES_MASK) {
+        val[p] = (p == 0) ? dadd(v, off0) : v;
       } else {
         val[p] = upd[p] ? v : INF;
       }
@@ -318,6 +329,8 @@ __device__ DiagResult diag_pair(const XAcc& X, int nl, const YAcc& Y, int nc, in
       if constexpr (BORDERED) {
         val[p] = (upd[p] || tb[p] == t + 1) ? v : INF;
       } else if constexpr (COST_MASK) {
+        val[p] = v;
+      } else if constexpr (RES_MASK) {
         val[p] = v;
       } else {
         val[p] = upd[p] ? v : INF;

@@ -61,6 +61,18 @@ extern "C" int ek_debug_trace(unsigned long long* out, int n) {
   if (n > 8192 * 8) n = 8192 * 8;
   return (int)cudaMemcpyFromSymbol(out, ekb::g_trace, sizeof(unsigned long long) * n);
 }
+// the long pairs of the k_nn2 launches since the last call (count returned, log reset)
+extern "C" int ek_debug_plog(unsigned long long* out, int max_rows) {
+  unsigned int n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, ekb::g_plog_n, sizeof(n));
+  if (n > 32768u) n = 32768u;
+  if ((int)n > max_rows) n = (unsigned)max_rows;
+  if (n && out) cudaMemcpyFromSymbol(out, ekb::g_plog, sizeof(unsigned long long) * 4 * n);
+  const unsigned int z = 0;
+  cudaMemcpyToSymbol(ekb::g_plog_n, &z, sizeof(z));
+  return (int)n;
+}
 #endif
 
 #ifdef EKB_LIVE

@@ -161,12 +161,16 @@ __device__ __forceinline__ const R* engine_table(R* tab, int len, int lmax, cons
 
 // The band an engine actually runs: guarded engines narrow it to what 32 lanes of P
 // slots hold (the widest w with diag_slots_needed <= 32P).
-template <int ENG>
+template <int ENG, int KIND = K_DTW>
 __device__ __forceinline__ int engine_band(int nl, int nc, int w) {
   if constexpr (engine_guarded(ENG)) {
     constexpr int P = engine_P(ENG);
     int wg = min(w, 16 * P - 2);
     while (wg > 0 && diag_slots_needed(nl, nc, wg) > 32 * P) --wg;
+    // MSM / TWE: the band whose two virtual diagonals both fall in slot 0 of their lanes
+    // (diag_pair's VIRT0: wg + 1 a multiple of P / 2), so only slot 0 is ever masked
+    if constexpr (KIND == K_MSM || KIND == K_TWE)
+      while (wg > 0 && (wg + 1) % (P / 2) != 0) --wg;
     return wg;
   } else {
     return w;
@@ -180,17 +184,21 @@ __device__ __forceinline__ void run_engine(const XAcc& X, int nl, const YAcc& Y,
   if constexpr (engine_guarded(ENG)) {
     // the widest band that fits 32 lanes of P slots; guard the sides it narrows
     constexpr int P = engine_P(ENG);
-    const int wg = engine_band<ENG>(nl, nc, w);
-    if (wg < nl - nc) {  // the final cell would fall outside: redo with the full engine
+    const int wg = engine_band<ENG, KIND>(nl, nc, w);
+    const int dlo_t = max(-w, 1 - nc), dhi_t = min(w, nl - 1);
+    const int dlo_g = max(-wg, 1 - nc), dhi_g = min(wg, nl - 1);
+    const int dbase = (dlo_g - 1) & ~1;
+    // MSM / TWE run the slot-0-masked form only: its alignment holds whenever the series are
+    // longer than the band (what a guarded engine is chosen for); anything else is redone
+    constexpr bool V0 = (KIND == K_MSM || KIND == K_TWE);
+    const bool aligned = !V0 || (wg > 0 && dlo_g - 1 == dbase && (dhi_g + 1 - dbase) % P == 0);
+    if (wg < nl - nc || !aligned) {  // the final cell would fall outside: redo with the full engine
       cost = __longlong_as_double(0x7ff8000000000000LL);
       tend = -1;
       return;
     }
-    const int dlo_t = max(-w, 1 - nc), dhi_t = min(w, nl - 1);
-    const int dlo_g = max(-wg, 1 - nc), dhi_g = min(wg, nl - 1);
-    const int dbase = (dlo_g - 1) & ~1;
     const unsigned guard = (dlo_g > dlo_t ? 1u : 0u) | (dhi_g < dhi_t ? 1u << ((dhi_g - dbase) / P) : 0u);
-    DiagResult r = diag_pair<KIND, MODE, P, SHARED_CUT, true>(X, nl, Y, nc, wg, cut, cutp, prm, ld, guard);
+    DiagResult r = diag_pair<KIND, MODE, P, SHARED_CUT, true, V0>(X, nl, Y, nc, wg, cut, cutp, prm, ld, guard);
     cost = r.cost;
     tend = r.t_end;
     if (r.ovf) {
@@ -770,7 +778,7 @@ __global__ void __launch_bounds__(128, nn_minb(KIND, ENG, MODE)) k_nn(const doub
         }
         if (share) cut = fmin(cut, fmin(cost, ld_cut(cutbits + q)));
       }
-      const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, engine_band<ENG>(nl, nc, w), tend, KIND == K_ERP ? 0 : 1) : 0;
+      const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, engine_band<ENG, KIND>(nl, nc, w), tend, KIND == K_ERP ? 0 : 1) : 0;
       if (lane == 0) {
         if (tend < 0) {  // guarded band overflowed: the pair is redone by k_nn_fix
           ovf_list[atomicAdd(ovf_count, 1)] = make_int2(q, c);
@@ -842,7 +850,7 @@ __global__ void __launch_bounds__(128) k_nn_fix(const double* __restrict__ Q, co
     int tend;
     run_engine<KIND, MODE, ENG, true>(SmemSeriesT<R>{X, nl}, nl, SmemSeriesT<R>{Y, nc}, nc, w, cut, cutbits + q, tabe, tablen,
                                       pp, ld, cost, tend);
-    const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, engine_band<ENG>(nl, nc, w), tend, KIND == K_ERP ? 0 : 1) : 0;
+    const int cells = tend > 0 ? warp_cells<ENG>(nl, nc, engine_band<ENG, KIND>(nl, nc, w), tend, KIND == K_ERP ? 0 : 1) : 0;
     if (lane == 0) {
       if (tend < 0) {  // a guarded redo overflowed too: the next, wider engine takes it
         ovf_list[atomicAdd(ovf_count, 1)] = make_int2(q, c);

@@ -29,6 +29,12 @@
 
 namespace ekb {
 
+#ifdef EKB_TRACE
+// long pairs of the last k_nn2 launch: (start ns, end ns, query, key / threshold * 1e6, rank-ordered claim index)
+__device__ unsigned long long g_plog[32768 * 4];
+__device__ unsigned int g_plog_n;
+#endif
+
 constexpr int kPadG = 96;  // elements of padding on each side of a padded series (>= 92, see below)
 
 // dst[s * pitch + kPadG + k], k in [-kPadG, L + kPadG): the series (rounded to R), 0.0 before
@@ -133,6 +139,9 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
     return -1;
   };
 
+#ifdef EKB_TRACE
+  unsigned long long tr_ratio = 0, tr_pst = 0, tr_prat = 0;
+#endif
   auto next_pair = [&](int& oq, int& oc) -> bool {
     for (;;) {
       while (todo) {
@@ -146,6 +155,9 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
         if (!warp_lb_reverse<MODE>(CP + (long long)c * pitch + kPadG, envq + (long long)it_q * lmax, L,
                                    lb_scale(thr)))
           continue;
+#ifdef EKB_TRACE
+        tr_ratio = (unsigned long long)(1e6 * (double)k / thr);
+#endif
         oq = it_q;
         oc = c;
         return true;
@@ -210,6 +222,22 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
     const R r_ = __shfl_sync(FULL, res, 16 * h + lf);
     const R ch = __shfl_sync(FULL, cut, 16 * h);
     const int cells = warp_cells<E_DIAG4>(L, L, w, te, 1);
+#ifdef EKB_TRACE
+    {
+      const unsigned long long ps = __shfl_sync(FULL, tr_pst, 16 * h), pr = __shfl_sync(FULL, tr_prat, 16 * h);
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (lane == 0 && te >= 400) {
+        const unsigned k = atomicAdd(&g_plog_n, 1u);
+        if (k < 32768) {
+          g_plog[k * 4 + 0] = ps;
+          g_plog[k * 4 + 1] = now;
+          g_plog[k * 4 + 2] = ((unsigned long long)q_ << 32) | (unsigned)te;
+          g_plog[k * 4 + 3] = pr;
+        }
+      }
+    }
+#endif
     const double cq = ld_cut(cutbits + q_);
     if (lane == 0) {
       double cost = EKB_INF;
@@ -312,6 +340,10 @@ __global__ void __launch_bounds__(128, EKB_NN2_MINB)
 #ifdef EKB_TRACE
       ++tr_pairs;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_last_pair));
+      if (half == h) {
+        tr_pst = tr_last_pair;
+        tr_prat = tr_ratio;
+      }
 #endif
       const double cq = ld_cut(cutbits + q);
       if (half == h) {
