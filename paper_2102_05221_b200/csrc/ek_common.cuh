@@ -180,8 +180,22 @@ EKB_DI float msm_alt_fma(bool between, float c, float dother, float de) {
   const float m = (dother < de) ? dother : de;
   return __fmaf_rn(m, between ? 0.f : 1.f, c);
 }
+// The factor from the sign bits without a compare and a select: nb = 1 when the point is NOT
+// between (0 / 1, one logic op on the two sign bits), and the factor's high word
+// nb * 0x3ff00000 comes from the FMA pipe's integer multiply-add, which these cells leave
+// idle while the select (ALU) pipe bounds them.
+EKB_DI double msm_alt_fma_nb(int nb, double c, double dother, double de) {
+  const double m = (dother < de) ? dother : de;
+  int hi;
+  asm("mad.lo.s32 %0, %1, 0x3ff00000, 0;" : "=r"(hi) : "r"(nb));
+  return __fma_rn(m, __hiloint2double(hi, 0), c);
+}
+EKB_DI float msm_alt_fma_nb(int nb, float c, float dother, float de) {
+  const float m = (dother < de) ? dother : de;
+  return __fmaf_rn(m, (float)nb, c);
+}
 #ifndef EKB_MSM_FMA
-#define EKB_MSM_FMA 1
+#define EKB_MSM_FMA 2  // 2: msm_alt_fma_nb, 1: msm_alt_fma, 0: msm_alt
 #endif
 
 // One cell.  D, T, L are the dependency values; the result is the reference's
@@ -219,8 +233,14 @@ EKB_DI R cell(R D, R T, R L, const RowD<KIND, R>& r, const ColD<KIND, R>& c, con
     const int se = sign_bit(e);
     bool brow = se != r.s;  // l_{i-1}<=l_i<=c_j or l_{i-1}>=l_i>=c_j (see msm_alt)
     bool bcol = se == c.s;  // l_i<=c_j<=c_{j-1} or l_i>=c_j>=c_{j-1}
-    R ar = EKB_MSM_FMA ? msm_alt_fma(brow, (R)p.msm_c, r.dr, de) : msm_alt(brow, (R)p.msm_c, r.dr, de);
-    R ac = EKB_MSM_FMA ? msm_alt_fma(bcol, (R)p.msm_c, c.dc, de) : msm_alt(bcol, (R)p.msm_c, c.dc, de);
+    R ar, ac;
+    if constexpr (EKB_MSM_FMA == 2) {  // not between: the row test's signs equal, the column test's differ
+      ar = msm_alt_fma_nb(se ^ r.s ^ 1, (R)p.msm_c, r.dr, de);
+      ac = msm_alt_fma_nb(se ^ c.s, (R)p.msm_c, c.dc, de);
+    } else {
+      ar = EKB_MSM_FMA ? msm_alt_fma(brow, (R)p.msm_c, r.dr, de) : msm_alt(brow, (R)p.msm_c, r.dr, de);
+      ac = EKB_MSM_FMA ? msm_alt_fma(bcol, (R)p.msm_c, c.dc, de) : msm_alt(bcol, (R)p.msm_c, c.dc, de);
+    }
     R v = dadd(D, de);
     v = dmin_ref(v, dadd(T, ar));
     return dmin_ref(v, dadd(L, ac));
