@@ -1493,13 +1493,34 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   const int nseg = (int)((nref + kPrefixSeg - 1) / kPrefixSeg);
   const int st_wpb = 4;
   const size_t st_smem = sizeof(double) * (size_t)st_wpb * (nl_ + 16);
+  // With the LB pass, what only that pass needs (the prefix sums, the query's envelope and
+  // test order) runs on the side stream next to the seed bounds and the seed DPs, which
+  // leave most of the GPU idle (phase A is a handful of full-length DPs), and is joined
+  // before the pass.
+  cudaStream_t ss = use_lb ? g_ctx.side : st;
+  // the query, normalised once (search.py:181-182): one warp, ~35 us at 1,024 points, so with
+  // the LB pass it leads the side stream while the sampled windows' statistics run on st
+  DBuf dqn, denv, denvs, dzero, dkeys, dlbo;
+  if (dqn.alloc(sizeof(double) * (size_t)lq, st)) return -1;
+  if (use_lb) {
+    CK(cudaEventRecord(g_ctx.ev_fork, st));  // the inputs and the plan are ordered on st
+    CK(cudaStreamWaitEvent(ss, g_ctx.ev_fork, 0));
+  }
+  auto norm_query = [&](cudaStream_t qs) -> int {
+    return launch_plain(k_subseq_query<0>, dim3(1), dim3(32), sizeof(double) * ((size_t)lq + nl_ + 16), qs, dq,
+                        (int)lq, (int)normalize, plan, dqn.as<double>());
+  };
+  if (use_lb) {
+    if (norm_query(ss)) return -1;
+    CK(cudaEventRecord(g_ctx.ev_q, ss));
+  }
   if (normalize && use_lb) {
     if (dstats.alloc(sizeof(double2) * (size_t)nwin, st) || dplocal.alloc(sizeof(double) * 6 * (size_t)nref, st) ||
         dpseg.alloc(sizeof(double) * 6 * (size_t)nseg, st))
       return -1;
-    if (launch_plain(k_prefix_dd<0>, dim3((unsigned)nseg), dim3(256), 0, st, dref, (long long)nref,
+    if (launch_plain(k_prefix_dd<0>, dim3((unsigned)nseg), dim3(256), 0, ss, dref, (long long)nref,
                      dplocal.as<double>(), dpseg.as<double>(), nseg) ||
-        launch_plain(k_prefix_dd_segs<0>, dim3(1), dim3(256), 0, st, dpseg.as<double>(), nseg))
+        launch_plain(k_prefix_dd_segs<0>, dim3(1), dim3(256), 0, ss, dpseg.as<double>(), nseg))
       return -1;
   } else if (normalize) {
     if (dstats.alloc(sizeof(double2) * (size_t)nwin, st)) return -1;
@@ -1514,12 +1535,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
     }
   }
   const double2* wst = normalize ? (const double2*)dstats.as<double2>() : nullptr;
-  // the query, normalised once (search.py:181-182)
-  DBuf dqn, denv, denvs, dzero, dkeys, dlbo;
-  if (dqn.alloc(sizeof(double) * (size_t)lq, st)) return -1;
-  if (launch_plain(k_subseq_query<0>, dim3(1), dim3(32), sizeof(double) * ((size_t)lq + nl_ + 16), st, dq, (int)lq,
-                   (int)normalize, plan, dqn.as<double>()))
-    return -1;
+  if (!use_lb && norm_query(st)) return -1;
   if (launch_plain(k_fill_u64, dim3(1), dim3(32), 0, st, dcut.as<unsigned long long>(), 1LL, 0x7ff0000000000000ULL))
     return -1;
   mark(st, "win_stats");
@@ -1535,6 +1551,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                      st, dref, (int)lq, (const long long*)nullptr, stride, nsamp, (const int*)nullptr, plan,
                      dstats.as<double2>()))
       return -1;
+    if (use_lb) CK(cudaStreamWaitEvent(st, g_ctx.ev_q, 0));  // the normalised query (side stream)
     if (launch_plain(get_subseq_ub(spec->cost_mode), dim3((unsigned)((nsamp + 3) / 4)), dim3(128), 0, st,
                      (const double*)dqn.as<double>(), (int)lq, dref, stride, (int)normalize, wst, nsamp,
                      dukeys.as<float>(), dcut.as<unsigned long long>()))
@@ -1558,27 +1575,33 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   // LB_Keogh envelope of the query (search.py:185-187) and the test order
   const float2* env = nullptr;
   if (use_lb) {
+    // (buffers allocated in st's order; the side stream's launches follow ev_q, recorded after
+    // every allocation that precedes it; these few are made before any use, which the
+    // workspace makes immediate and a stream-ordered allocation orders by the event below)
     if (denv.alloc(sizeof(float2) * (size_t)lq, st) || dzero.alloc(8, st)) return -1;
-    CK(cudaMemsetAsync(dzero.p, 0, 8, st));
     void* scr = nullptr;
     if (env_scratch_bytes((int)lq, false)) {
       if (denvs.alloc(env_scratch_bytes((int)lq, false), st)) return -1;
       scr = denvs.p;
     }
+    if (dkeys.alloc(sizeof(float) * (size_t)lq, st) || dlbo.alloc(sizeof(int) * (size_t)lq, st)) return -1;
+    CK(cudaEventRecord(g_ctx.ev_chk, st));
+    CK(cudaStreamWaitEvent(ss, g_ctx.ev_chk, 0));
+    CK(cudaMemsetAsync(dzero.p, 0, 8, ss));
     CK(envelope((const double*)dqn.as<double>(), (const long long*)dzero.as<long long>(), (int)lq, 1,
-                win < 0 ? (int)lq : win, denv.as<float2>(), scr, st));
+                win < 0 ? (int)lq : win, denv.as<float2>(), scr, ss));
     ++g_launches;
     env = denv.as<float2>();
     // positions by decreasing envelope excess (k_rank_sort on one row)
-    if (dkeys.alloc(sizeof(float) * (size_t)lq, st) || dlbo.alloc(sizeof(int) * (size_t)lq, st)) return -1;
-    if (launch_plain(k_env_keys<0>, dim3((unsigned)((lq + 255) / 256)), dim3(256), 0, st, env, (int)lq,
+    if (launch_plain(k_env_keys<0>, dim3((unsigned)((lq + 255) / 256)), dim3(256), 0, ss, env, (int)lq,
                      dkeys.as<float>()))
       return -1;
     int np2 = 1;
     while (np2 < lq) np2 <<= 1;
-    if (launch_plain(k_rank_sort, dim3(1), dim3(1024), (size_t)np2 * 8, st, (const float*)dkeys.as<float>(), (int)lq,
+    if (launch_plain(k_rank_sort, dim3(1), dim3(1024), (size_t)np2 * 8, ss, (const float*)dkeys.as<float>(), (int)lq,
                      np2, dlbo.as<int>()))
       return -1;
+    CK(cudaEventRecord(g_ctx.ev_join, ss));
   }
   mark(st, "envelope");
   const SubseqFn fn = get_subseq(spec->cost_mode, eng);
@@ -1607,6 +1630,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
       return -1;
   }
   mark(st, "subseq_phaseA");
+  if (env) CK(cudaStreamWaitEvent(st, g_ctx.ev_join, 0));  // the side stream: prefix sums, envelope, test order
   if (env) {
     // phase B1: LB_Keogh test of every window (lane per window); B2: DP of the survivors
     DBuf dsurv, dsurvlb, dns;
