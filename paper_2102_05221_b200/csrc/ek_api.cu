@@ -1469,19 +1469,42 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   if (eng < 0) return fail("query length %lld exceeds this build's engines", (long long)lq);
   const bool share = !profile && (variant == 1 || variant == 2);
   ArenaScope ws(st, env_int("EKB_WORKSPACE", 1) != 0);
-  // numpy pairwise-sum plan for length lq
-  std::vector<int2> leaves;
-  std::vector<int> ops;
-  np_plan_build(0, (int)lq, leaves, ops);
-  DBuf dleaves, dops, dcut, dout, dtend, dcnt;
-  if (dleaves.alloc(sizeof(int2) * leaves.size(), st) || dops.alloc(sizeof(int) * ops.size(), st) ||
-      dcut.alloc(8, st) || dout.alloc(sizeof(double) * (size_t)nwin, st) || dtend.alloc(sizeof(int) * (size_t)nwin, st) ||
+  // numpy pairwise-sum plan for length lq: built and uploaded once per length, kept on the
+  // device (a few KB; the upload from pageable memory is a synchronous staging copy)
+  struct PlanDev {
+    int2* leaves = nullptr;
+    int* ops = nullptr;
+    int nleaves = 0, nops = 0;
+  };
+  static std::map<long long, PlanDev> plans;
+  PlanDev& pd_ = plans[lq];
+  if (!pd_.leaves) {
+    if (plans.size() > 64) {  // (lengths come and go: drop the idle plans)
+      cudaDeviceSynchronize();
+      for (auto& kv : plans) {
+        if (kv.second.leaves) cudaFree(kv.second.leaves);
+        if (kv.second.ops) cudaFree(kv.second.ops);
+      }
+      plans.clear();
+    }
+    PlanDev& nd = plans[lq];
+    std::vector<int2> leaves;
+    std::vector<int> ops;
+    np_plan_build(0, (int)lq, leaves, ops);
+    CK(cudaMalloc((void**)&nd.leaves, sizeof(int2) * std::max<size_t>(1, leaves.size())));
+    CK(cudaMalloc((void**)&nd.ops, sizeof(int) * std::max<size_t>(1, ops.size())));
+    CK(cudaMemcpy(nd.leaves, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(nd.ops, ops.data(), sizeof(int) * ops.size(), cudaMemcpyHostToDevice));
+    nd.nleaves = (int)leaves.size();
+    nd.nops = (int)ops.size();
+  }
+  const PlanDev& pl = plans[lq];
+  DBuf dcut, dout, dtend, dcnt;
+  if (dcut.alloc(8, st) || dout.alloc(sizeof(double) * (size_t)nwin, st) || dtend.alloc(sizeof(int) * (size_t)nwin, st) ||
       dcnt.alloc(32, st))
     return -1;
-  CK(cudaMemcpyAsync(dleaves.p, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dops.p, ops.data(), sizeof(int) * ops.size(), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(dcnt.p, 0, 32, st));
-  NpPlan plan{dleaves.as<int2>(), (int)leaves.size(), dops.as<int>(), (int)ops.size()};
+  NpPlan plan{pl.leaves, pl.nleaves, pl.ops, pl.nops};
   mark_reset();
   mark(st, "start");
   const int nl_ = plan.nleaves;
@@ -1686,11 +1709,12 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                    (const int*)dtend.as<int>(), nwin, (int)lq, wv, (int)engine_is_diag(eng), eng_S(eng), pd, pi, pc, pa,
                    pcl))
     return -1;
-  std::vector<long long> hall(5 * (size_t)nb);
-  CK(cudaMemcpyAsync(hall.data(), pred.p, 5 * 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
+  static long long* hall = nullptr;  // page-locked landing buffer of the partials (5 x 1024 entries at most)
+  if (!hall) CK(cudaHostAlloc((void**)&hall, 5 * 8 * 1024, cudaHostAllocDefault));
+  CK(cudaMemcpyAsync(hall, pred.p, 5 * 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  const double* const hd = reinterpret_cast<const double*>(hall.data());
-  const long long* const hi = hall.data() + nb;
+  const double* const hd = reinterpret_cast<const double*>(hall);
+  const long long* const hi = hall + nb;
   const long long* const hc = hi + nb;
   const long long* const ha = hc + nb;
   const long long* const hcl = ha + nb;
