@@ -377,11 +377,11 @@ def time_steps(r, steps, warmup, flush):
         torch.cuda.synchronize()
         full.append(phase_times(r.L))
     r.L.ek_set_profiling(0)
-    for p in phases:  # the DP kernels' times stay the timed steps' own
-        for k in full[0]:
-            if k not in p:
-                p[k] = float(np.mean([f[k] for f in full]))
-    phases = [{k: p[k] for k in full[0]} for p in phases]
+    # the DP kernels' times stay the timed steps' own (their bracketing marks are recorded in
+    # mode 2 too); every other phase comes from the full breakdown
+    dp = ("nn_phase", "nn_fix", "triangle", "subseq_phase")
+    phases = [{k: (p[k] if k.startswith(dp) and k in p else float(np.mean([f[k] for f in full]))) for k in full[0]}
+              for p in phases]
     step_ms = [a.elapsed_time(b) for a, b in ev]
     return step_ms, phases, cells, launches, wall
 

@@ -1506,7 +1506,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   CK(cudaMemsetAsync(dcnt.p, 0, 32, st));
   NpPlan plan{pl.leaves, pl.nleaves, pl.ops, pl.nops};
   mark_reset();
-  mark(st, "start");
+  mark(st, "start", false);
   const int nl_ = plan.nleaves;
   const bool use_lb = share && lq * 5 * sizeof(double) <= 200 * 1024;
   // z-normalisation statistics: with the LB pass, double-double prefix sums for its
@@ -1561,7 +1561,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
   if (!use_lb && norm_query(st)) return -1;
   if (launch_plain(k_fill_u64, dim3(1), dim3(32), 0, st, dcut.as<unsigned long long>(), 1LL, 0x7ff0000000000000ULL))
     return -1;
-  mark(st, "win_stats");
+  mark(st, "win_stats", false);
   // cutoff seed: exact diagonal bounds of sampled windows; the best few run first (phase A)
   DBuf dseed, dukeys, dsord;
   long long ns = 0;
@@ -1594,7 +1594,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
       return -1;
     }
   }
-  mark(st, "seed_bounds");
+  mark(st, "seed_bounds", false);
   // LB_Keogh envelope of the query (search.py:185-187) and the test order
   const float2* env = nullptr;
   if (use_lb) {
@@ -1669,7 +1669,7 @@ static int subseq_dev_impl(const ek_spec* spec, int32_t variant, const double* d
                           dtend.as<int>(), dsurv.as<long long>(), dsurvlb.as<float>(), dns.as<int>(),
                           dcnt.as<int>() + 2))
       return -1;
-    mark(st, "subseq_lb");
+    mark(st, "subseq_lb", false);
     if (normalize &&  // exact statistics of the survivors for their DP
         launch_plain(k_win_stats_list<0>, dim3((unsigned)(g_ctx.nsm * 8)), dim3(32 * st_wpb), st_smem, st, dref,
                      (int)lq, (const long long*)dsurv.as<long long>(), 0LL, nwin, (const int*)dns.as<int>(), plan,
