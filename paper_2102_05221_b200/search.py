@@ -268,7 +268,7 @@ def subsequence_search(query, reference, cfg: SearchConfig):
     if cfg.precision != "float64":
         raise SpecError("subsequence search runs in float64 only")
     query = as_series(query)
-    reference = as_series(reference)
+    reference = as_series(reference, finite_on_device=True)  # the library validates the uploaded stream
     lq = len(query)
     if lq > len(reference):
         raise DimensionError(f"query length {lq} exceeds reference length {len(reference)}")
@@ -300,7 +300,7 @@ def subsequence_profile(query, reference, spec: DistanceSpec, normalize: bool = 
     if spec.kind not in ("dtw", "cdtw"):
         raise SpecError("subsequence search supports dtw and cdtw only")
     query = as_series(query)
-    reference = as_series(reference)
+    reference = as_series(reference, finite_on_device=True)  # the library validates the uploaded stream
     lq = len(query)
     if lq > len(reference):
         raise DimensionError(f"query length {lq} exceeds reference length {len(reference)}")

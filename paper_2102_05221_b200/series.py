@@ -16,14 +16,19 @@ import numpy as np
 from .errors import DegenerateInputError, EmptyDatasetError, ParseError
 
 
-def as_series(values) -> np.ndarray:
-    """Contiguous 1-D float64 array, length >= 1, all finite; ValueError otherwise."""
+def as_series(values, finite_on_device: bool = False) -> np.ndarray:
+    """Contiguous 1-D float64 array, length >= 1, all finite; ValueError otherwise.
+
+    ``finite_on_device``: the caller hands the array to a library entry that checks
+    finiteness on the GPU after the upload and reports the same ValueError (ek_subseq,
+    ek_subseq_profile: csrc/ek_api.cu inputs_finite), so a long stream is not scanned twice.
+    """
     arr = np.ascontiguousarray(values, dtype=np.float64)
     if arr.ndim != 1:
         raise ValueError(f"time series must be 1-D, got shape {arr.shape}")
     if arr.size < 1:
         raise ValueError("time series must contain at least one value")
-    if not np.isfinite(arr).all():
+    if not (finite_on_device and arr.size >= 4096) and not np.isfinite(arr).all():
         raise ValueError("time series values must all be finite")
     return arr
 

@@ -330,6 +330,13 @@ def test_nonfinite_inputs_raise(gpu, rng, bad):
     ref[50] = bad
     with pytest.raises(ValueError, match="must all be finite"):
         gpu.subsequence_search(Q[0], ref, gpu.SearchConfig(spec=spec))
+    # a long stream is validated on the device only (as_series(finite_on_device=True))
+    long_ref = rng.normal(size=6000)
+    long_ref[4321] = bad
+    with pytest.raises(ValueError, match="must all be finite"):
+        gpu.subsequence_search(Q[0], long_ref, gpu.SearchConfig(spec=spec))
+    with pytest.raises(ValueError, match="must all be finite"):
+        gpu.subsequence_profile(Q[0], long_ref, spec)
     # the library stays usable afterwards
     idx = gpu.nn_batch(spec, "eapruned", Q, C[:4])[0]
     assert idx.shape == (3,)
