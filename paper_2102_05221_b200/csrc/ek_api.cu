@@ -1370,6 +1370,11 @@ static int pairwise_dev_impl(const ek_spec* spec, int32_t variant, const double*
     const int slot = series_slot(max_len, engine_pad(eng));
     tsmem = elem_size(spec) * ((size_t)wpb * (32 / engine_W(eng)) * 2 * slot + 2 * ((size_t)max_len + kTabPad) + 1);
   }
+  // equal lengths on the half-warp diagonal engine: compact pads (Params.compact_pad)
+  if (equal_len && eng == E_DIAG4H && env_int("EKB_COMPACT_PAD", 1) != 0) {
+    tp.compact_pad = 40;
+    tsmem = elem_size(spec) * (size_t)wpb * 2 * 2 * series_slot(max_len, tp.compact_pad);
+  }
   if (launch_persistent(tf, 32 * wpb, tsmem, st, np,
                         d_series, (const long long*)d_off, (const int*)d_len, (int)n, win, (int)max_len, tp, d_D,
                         plo, phi, d_vec, dtot.as<unsigned long long>(), dcnt.as<int>()))

@@ -51,6 +51,12 @@ struct Params {
   // k_triangle on equal lengths with a row-stripe engine that reads an |i-j| table (WDTW,
   // TWE): one table per block instead of one per pair slot (every pair has the same one)
   int shared_tab;
+  // k_triangle on equal lengths with the half-warp diagonal engine (E_DIAG4H): pads of this
+  // many elements around each staged series instead of the engine's general pad (0 = that).
+  // 16 lanes x P = 4 with series of one length n read indices in [-32, n + 30] only
+  // (diag_pair: i = (t + d) / 2, t <= 2n - 2 at the last load, |d| <= 62), so 40 elements
+  // do, against the 72 that unequal lengths need (C3 ERP: 4 -> 5 resident blocks).
+  int compact_pad;
 };
 
 // Params for one pair whose longest series has length m.

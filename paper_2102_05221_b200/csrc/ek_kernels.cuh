@@ -365,9 +365,14 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
     // two pairs per claim, one per half-warp, in lockstep when their shapes match; a pair
     // of different shapes runs in two passes with both halves on the same pair
     const int half = (threadIdx.x >> 4) & 1, hl = threadIdx.x & 15;
-    R* Xh = X + half * (wst / 2);  // each half: [X][Y][|i-j| table (unless shared)]
-    R* Yh = Xh + series_slot(lmax, PAD);
-    R* tabh = Yh - PAD + series_slot(lmax, PAD);
+    // each half: [X][Y][|i-j| table (unless shared)]; equal lengths on the diagonal engine:
+    // compact pads (Params.compact_pad), no table
+    const bool cpad = engine_is_diag(ENG) && prm.compact_pad > 0;
+    const int pad = cpad ? prm.compact_pad : PAD;
+    const int hst = cpad ? 2 * series_slot(lmax, pad) : wst / 2;
+    R* Xh = cpad ? (R*)smem + (wib * 2 + half) * hst + pad : X + half * hst;
+    R* Yh = Xh + series_slot(lmax, pad);
+    R* tabh = Yh - pad + series_slot(lmax, pad);
     for (;;) {
       long long p = 0;
       if (lane == 0) p = plo + (long long)atomicAdd((unsigned long long*)counter, 2ULL);
@@ -395,8 +400,8 @@ __global__ void __launch_bounds__(128) k_triangle(const double* __restrict__ ser
         if (w >= nl - nc) {  // the same for both halves (same shape)
           const Params pp = pair_params(prm, nl);
           __syncwarp();
-          stage_series<KIND, R, 16>(Xh, series + off[s], nl, PAD);
-          stage_series<KIND, R, 16>(Yh, series + off[t], nc, PAD);
+          stage_series<KIND, R, 16>(Xh, series + off[s], nl, pad);
+          stage_series<KIND, R, 16>(Yh, series + off[t], nc, pad);
           const int tablen = max(nl, nc) + 1;
           const R* tabe = shtab ? btab : engine_table<KIND, ENG>(tabh, tablen, lmax, pp);
           __syncwarp();
