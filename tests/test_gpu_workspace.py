@@ -94,3 +94,20 @@ def test_workspace_subsequence_repeat(gpu):
         got = ekb.subsequence_search(q, stream, SearchConfig(spec=spec, variant="eapruned", normalize=True))[:2]
         want = eko.subsequence(spec, "eapruned", q, stream, True, chunk=512, threads=4)[:2]
         assert got == want, (n, lq)
+
+
+def test_subsequence_plan_cache_eviction(gpu):
+    """More query lengths than the per-length plan cache keeps (64): the cache is dropped and
+    rebuilt, and the answers stay the oracle's."""
+    import paper_2102_05221_b200 as ekb
+    from paper_2102_05221_b200 import SearchConfig
+
+    rng = np.random.default_rng(23)
+    stream = np.cumsum(rng.standard_normal(1200))
+    for lq in list(range(8, 80)) + [8, 40, 79]:
+        q = np.cumsum(rng.standard_normal(lq))
+        spec = ekb.DistanceSpec(kind="cdtw", window=max(1, lq // 10))
+        got = ekb.subsequence_search(q, stream, SearchConfig(spec=spec, variant="eapruned", normalize=True))[:2]
+        if lq % 9 == 0 or lq in (8, 79):
+            want = eko.subsequence(spec, "eapruned", q, stream, True, chunk=512, threads=4)[:2]
+            assert got == want, lq
