@@ -984,7 +984,9 @@ static int nn_dev_impl(const ek_spec* spec, int32_t variant, const double* dQ, c
   // 4 + 64 ranks one pair per item, then items of 8 (measured best on C2 before the LB
   // keys).  LB path: items whose pairs all fail their key cost a load and a ballot, so
   // the tail uses full-warp items of 32.
-  const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? env_int("EKB_NN_SEG1", 64) : ka + env_int("EKB_NN_SEG1R", 64)));
+  // (ranked path: measured on C4, MSM 72.9 ms at 32 against 73.8 at 64, TWE 32.9 ms at 8 against 34.1 at 64)
+  const int seg1r_default = kind_tag(spec->kind) == K_TWE ? 8 : kind_tag(spec->kind) == K_MSM ? 32 : 64;
+  const int kb1 = (int)std::min<int64_t>(ncand, (one_launch ? env_int("EKB_NN_SEG1", 64) : ka + env_int("EKB_NN_SEG1R", seg1r_default)));
   // (k_nn2 takes smaller tail items: its survivors are spread over more warps)
   const int K1_lb = env_int("EKB_NN_K1", 1), K2 = one_launch ? env_int("EKB_NN_K2", use_nn2 ? 2 : 4) : 8;
   const NNFn fnB = pick_nn(spec->kind, spec_mode(spec), engB);
