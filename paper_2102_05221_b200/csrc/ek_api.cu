@@ -160,11 +160,12 @@ struct ArenaScope {
     Arena& a = g_arenas[st];
     if (a.want > a.cap) {
       const size_t cap = a.want + a.want / 8;
-      // plain cudaMalloc / cudaFree: both synchronise the device, so no stream still uses the old block
-      if (a.base) cudaFree(a.base);
+      // stream-ordered on the workspace's own stream: everything that used the old block was
+      // enqueued on it (or joined back into it) before, and nothing synchronises the device
+      if (a.base) cudaFreeAsync(a.base, st);
       a.base = nullptr;
       a.cap = 0;
-      if (cudaMalloc((void**)&a.base, cap) == cudaSuccess) a.cap = cap;
+      if (cudaMallocAsync((void**)&a.base, cap, st) == cudaSuccess) a.cap = cap;
       else cudaGetLastError();
     }
     a.off = 0;
